@@ -1,0 +1,172 @@
+/*
+ * hkv_b200.h — C-ABI of the B200-native cache-semantic hash table.
+ *
+ * This is the drop-in boundary for the reference's hot path,
+ * `cachekv.CacheTable` (/root/reference/pkg/src/cachekv/table.py:138-1305).
+ * The reference has no FFI (pure Python on numpy); each entry point below
+ * replaces one reference method, cited per function.  The Python mirror of
+ * the reference class (paper_2603_17168_b200/table.py) binds these symbols
+ * with ctypes; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - Every array argument is a device-accessible pointer (HBM, or mapped
+ *    pinned host memory), C-contiguous, owned by the caller.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    asynchronous unless documented as synchronising.
+ *  - Return value: HKV_OK or an hkv_status; hkv_last_error() gives the text.
+ *    Usage errors are detected on the host before any launch (shapes,
+ *    policy/score mismatch, cursor range).  Reserved-sentinel keys are
+ *    detected on the device: the offending batch performs no mutation and the
+ *    table's device error latch is set (read it with hkv_device_error).
+ *  - Keys are uint64 (EMPTY = ~0, LOCKED = ~0-1 reserved), values float32
+ *    rows of value_dim, scores uint64.
+ */
+#ifndef HKV_B200_H
+#define HKV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hkv_table hkv_table;
+typedef void *hkv_stream; /* cudaStream_t */
+
+enum hkv_status {
+    HKV_OK = 0,
+    HKV_EINVAL = 1,  /* usage error -> ValueError in the Python mirror */
+    HKV_ECUDA = 2,   /* CUDA runtime error */
+    HKV_ENOMEM = 3,  /* device / pinned host allocation failed */
+};
+
+enum hkv_mode { HKV_MODE_SINGLE = 0, HKV_MODE_DUAL = 1 };            /* table.py:63-65 */
+enum hkv_policy {                                                     /* scoring.py:27-32 */
+    HKV_LRU = 0, HKV_LFU = 1, HKV_EPOCH_LRU = 2, HKV_EPOCH_LFU = 3, HKV_CUSTOMIZED = 4
+};
+enum hkv_outcome {                                                    /* table.py:68-75 */
+    HKV_INSERTED = 0, HKV_UPDATED = 1, HKV_REJECTED = 2, HKV_EVICTED = 3,
+    HKV_FOUND = 4, HKV_NOTFOUND = 5, HKV_ERASED = 6
+};
+enum hkv_upsert_op { HKV_OP_INSERT_OR_ASSIGN = 0, HKV_OP_FIND_OR_INSERT = 1 };
+enum hkv_device_error_bits { HKV_DERR_SENTINEL_KEY = 1 };
+
+/* TableConfig (table.py:94-131).  Validation errors mirror table.py:108-127. */
+typedef struct {
+    int64_t capacity;          /* positive multiple of 128, power-of-two bucket count */
+    int64_t value_dim;         /* >= 1 */
+    int32_t mode;              /* hkv_mode */
+    int32_t score_policy;      /* hkv_policy */
+    int64_t fast_tier_budget;  /* buckets whose values live in HBM; -1 = all (store.py:40-63) */
+    int32_t digest_filter;     /* 1 = digest-accelerated probe; 0 = ablation (compare all slots) */
+    int32_t admit_ties_unified;/* dual mode: admit score == min (table.py:1112-1115) */
+    int32_t overflow_in_hbm;   /* 0 = overflow arena in mapped pinned host memory (tiering), 1 = HBM */
+    int32_t device;            /* CUDA device ordinal */
+} hkv_config;
+
+/* TxnCounters (metrics.py:14-20), in this order. */
+enum { HKV_CTR_DIGEST_LINE_LOADS = 0, HKV_CTR_FULL_KEY_COMPARES, HKV_CTR_SCORE_SCANS,
+       HKV_CTR_SLOT_LOCK_RETRIES, HKV_CTR_VALUE_COPIES_FAST, HKV_CTR_VALUE_COPIES_OVERFLOW,
+       HKV_NUM_COUNTERS };
+
+const char *hkv_last_error(void);
+const char *hkv_version(void);
+
+/* CacheTable.__init__ (table.py:139-160) + TieredValueStore (store.py:41-79). */
+int hkv_create(const hkv_config *cfg, hkv_table **out);
+int hkv_destroy(hkv_table *t);
+
+/* find (table.py:304-323): found[i] in {0,1}; out rows of misses untouched;
+ * out may be NULL (contains, table.py:344-351). */
+int hkv_find(hkv_table *t, const uint64_t *keys, int64_t n, float *out, uint8_t *found,
+             hkv_stream stream);
+int hkv_contains(hkv_table *t, const uint64_t *keys, int64_t n, uint8_t *found, hkv_stream stream);
+/* find_ptr (table.py:325-342): tier 0 fast / 1 overflow, element offset in the
+ * tier arena, -1 for misses. */
+int hkv_find_ptr(hkv_table *t, const uint64_t *keys, int64_t n, uint8_t *found, uint8_t *tier,
+                 int64_t *offset, hkv_stream stream);
+
+/* insert_or_assign / insert_and_evict / find_or_insert (table.py:515-551,
+ * 934-1181).  Serial batch-order semantics.
+ *   op            hkv_upsert_op
+ *   values        (n, dim) input; in/out for FIND_OR_INSERT (values_inout)
+ *   scores        (n,) iff policy == HKV_CUSTOMIZED, else NULL
+ *   evicted_*     NULL, or (n)-row buffers: insert_and_evict outputs ordered by
+ *                 the evicting op's batch index; *n_evicted_dev (device int64)
+ *                 receives the count
+ *   ticks         NULL -> tick[i] = clock + i + 1 and clock += n (table.py:192-196);
+ *                 else per-op ticks and clock += clock_advance (sharded tables). */
+int hkv_upsert(hkv_table *t, int32_t op, const uint64_t *keys, float *values,
+               const uint64_t *scores, int64_t n, uint8_t *outcomes, uint64_t *evicted_keys,
+               float *evicted_values, uint64_t *evicted_scores, int64_t *n_evicted_dev,
+               const uint64_t *ticks, uint64_t clock_advance, hkv_stream stream);
+
+/* assign (table.py:438-442) when values != NULL; assign_scores (444-449) with
+ * explicit scores (kCustomized) or refresh != 0.  Last duplicate wins. */
+int hkv_assign(hkv_table *t, const uint64_t *keys, const float *values, const uint64_t *scores,
+               int32_t refresh, int64_t n, uint8_t *outcomes, hkv_stream stream);
+
+/* erase (table.py:553-558, 1006-1023). */
+int hkv_erase(hkv_table *t, const uint64_t *keys, int64_t n, uint8_t *outcomes, hkv_stream stream);
+
+/* export_batch_if (table.py:374-434).  Scans rows [cursor, capacity) in
+ * (bucket, slot) order keeping user keys with score >= min_score (when
+ * has_min_score; service.py:263-268) and, when row_mask != NULL, with
+ * row_mask[r - cursor] != 0 for rows r < cursor + mask_rows.  Writes up to
+ * max_count entries.  SYNCHRONISING: *count and *next_cursor (-1 = None) are
+ * host values. */
+int hkv_export(hkv_table *t, int64_t cursor, int64_t max_count, int32_t has_min_score,
+               uint64_t min_score, const uint8_t *row_mask, int64_t mask_rows, uint64_t *out_keys,
+               float *out_values, uint64_t *out_scores, int64_t *count, int64_t *next_cursor,
+               hkv_stream stream);
+
+/* size / load_factor (table.py:198-204).  SYNCHRONISING. */
+int hkv_size(hkv_table *t, int64_t *size, hkv_stream stream);
+/* set_epoch (table.py:206; scoring.py:45-50). */
+int hkv_set_epoch(hkv_table *t, uint64_t epoch);
+int hkv_get_epoch(hkv_table *t, uint64_t *epoch);
+/* Logical clock, first_eviction_lambda (table.py:156, 986-991), TxnCounters.
+ * SYNCHRONISING. */
+int hkv_clock(hkv_table *t, uint64_t *clock, hkv_stream stream);
+int hkv_first_eviction_lambda(hkv_table *t, int32_t *is_set, double *value, hkv_stream stream);
+int hkv_counters(hkv_table *t, int64_t *out /* HKV_NUM_COUNTERS */, hkv_stream stream);
+int hkv_reset_counters(hkv_table *t, hkv_stream stream);
+/* Device error latch (bitmask of hkv_device_error_bits); clears it.  SYNCHRONISING. */
+int hkv_device_error(hkv_table *t, int32_t *bits, hkv_stream stream);
+
+/* Raw state transfer (test / checkpoint support; the reference has no import
+ * API).  Host pointers; layout is the reference's arrays
+ * (table.py:143-146, store.py:56-61): keys/scores (B,128) u64, digests (B,128)
+ * u8, values (capacity, dim) f32 in row order.  occupancy is derived from keys.
+ * SYNCHRONISING. */
+int hkv_import_state(hkv_table *t, const uint64_t *keys, const uint8_t *digests,
+                     const uint64_t *scores, const float *values, uint64_t clock,
+                     int32_t fel_set, double fel);
+int hkv_export_state(hkv_table *t, uint64_t *keys, uint8_t *digests, uint64_t *scores,
+                     float *values, int64_t *occupancy);
+
+/* Metadata snapshot held in HBM (keys, digests, scores, occupancy bits, size,
+ * clock): the bench restores it between timed repeats so the load factor
+ * stays fixed.  Values are not part of the snapshot. */
+int hkv_snapshot(hkv_table *t, hkv_stream stream);
+int hkv_restore(hkv_table *t, hkv_stream stream);
+
+/* Device-side consistency scan (table.py:1284-1299).  SYNCHRONISING.
+ * *ok = 1 when occupancy bits, size counter and digests agree with the keys. */
+int hkv_check_consistency(hkv_table *t, int32_t *ok, hkv_stream stream);
+
+/* Sharding helper (multi-GPU routing): for each key compute the
+ * destination rank of its global bucket (h & (global_buckets-1)) >> log2(local
+ * buckets), and a stable counting-sort permutation grouping keys by
+ * destination.  perm[j] = source index of the j-th routed key; counts[r] =
+ * keys for rank r (device int64[world]). */
+int hkv_route(const uint64_t *keys, int64_t n, int64_t global_buckets, int32_t world,
+              int32_t *perm, int64_t *counts, hkv_stream stream);
+
+/* Launch-count instrumentation: number of kernels this library has launched. */
+int64_t hkv_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HKV_B200_H */

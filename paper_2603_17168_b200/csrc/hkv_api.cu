@@ -1,0 +1,541 @@
+// hkv_api.cu — the C-ABI (include/hkv_b200.h): table construction, memory
+// placement (HBM / mapped pinned host tier), per-stream workspaces and the
+// entry points that replace cachekv.CacheTable's methods.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "../../include/hkv_b200.h"
+#include "hkv_kernels.h"
+
+namespace hkv {
+unsigned long long g_launches = 0;
+}
+
+using namespace hkv;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct TableScalars {
+  unsigned long long size;
+  unsigned long long clock;
+  unsigned long long counters[6];
+  unsigned long long round;
+  int err;
+  int fel_set;
+  double fel;
+  int check[4];  // consistency scratch: ok, pad, total(u64)
+};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return HKV_ECUDA;
+}
+
+}  // namespace
+
+struct hkv_table {
+  hkv_config cfg;
+  int64_t buckets = 0;
+  int log2b = 0;
+  int num_sms = 148;
+  uint64_t fast_rows = 0;
+  uint64_t epoch = 0;
+  TableDev dev{};
+  uint64_t* keys = nullptr;
+  uint8_t* digests = nullptr;
+  uint64_t* scores = nullptr;
+  uint32_t* bits = nullptr;
+  float* vfast = nullptr;
+  float* vover = nullptr;       // device pointer of the overflow arena
+  float* vover_host = nullptr;  // pinned host allocation (mapped), if used
+  TableScalars* sc = nullptr;
+  unsigned long long* lead = nullptr;
+  // metadata snapshot
+  uint64_t* snap_keys = nullptr;
+  uint8_t* snap_digests = nullptr;
+  uint64_t* snap_scores = nullptr;
+  uint32_t* snap_bits = nullptr;
+  TableScalars* snap_sc = nullptr;
+  std::mutex mu;
+  std::map<cudaStream_t, Workspace> ws;
+
+  Workspace& workspace(cudaStream_t s) {
+    std::lock_guard<std::mutex> g(mu);
+    return ws[s];
+  }
+};
+
+namespace {
+
+std::mutex g_route_mu;
+std::map<cudaStream_t, Workspace> g_route_ws;
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void free_table(hkv_table* t) {
+  if (!t) return;
+  DeviceGuard g(t->cfg.device);
+  void* dptrs[] = {t->keys, t->digests, t->scores, t->bits, t->vfast, t->sc, t->lead,
+                   t->snap_keys, t->snap_digests, t->snap_scores, t->snap_bits, t->snap_sc};
+  for (void* p : dptrs)
+    if (p) cudaFree(p);
+  if (t->vover_host) cudaFreeHost(t->vover_host);
+  else if (t->vover) cudaFree(t->vover);
+  for (auto& kv : t->ws) ws_free(kv.second);
+  delete t;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hkv_last_error(void) { return g_err.c_str(); }
+const char* hkv_version(void) { return "hkv_b200 0.1 sm_100a"; }
+int64_t hkv_launch_count(void) { return (int64_t)g_launches; }
+
+int hkv_create(const hkv_config* cfg, hkv_table** out) {
+  if (!cfg || !out) return fail(HKV_EINVAL, "null argument");
+  *out = nullptr;
+  const hkv_config c = *cfg;
+  // table.py:108-127 (same messages)
+  if (c.capacity <= 0 || c.capacity % kSlots != 0) return fail(HKV_EINVAL, "capacity must be a positive multiple of 128");
+  const int64_t bc = c.capacity / kSlots;
+  if (bc & (bc - 1)) return fail(HKV_EINVAL, "bucket count must be a power of two");
+  if (c.value_dim < 1) return fail(HKV_EINVAL, "value_dim must be >= 1");
+  if (c.capacity > (1ll << 31)) return fail(HKV_EINVAL, "capacity above 2^31 slots per device is not supported");
+  const int64_t budget = c.fast_tier_budget < 0 ? bc : c.fast_tier_budget;
+  if (budget > bc) return fail(HKV_EINVAL, "fast_tier_budget out of range");
+  if (c.mode != HKV_MODE_SINGLE && c.mode != HKV_MODE_DUAL) return fail(HKV_EINVAL, "unknown mode");
+  if (c.score_policy < HKV_LRU || c.score_policy > HKV_CUSTOMIZED) return fail(HKV_EINVAL, "unknown policy");
+  if (c.value_dim > (1 << 20)) return fail(HKV_EINVAL, "value_dim too large");
+
+  DeviceGuard g(c.device);
+  hkv_table* t = new hkv_table();
+  t->cfg = c;
+  t->cfg.fast_tier_budget = budget;
+  t->buckets = bc;
+  while ((1ll << t->log2b) < bc) t->log2b++;
+  cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, c.device);
+  t->fast_rows = (uint64_t)budget * kSlots;
+  const uint64_t cap = (uint64_t)c.capacity;
+  const uint64_t dim = (uint64_t)c.value_dim;
+  const uint64_t over_rows = cap - t->fast_rows;
+  cudaError_t e;
+  if ((e = cudaMalloc((void**)&t->keys, cap * 8)) || (e = cudaMalloc((void**)&t->digests, cap)) ||
+      (e = cudaMalloc((void**)&t->scores, cap * 8)) || (e = cudaMalloc((void**)&t->bits, (size_t)bc * 16)) ||
+      (e = cudaMalloc((void**)&t->sc, sizeof(TableScalars)))) {
+    free_table(t);
+    return fail(HKV_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e));
+  }
+  if (t->fast_rows && (e = cudaMalloc((void**)&t->vfast, t->fast_rows * dim * 4))) {
+    free_table(t);
+    return fail(HKV_ENOMEM, std::string("HBM value arena allocation failed: ") + cudaGetErrorString(e));
+  }
+  if (over_rows) {
+    if (c.overflow_in_hbm) {
+      e = cudaMalloc((void**)&t->vover, over_rows * dim * 4);
+    } else {
+      // tiered KV separation: overflow values in mapped pinned host memory
+      e = cudaHostAlloc((void**)&t->vover_host, over_rows * dim * 4, cudaHostAllocMapped | cudaHostAllocPortable);
+      if (!e) e = cudaHostGetDevicePointer((void**)&t->vover, t->vover_host, 0);
+    }
+    if (e) {
+      free_table(t);
+      return fail(HKV_ENOMEM, std::string("overflow arena allocation failed: ") + cudaGetErrorString(e));
+    }
+  }
+  if (c.mode == HKV_MODE_DUAL && (e = cudaMalloc((void**)&t->lead, (size_t)bc * 8))) {
+    free_table(t);
+    return fail(HKV_ENOMEM, "lead array allocation failed");
+  }
+  // initial state, table.py:143-149 / store.py:36-37
+  if ((e = cudaMemset(t->keys, 0xFF, cap * 8)) || (e = cudaMemset(t->digests, 0, cap)) ||
+      (e = cudaMemset(t->scores, 0, cap * 8)) || (e = cudaMemset(t->bits, 0, (size_t)bc * 16)) ||
+      (e = cudaMemset(t->sc, 0, sizeof(TableScalars))) ||
+      (t->vfast && (e = cudaMemset(t->vfast, 0, t->fast_rows * dim * 4))) ||
+      (t->vover && (e = cudaMemset(t->vover, 0, over_rows * dim * 4))) ||
+      (t->lead && (e = cudaMemset(t->lead, 0, (size_t)bc * 8)))) {
+    free_table(t);
+    return cuda_fail(e, "hkv_create init");
+  }
+  if ((e = cudaDeviceSynchronize())) {
+    free_table(t);
+    return cuda_fail(e, "hkv_create sync");
+  }
+  TableDev& d = t->dev;
+  d.keys = t->keys;
+  d.digests = t->digests;
+  d.scores = t->scores;
+  d.bits = t->bits;
+  d.vfast = t->vfast;
+  d.vover = t->vover;
+  d.fast_rows = t->fast_rows;
+  d.mask = (uint64_t)(bc - 1);
+  d.capacity = cap;
+  d.dim = (int)c.value_dim;
+  d.dual = c.mode == HKV_MODE_DUAL;
+  d.policy = c.score_policy;
+  d.digest_filter = c.digest_filter;
+  d.admit_unified = c.admit_ties_unified;
+  d.size = &t->sc->size;
+  d.clock = &t->sc->clock;
+  d.counters = t->sc->counters;
+  d.err = &t->sc->err;
+  d.fel_set = &t->sc->fel_set;
+  d.fel = &t->sc->fel;
+  *out = t;
+  return HKV_OK;
+}
+
+int hkv_destroy(hkv_table* t) {
+  if (!t) return HKV_OK;
+  {
+    DeviceGuard g(t->cfg.device);
+    cudaDeviceSynchronize();
+  }
+  free_table(t);
+  return HKV_OK;
+}
+
+#define CHECK_T()                                   \
+  if (!t) return fail(HKV_EINVAL, "null table");    \
+  if (n < 0) return fail(HKV_EINVAL, "negative batch size"); \
+  DeviceGuard _g(t->cfg.device)
+
+int hkv_find(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uint8_t* found, hkv_stream stream) {
+  CHECK_T();
+  if (n && (!keys || !found)) return fail(HKV_EINVAL, "null keys/found");
+  launch_find(t->dev, keys, n, out, found, nullptr, nullptr, out ? 0 : 1, (cudaStream_t)stream, t->num_sms);
+  cudaError_t e = cudaGetLastError();
+  return e ? cuda_fail(e, "hkv_find") : HKV_OK;
+}
+
+int hkv_contains(hkv_table* t, const uint64_t* keys, int64_t n, uint8_t* found, hkv_stream stream) {
+  CHECK_T();
+  if (n && (!keys || !found)) return fail(HKV_EINVAL, "null keys/found");
+  launch_find(t->dev, keys, n, nullptr, found, nullptr, nullptr, 1, (cudaStream_t)stream, t->num_sms);
+  cudaError_t e = cudaGetLastError();
+  return e ? cuda_fail(e, "hkv_contains") : HKV_OK;
+}
+
+int hkv_find_ptr(hkv_table* t, const uint64_t* keys, int64_t n, uint8_t* found, uint8_t* tier, int64_t* offset,
+                 hkv_stream stream) {
+  CHECK_T();
+  if (n && (!keys || !found || !tier || !offset)) return fail(HKV_EINVAL, "null argument");
+  launch_find(t->dev, keys, n, nullptr, found, tier, offset, 2, (cudaStream_t)stream, t->num_sms);
+  cudaError_t e = cudaGetLastError();
+  return e ? cuda_fail(e, "hkv_find_ptr") : HKV_OK;
+}
+
+int hkv_upsert(hkv_table* t, int32_t op, const uint64_t* keys, float* values, const uint64_t* scores, int64_t n,
+               uint8_t* outcomes, uint64_t* evicted_keys, float* evicted_values, uint64_t* evicted_scores,
+               int64_t* n_evicted_dev, const uint64_t* ticks, uint64_t clock_advance, hkv_stream stream) {
+  CHECK_T();
+  if (op != HKV_OP_INSERT_OR_ASSIGN && op != HKV_OP_FIND_OR_INSERT) return fail(HKV_EINVAL, "unknown upsert op");
+  // table.py:178-188
+  const bool custom = t->cfg.score_policy == HKV_CUSTOMIZED;
+  if (custom && !scores) return fail(HKV_EINVAL, "kCustomized requires explicit scores");
+  if (!custom && scores) return fail(HKV_EINVAL, "explicit scores require the kCustomized policy");
+  if (n && (!keys || !values || !outcomes)) return fail(HKV_EINVAL, "null keys/values/outcomes");
+  const bool collect = evicted_keys || evicted_values || evicted_scores;
+  if (collect && (!evicted_keys || !evicted_values || !evicted_scores || !n_evicted_dev))
+    return fail(HKV_EINVAL, "insert_and_evict needs all evicted outputs");
+  if (collect && op != HKV_OP_INSERT_OR_ASSIGN) return fail(HKV_EINVAL, "evicted outputs need insert_or_assign");
+  if (n > 0xFFFFFFFEll) return fail(HKV_EINVAL, "batch too large");
+  cudaStream_t s = (cudaStream_t)stream;
+  OpArgs a{};
+  a.keys = keys;
+  a.values = values;
+  a.scores = scores;
+  a.ticks = ticks;
+  a.outcomes = outcomes;
+  a.op = op == HKV_OP_FIND_OR_INSERT ? kOpFindOrInsert : kOpUpsert;
+  a.collect = collect;
+  a.epoch = t->epoch;
+  cudaError_t e = run_mutation(t->dev, a, n, t->log2b, t->workspace(s), &t->sc->round, t->lead, n_evicted_dev,
+                               evicted_keys, evicted_values, evicted_scores, ticks ? clock_advance : (uint64_t)n, s,
+                               t->num_sms);
+  return e ? cuda_fail(e, "hkv_upsert") : HKV_OK;
+}
+
+int hkv_erase(hkv_table* t, const uint64_t* keys, int64_t n, uint8_t* outcomes, hkv_stream stream) {
+  CHECK_T();
+  if (n && (!keys || !outcomes)) return fail(HKV_EINVAL, "null keys/outcomes");
+  cudaStream_t s = (cudaStream_t)stream;
+  OpArgs a{};
+  a.keys = keys;
+  a.outcomes = outcomes;
+  a.op = kOpErase;
+  a.epoch = t->epoch;
+  a.values = nullptr;
+  cudaError_t e = run_mutation(t->dev, a, n, t->log2b, t->workspace(s), &t->sc->round, t->lead, nullptr, nullptr,
+                               nullptr, nullptr, 0, s, t->num_sms);
+  return e ? cuda_fail(e, "hkv_erase") : HKV_OK;
+}
+
+int hkv_assign(hkv_table* t, const uint64_t* keys, const float* values, const uint64_t* scores, int32_t refresh,
+               int64_t n, uint8_t* outcomes, hkv_stream stream) {
+  CHECK_T();
+  const bool custom = t->cfg.score_policy == HKV_CUSTOMIZED;
+  if (!values) {
+    // assign_scores (table.py:444-449 -> _coerce_scores 178-188)
+    if (!scores && custom) return fail(HKV_EINVAL, "kCustomized requires explicit scores");
+    if (scores && !custom) return fail(HKV_EINVAL, "explicit scores require the kCustomized policy");
+    if (!scores) refresh = 1;
+  } else {
+    refresh = 0;
+  }
+  if (n && (!keys || !outcomes)) return fail(HKV_EINVAL, "null keys/outcomes");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = run_assign(t->dev, keys, values, scores, refresh, t->epoch, n, outcomes, t->log2b,
+                             t->workspace(s), s, t->num_sms);
+  return e ? cuda_fail(e, "hkv_assign") : HKV_OK;
+}
+
+int hkv_export(hkv_table* t, int64_t cursor, int64_t max_count, int32_t has_min_score, uint64_t min_score,
+               const uint8_t* row_mask, int64_t mask_rows, uint64_t* out_keys, float* out_values,
+               uint64_t* out_scores, int64_t* count, int64_t* next_cursor, hkv_stream stream) {
+  if (!t) return fail(HKV_EINVAL, "null table");
+  DeviceGuard _g(t->cfg.device);
+  // table.py:386-391
+  if (cursor < 0 || cursor >= t->cfg.capacity) return fail(HKV_EINVAL, "cursor out of range");
+  if (max_count < 1) return fail(HKV_EINVAL, "max_count must be >= 1");
+  if (!count || !next_cursor || !out_keys || !out_values || !out_scores) return fail(HKV_EINVAL, "null output");
+  if (row_mask && (mask_rows < 0 || cursor + mask_rows > t->cfg.capacity)) return fail(HKV_EINVAL, "mask range");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = run_export(t->dev, cursor, max_count, has_min_score, min_score, row_mask, mask_rows, out_keys,
+                             out_values, out_scores, count, next_cursor, t->workspace(s), s, t->num_sms);
+  return e ? cuda_fail(e, "hkv_export") : HKV_OK;
+}
+
+static int read_scalars(hkv_table* t, TableScalars* h, hkv_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(h, t->sc, sizeof(TableScalars), cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaStreamSynchronize(s);
+  return e ? cuda_fail(e, "read scalars") : HKV_OK;
+}
+
+int hkv_size(hkv_table* t, int64_t* size, hkv_stream stream) {
+  if (!t || !size) return fail(HKV_EINVAL, "null argument");
+  DeviceGuard _g(t->cfg.device);
+  TableScalars h;
+  int rc = read_scalars(t, &h, stream);
+  if (rc) return rc;
+  *size = (int64_t)h.size;
+  return HKV_OK;
+}
+
+int hkv_set_epoch(hkv_table* t, uint64_t epoch) {
+  if (!t) return fail(HKV_EINVAL, "null table");
+  // scoring.py:45-50
+  if (epoch < t->epoch) return fail(HKV_EINVAL, "epoch may not decrease");
+  if (epoch > 0xFFFFFFFFull) return fail(HKV_EINVAL, "epoch must fit in 32 bits");
+  t->epoch = epoch;
+  return HKV_OK;
+}
+
+int hkv_get_epoch(hkv_table* t, uint64_t* epoch) {
+  if (!t || !epoch) return fail(HKV_EINVAL, "null argument");
+  *epoch = t->epoch;
+  return HKV_OK;
+}
+
+int hkv_clock(hkv_table* t, uint64_t* clock, hkv_stream stream) {
+  if (!t || !clock) return fail(HKV_EINVAL, "null argument");
+  DeviceGuard _g(t->cfg.device);
+  TableScalars h;
+  int rc = read_scalars(t, &h, stream);
+  if (rc) return rc;
+  *clock = h.clock;
+  return HKV_OK;
+}
+
+int hkv_first_eviction_lambda(hkv_table* t, int32_t* is_set, double* value, hkv_stream stream) {
+  if (!t || !is_set || !value) return fail(HKV_EINVAL, "null argument");
+  DeviceGuard _g(t->cfg.device);
+  TableScalars h;
+  int rc = read_scalars(t, &h, stream);
+  if (rc) return rc;
+  *is_set = h.fel_set;
+  *value = h.fel;
+  return HKV_OK;
+}
+
+int hkv_counters(hkv_table* t, int64_t* out, hkv_stream stream) {
+  if (!t || !out) return fail(HKV_EINVAL, "null argument");
+  DeviceGuard _g(t->cfg.device);
+  TableScalars h;
+  int rc = read_scalars(t, &h, stream);
+  if (rc) return rc;
+  for (int k = 0; k < HKV_NUM_COUNTERS; k++) out[k] = (int64_t)h.counters[k];
+  return HKV_OK;
+}
+
+int hkv_reset_counters(hkv_table* t, hkv_stream stream) {
+  if (!t) return fail(HKV_EINVAL, "null table");
+  DeviceGuard _g(t->cfg.device);
+  cudaError_t e = cudaMemsetAsync(t->sc->counters, 0, sizeof(t->sc->counters), (cudaStream_t)stream);
+  return e ? cuda_fail(e, "reset counters") : HKV_OK;
+}
+
+int hkv_device_error(hkv_table* t, int32_t* bits, hkv_stream stream) {
+  if (!t || !bits) return fail(HKV_EINVAL, "null argument");
+  DeviceGuard _g(t->cfg.device);
+  cudaStream_t s = (cudaStream_t)stream;
+  int v = 0;
+  cudaError_t e = cudaMemcpyAsync(&v, &t->sc->err, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaMemsetAsync(&t->sc->err, 0, sizeof(int), s);
+  if (!e) e = cudaStreamSynchronize(s);
+  if (e) return cuda_fail(e, "device error");
+  *bits = v;
+  return HKV_OK;
+}
+
+int hkv_import_state(hkv_table* t, const uint64_t* keys, const uint8_t* digests, const uint64_t* scores,
+                     const float* values, uint64_t clock, int32_t fel_set, double fel) {
+  if (!t || !keys || !digests || !scores || !values) return fail(HKV_EINVAL, "null argument");
+  DeviceGuard _g(t->cfg.device);
+  const uint64_t cap = (uint64_t)t->cfg.capacity, dim = (uint64_t)t->cfg.value_dim;
+  cudaError_t e;
+  if ((e = cudaMemcpy(t->keys, keys, cap * 8, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(t->digests, digests, cap, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(t->scores, scores, cap * 8, cudaMemcpyHostToDevice)))
+    return cuda_fail(e, "import metadata");
+  if (t->fast_rows && (e = cudaMemcpy(t->vfast, values, t->fast_rows * dim * 4, cudaMemcpyHostToDevice)))
+    return cuda_fail(e, "import values");
+  if (cap > t->fast_rows &&
+      (e = cudaMemcpy(t->vover, values + t->fast_rows * dim, (cap - t->fast_rows) * dim * 4, cudaMemcpyDefault)))
+    return cuda_fail(e, "import overflow values");
+  if ((e = run_bits_from_keys(t->dev, t->buckets, 0))) return cuda_fail(e, "import bits");
+  TableScalars h;
+  if ((e = cudaMemcpy(&h, t->sc, sizeof(h), cudaMemcpyDeviceToHost))) return cuda_fail(e, "import scalars");
+  h.clock = clock;
+  h.fel_set = fel_set;
+  h.fel = fel;
+  if ((e = cudaMemcpy(t->sc, &h, sizeof(h), cudaMemcpyHostToDevice))) return cuda_fail(e, "import scalars");
+  e = cudaDeviceSynchronize();
+  return e ? cuda_fail(e, "import sync") : HKV_OK;
+}
+
+int hkv_export_state(hkv_table* t, uint64_t* keys, uint8_t* digests, uint64_t* scores, float* values,
+                     int64_t* occupancy) {
+  if (!t) return fail(HKV_EINVAL, "null table");
+  DeviceGuard _g(t->cfg.device);
+  const uint64_t cap = (uint64_t)t->cfg.capacity, dim = (uint64_t)t->cfg.value_dim;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e) return cuda_fail(e, "export sync");
+  if (keys && (e = cudaMemcpy(keys, t->keys, cap * 8, cudaMemcpyDeviceToHost))) return cuda_fail(e, "export keys");
+  if (digests && (e = cudaMemcpy(digests, t->digests, cap, cudaMemcpyDeviceToHost))) return cuda_fail(e, "export");
+  if (scores && (e = cudaMemcpy(scores, t->scores, cap * 8, cudaMemcpyDeviceToHost))) return cuda_fail(e, "export");
+  if (values) {
+    if (t->fast_rows && (e = cudaMemcpy(values, t->vfast, t->fast_rows * dim * 4, cudaMemcpyDeviceToHost)))
+      return cuda_fail(e, "export values");
+    if (cap > t->fast_rows &&
+        (e = cudaMemcpy(values + t->fast_rows * dim, t->vover, (cap - t->fast_rows) * dim * 4, cudaMemcpyDefault)))
+      return cuda_fail(e, "export overflow values");
+  }
+  if (occupancy) {
+    uint32_t* hb = (uint32_t*)malloc((size_t)t->buckets * 16);
+    if (!hb) return fail(HKV_ENOMEM, "host alloc");
+    if ((e = cudaMemcpy(hb, t->bits, (size_t)t->buckets * 16, cudaMemcpyDeviceToHost))) {
+      free(hb);
+      return cuda_fail(e, "export bits");
+    }
+    for (int64_t b = 0; b < t->buckets; b++)
+      occupancy[b] = __builtin_popcount(hb[4 * b]) + __builtin_popcount(hb[4 * b + 1]) +
+                     __builtin_popcount(hb[4 * b + 2]) + __builtin_popcount(hb[4 * b + 3]);
+    free(hb);
+  }
+  return HKV_OK;
+}
+
+int hkv_snapshot(hkv_table* t, hkv_stream stream) {
+  if (!t) return fail(HKV_EINVAL, "null table");
+  DeviceGuard _g(t->cfg.device);
+  const uint64_t cap = (uint64_t)t->cfg.capacity;
+  cudaError_t e;
+  if (!t->snap_keys) {
+    if ((e = cudaMalloc((void**)&t->snap_keys, cap * 8)) || (e = cudaMalloc((void**)&t->snap_digests, cap)) ||
+        (e = cudaMalloc((void**)&t->snap_scores, cap * 8)) ||
+        (e = cudaMalloc((void**)&t->snap_bits, (size_t)t->buckets * 16)) ||
+        (e = cudaMalloc((void**)&t->snap_sc, sizeof(TableScalars))))
+      return fail(HKV_ENOMEM, std::string("snapshot allocation failed: ") + cudaGetErrorString(e));
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((e = cudaMemcpyAsync(t->snap_keys, t->keys, cap * 8, cudaMemcpyDeviceToDevice, s)) ||
+      (e = cudaMemcpyAsync(t->snap_digests, t->digests, cap, cudaMemcpyDeviceToDevice, s)) ||
+      (e = cudaMemcpyAsync(t->snap_scores, t->scores, cap * 8, cudaMemcpyDeviceToDevice, s)) ||
+      (e = cudaMemcpyAsync(t->snap_bits, t->bits, (size_t)t->buckets * 16, cudaMemcpyDeviceToDevice, s)) ||
+      (e = cudaMemcpyAsync(t->snap_sc, t->sc, sizeof(TableScalars), cudaMemcpyDeviceToDevice, s)))
+    return cuda_fail(e, "snapshot");
+  return HKV_OK;
+}
+
+int hkv_restore(hkv_table* t, hkv_stream stream) {
+  if (!t) return fail(HKV_EINVAL, "null table");
+  if (!t->snap_keys) return fail(HKV_EINVAL, "no snapshot taken");
+  DeviceGuard _g(t->cfg.device);
+  const uint64_t cap = (uint64_t)t->cfg.capacity;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(t->keys, t->snap_keys, cap * 8, cudaMemcpyDeviceToDevice, s)) ||
+      (e = cudaMemcpyAsync(t->digests, t->snap_digests, cap, cudaMemcpyDeviceToDevice, s)) ||
+      (e = cudaMemcpyAsync(t->scores, t->snap_scores, cap * 8, cudaMemcpyDeviceToDevice, s)) ||
+      (e = cudaMemcpyAsync(t->bits, t->snap_bits, (size_t)t->buckets * 16, cudaMemcpyDeviceToDevice, s)) ||
+      (e = cudaMemcpyAsync(t->sc, t->snap_sc, sizeof(TableScalars), cudaMemcpyDeviceToDevice, s)))
+    return cuda_fail(e, "restore");
+  return HKV_OK;
+}
+
+int hkv_check_consistency(hkv_table* t, int32_t* ok, hkv_stream stream) {
+  if (!t || !ok) return fail(HKV_EINVAL, "null argument");
+  DeviceGuard _g(t->cfg.device);
+  cudaStream_t s = (cudaStream_t)stream;
+  int init[4] = {1, 0, 0, 0};
+  cudaError_t e = cudaMemcpyAsync(t->sc->check, init, sizeof(init), cudaMemcpyHostToDevice, s);
+  if (!e) e = run_consistency(t->dev, t->buckets, t->sc->check, s);
+  TableScalars h;
+  if (!e) e = cudaMemcpyAsync(&h, t->sc, sizeof(h), cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaStreamSynchronize(s);
+  if (e) return cuda_fail(e, "consistency");
+  unsigned long long total;
+  memcpy(&total, &h.check[2], sizeof(total));
+  *ok = h.check[0] == 1 && total == h.size;
+  return HKV_OK;
+}
+
+int hkv_route(const uint64_t* keys, int64_t n, int64_t global_buckets, int32_t world, int32_t* perm,
+              int64_t* counts, hkv_stream stream) {
+  if (n < 0 || world < 1 || world > 64 || global_buckets < world || (global_buckets & (global_buckets - 1)) ||
+      (world & (world - 1)))
+    return fail(HKV_EINVAL, "bad route arguments (world and bucket count must be powers of two, world <= 64)");
+  cudaStream_t s = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> g(g_route_mu);
+  cudaError_t e = run_route(keys, n, global_buckets, world, perm, counts, g_route_ws[s], s);
+  return e ? cuda_fail(e, "hkv_route") : HKV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,200 @@
+// hkv_common.cuh — device-side layout, hashing and score policies shared by
+// every kernel of the B200 table.
+//
+// HBM layout (bucket-major; one bucket = 128 slots, the key's whole
+// candidate space):
+//   digests [B][128] u8   one 128-B line per bucket (the probe's first read)
+//   bits    [B][4]   u32  128-bit occupancy bitmap (bit s <=> keys[b][s] is a
+//                         user key); replaces the reference's occupancy
+//                         counter + argmax(keys==EMPTY) scan (table.py:1171)
+//   keys    [B][128] u64  8 lines per bucket
+//   scores  [B][128] u64  8 lines per bucket (read only on full-bucket decisions)
+//   values  rows [capacity][dim] f32: rows < fast_rows in HBM, the rest in the
+//           overflow arena (mapped pinned host memory, or HBM)
+#pragma once
+#include <cooperative_groups.h>
+#include <cstdint>
+#include <type_traits>
+#include <cuda_runtime.h>
+
+namespace hkv {
+
+namespace cg = cooperative_groups;
+
+constexpr int kSlots = 128;
+constexpr uint64_t kEmptyKey = 0xFFFFFFFFFFFFFFFFull;   // hashing.py:10
+constexpr uint64_t kLockedKey = 0xFFFFFFFFFFFFFFFEull;  // hashing.py:11
+constexpr uint64_t kMaxScore = 0xFFFFFFFFFFFFFFFFull;
+constexpr uint64_t kLow32 = 0xFFFFFFFFull;
+
+enum Policy : int { kLru = 0, kLfu = 1, kEpochLru = 2, kEpochLfu = 3, kCustom = 4 };
+enum Outcome : uint8_t {
+  kInserted = 0, kUpdated = 1, kRejected = 2, kEvicted = 3, kFound = 4, kNotFound = 5, kErased = 6
+};
+enum Ctr : int { kLoads = 0, kCompares = 1, kScans = 2, kRetries = 3, kVFast = 4, kVOver = 5 };
+
+// Table metadata handed to kernels by value.
+struct TableDev {
+  uint64_t* keys;
+  uint8_t* digests;
+  uint64_t* scores;
+  uint32_t* bits;
+  float* vfast;       // rows [0, fast_rows)
+  float* vover;       // rows [fast_rows, capacity), indexed row - fast_rows
+  uint64_t fast_rows;
+  uint64_t mask;      // bucket_count - 1
+  uint64_t capacity;
+  int dim;
+  int dual;
+  int policy;
+  int digest_filter;
+  int admit_unified;
+  // device scalars
+  unsigned long long* size;      // int64 two's complement
+  unsigned long long* clock;
+  unsigned long long* counters;  // [6]
+  int* err;                      // error latch
+  int* fel_set;
+  double* fel;
+};
+
+// hashing.py:21-29 fmix64 (Murmur3 finalizer)
+__device__ __forceinline__ uint64_t fmix64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xFF51AFD7ED558CCDull;
+  x ^= x >> 33;
+  x *= 0xC4CEB9FE1A85EC53ull;
+  x ^= x >> 33;
+  return x;
+}
+// hashing.py:52-57 second hash for dual mode
+__device__ __forceinline__ uint64_t second_hash(uint64_t h1) {
+  return fmix64(h1 ^ 0x9E3779B97F4A7C15ull);
+}
+// hashing.py:60-66: digest = bits 32..39
+__device__ __forceinline__ uint32_t digest_of(uint64_t h) { return (uint32_t)(h >> 32) & 0xFFu; }
+
+// scoring.py:56-76 score_on_insert
+__device__ __forceinline__ uint64_t insert_score(int policy, uint64_t epoch, uint64_t tick,
+                                                 uint64_t custom) {
+  switch (policy) {
+    case kLru: return tick;
+    case kLfu: return 1;
+    case kEpochLru: return (epoch << 32) | (tick & kLow32);
+    case kEpochLfu: return (epoch << 32) | 1;
+    default: return custom;
+  }
+}
+
+// scoring.py:79-102 score_on_hit
+__device__ __forceinline__ uint64_t hit_score(int policy, uint64_t old, uint64_t epoch,
+                                              uint64_t tick, bool has_custom, uint64_t custom) {
+  switch (policy) {
+    case kLru: return tick;
+    case kLfu: return old == kMaxScore ? old : old + 1;
+    case kEpochLru: return (epoch << 32) | (tick & kLow32);
+    case kEpochLfu: {
+      if ((old >> 32) == epoch) {
+        uint64_t low = old & kLow32;
+        if (low < kLow32) low++;
+        return (epoch << 32) | low;
+      }
+      return (epoch << 32) | 1;
+    }
+    default: return has_custom ? custom : old;
+  }
+}
+
+__device__ __forceinline__ bool hit_needs_old(int policy) {
+  return policy == kLfu || policy == kEpochLfu || policy == kCustom;
+}
+
+// store.py:84-94 / 115-131: position-addressed value row.
+__device__ __forceinline__ float* value_row(const TableDev& t, uint64_t row) {
+  return row < t.fast_rows ? t.vfast + row * (uint64_t)t.dim
+                           : t.vover + (row - t.fast_rows) * (uint64_t)t.dim;
+}
+
+// 16 digest bytes (one uint4) vs the query digest -> 16-bit match mask.
+__device__ __forceinline__ uint32_t match16(uint4 w, uint32_t d) {
+  const uint32_t dd = d * 0x01010101u;
+  uint32_t m = 0;
+  uint32_t x;
+  x = __vcmpeq4(w.x, dd);
+  m |= (x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u);
+  x = __vcmpeq4(w.y, dd);
+  m |= ((x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u)) << 4;
+  x = __vcmpeq4(w.z, dd);
+  m |= ((x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u)) << 8;
+  x = __vcmpeq4(w.w, dd);
+  m |= ((x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u)) << 12;
+  return m;
+}
+
+__device__ __forceinline__ uint32_t match4(uint32_t w, uint32_t d) {
+  uint32_t x = __vcmpeq4(w, d * 0x01010101u);
+  return (x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u);
+}
+
+// Streaming loads/stores for data touched once.
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// Copy one value row of `dim` floats with a tile of G lanes, VEC floats per
+// access (VEC = 4 requires 16-B aligned rows, i.e. dim % 4 == 0).  Loads are
+// issued in groups of U before the matching stores so a lane keeps U
+// requests in flight.
+template <typename V>
+__device__ __forceinline__ V ld_vec(const V* p) { return *p; }
+template <typename V>
+__device__ __forceinline__ void st_vec(V* p, V v) { *p = v; }
+
+template <int G, int VEC, int U = 4>
+__device__ __forceinline__ void copy_row(float* dst, const float* src, int dim, int rank) {
+  using V = typename std::conditional<VEC == 4, uint4, typename std::conditional<VEC == 2, float2, float>::type>::type;
+  const V* s = reinterpret_cast<const V*>(src);
+  V* d = reinterpret_cast<V*>(dst);
+  const int nv = dim / VEC;
+  for (int e0 = rank; e0 < nv; e0 += G * U) {
+    V v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int e = e0 + u * G;
+      if (e < nv) v[u] = ld_vec(s + e);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int e = e0 + u * G;
+      if (e < nv) st_vec(d + e, v[u]);
+    }
+  }
+}
+
+// Block-level flush of per-thread counters into the table counters.
+template <int NT>
+__device__ __forceinline__ void flush_counters(unsigned long long* dst, unsigned long long* c, int nc) {
+  __shared__ unsigned long long sh[6];
+  if (threadIdx.x < 6) sh[threadIdx.x] = 0;
+  __syncthreads();
+  for (int k = 0; k < nc; k++) {
+    unsigned long long v = c[k];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sh[k], v);
+  }
+  __syncthreads();
+  if (threadIdx.x < nc && sh[threadIdx.x]) atomicAdd(&dst[threadIdx.x], sh[threadIdx.x]);
+}
+
+extern unsigned long long g_launches;  // host-side launch counter (hkv_api.cu)
+
+}  // namespace hkv

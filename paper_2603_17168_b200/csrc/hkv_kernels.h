@@ -1,0 +1,87 @@
+// hkv_kernels.h — host-side launchers for the table kernels (internal).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "hkv_common.cuh"
+
+namespace hkv {
+
+// Per-batch device scalars (zeroed by the launcher before each batch).
+struct Scalars {
+  int err;                       // sentinel key seen in this batch
+  unsigned nseg;                 // bucket segments
+  unsigned first_ev;             // lowest batch index with an Evicted outcome
+  unsigned npend[2];             // dual-mode pending list sizes (per round parity)
+  unsigned pad;
+  long long size_before;         // table size when the batch started
+  unsigned long long nfound;     // assign: found ops (clock advance for refresh)
+  long long n_sel;               // DeviceSelect count
+};
+
+// Per-stream scratch, grown on demand.
+struct Workspace {
+  int64_t cap_n = 0;
+  int64_t cap_ev = 0;  // rows of evicted-value scratch
+  int dim = 0;
+  uint32_t* bkt = nullptr;
+  uint32_t* idx = nullptr;
+  uint32_t* sbkt = nullptr;
+  uint32_t* sidx = nullptr;
+  uint32_t* seg = nullptr;
+  uint32_t* aux = nullptr;   // assign: rows / evicted list
+  uint32_t* aux2 = nullptr;  // assign: found ranks
+  uint32_t* b2 = nullptr;    // dual: second bucket
+  uint32_t* pend = nullptr;  // dual: second pending list
+  uint64_t* ek = nullptr;
+  uint64_t* es = nullptr;
+  float* ev = nullptr;
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  Scalars* sc = nullptr;
+};
+
+struct OpArgs {
+  const uint64_t* keys;
+  float* values;
+  const uint64_t* scores;
+  const uint64_t* ticks;
+  uint8_t* outcomes;
+  uint64_t* ek;  // per-op evicted key scratch (collect)
+  uint64_t* es;
+  float* ev;
+  int op;        // 0 insert_or_assign, 1 find_or_insert, 2 erase
+  int collect;
+  uint64_t epoch;
+  Scalars* sc;
+};
+
+enum { kOpUpsert = 0, kOpFindOrInsert = 1, kOpErase = 2 };
+
+void launch_find(const TableDev& t, const uint64_t* keys, int64_t n, float* out, uint8_t* found,
+                 uint8_t* tier, int64_t* offset, int mode, cudaStream_t s, int num_sms);
+
+// Returns cudaSuccess or the first error.
+cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, Workspace& ws,
+                         unsigned long long* round_ctr, unsigned long long* lead, int64_t* n_evicted,
+                         uint64_t* ek_out, float* ev_out, uint64_t* es_out, uint64_t clock_advance,
+                         cudaStream_t s, int num_sms);
+
+cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* values,
+                       const uint64_t* scores, int refresh, uint64_t epoch, int64_t n, uint8_t* outcomes,
+                       int log2_buckets, Workspace& ws, cudaStream_t s, int num_sms);
+
+cudaError_t run_export(const TableDev& t, int64_t cursor, int64_t max_count, int has_min, uint64_t min_score,
+                       const uint8_t* mask, int64_t mask_rows, uint64_t* ok, float* ov, uint64_t* os,
+                       int64_t* count, int64_t* next, Workspace& ws, cudaStream_t s, int num_sms);
+
+cudaError_t run_bits_from_keys(const TableDev& t, int64_t buckets, cudaStream_t s);
+cudaError_t run_consistency(const TableDev& t, int64_t buckets, int* ok_dev, cudaStream_t s);
+cudaError_t run_route(const uint64_t* keys, int64_t n, int64_t global_buckets, int world, int32_t* perm,
+                      int64_t* counts, Workspace& ws, cudaStream_t s);
+
+cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, bool need_ev, bool dual);
+void ws_free(Workspace& ws);
+
+}  // namespace hkv

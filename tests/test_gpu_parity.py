@@ -1,0 +1,255 @@
+"""Parity of the B200 table (CUDA kernels through the C-ABI) with the oracle
+and with the reference's recorded outputs.  Bit-exact everywhere: keys,
+digests, scores, values, outcomes, evicted tuples, counters.
+
+Run on a B200: python -m pytest tests -m gpu
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from golden_replay import CASE_FILES, load_case, replay  # noqa: E402
+from oracle.oracle import OracleTable  # noqa: E402
+from refdiff import make_script, outputs_equal, run_impl  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+MODES = ["single", "dual"]
+POLICIES = ["kLru", "kLfu", "kEpochLru", "kEpochLfu", "kCustomized"]
+
+
+@pytest.fixture(scope="module")
+def hkv():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu test ran without a CUDA device")
+    import paper_2603_17168_b200 as p
+
+    return p
+
+
+def make_table(hkv, cap, dim, mode="single", policy="kLru", budget=None, unified=False, **kw):
+    return hkv.CacheTable(hkv.TableConfig(capacity=cap, value_dim=dim, mode=mode, score_policy=policy,
+                                          fast_tier_budget=budget, admit_ties_unified=unified, **kw))
+
+
+def assert_same_state(t, o):
+    st = t.export_state()
+    assert st["keys"].tobytes() == o.keys.tobytes(), "keys"
+    assert st["digests"].tobytes() == o.digests.tobytes(), "digests"
+    assert st["scores"].tobytes() == o.scores.tobytes(), "scores"
+    assert st["values"].tobytes() == o.values.tobytes(), "values"
+    assert np.array_equal(st["occupancy"], o.occupancy), "occupancy"
+    assert st["size"] == o.size(), "size"
+    assert st["clock"] == o.clock, "clock"
+    assert st["fel"] == o.first_eviction_lambda, "first_eviction_lambda"
+
+
+@pytest.mark.parametrize("path", CASE_FILES, ids=[os.path.basename(p)[:-4] for p in CASE_FILES])
+def test_replays_reference_fixture(hkv, path):
+    """Every op of a script recorded from the reference itself."""
+    meta, ops, state, ctr = load_case(path)
+    t = make_table(hkv, meta["capacity"], meta["dim"], meta["mode"], meta["policy"], meta["budget"],
+                   meta["unified"], overflow_in_hbm=False)
+    assert replay(t, ops) is None
+    st = t.export_state()
+    for name in ("keys", "digests", "scores", "occupancy", "values"):
+        assert st[name].tobytes() == state[name].tobytes(), name
+    assert st["size"] == int(state["size"])
+    assert st["clock"] == int(state["clock"])
+    fel = st["fel"]
+    assert (-1.0 if fel is None else fel) == float(state["fel"])
+    assert t.counters.as_dict() == ctr
+    assert t.check_consistency()
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("policy", POLICIES)
+def test_oracle_differential_contended(hkv, mode, policy):
+    """Random scripts with heavy bucket contention and in-batch duplicates."""
+    cap, dim = 128 * 64, 8
+    t = make_table(hkv, cap, dim, mode, policy, budget=16, overflow_in_hbm=(policy == "kLfu"))
+    o = OracleTable(cap, dim, mode, policy, 16)
+    for j, (op, a) in enumerate(make_script(100 + 10 * MODES.index(mode) + POLICIES.index(policy), cap, dim, policy, n_batches=40,
+                                            batch=3000, universe_scale=3.0, dup_frac=0.3)):
+        r_t = run_impl(t, op, a)
+        r_o = run_impl(o, op, a)
+        assert outputs_equal(r_o, r_t), f"op {j} {op}"
+    assert_same_state(t, o)
+    assert t.counters.as_dict() == o.counters
+    assert t.check_consistency()
+
+
+def _c1_inputs(cap, dim):
+    from paper_2603_17168_b200.workloads import uniform_distinct_keys
+
+    k0 = uniform_distinct_keys(cap // 2, seed=0)
+    v0 = np.random.default_rng(0).standard_normal((len(k0), dim)).astype(np.float32)
+    k1 = uniform_distinct_keys(cap, 0, stream_offset=2**41)
+    v1 = np.random.default_rng(1).standard_normal((len(k1), dim)).astype(np.float32)
+    return k0, v0, k1, v1
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_c1_config_bit_exact(hkv, mode):
+    """BASELINE config 1: 2^20 slots, dim 8, kLru; prefill to 0.5, a 1M fresh
+    insert_and_evict batch, then a 1M mixed find — all bit-exact."""
+    cap, dim = 2**20, 8
+    k0, v0, k1, v1 = _c1_inputs(cap, dim)
+    t = make_table(hkv, cap, dim, mode)
+    o = OracleTable(cap, dim, mode)
+    assert np.array_equal(t.insert_or_assign(k0, v0), o.insert_or_assign(k0, v0))
+    a = t.insert_and_evict(k1, v1)
+    b = o.insert_and_evict(k1, v1)
+    assert all(x.tobytes() == y.tobytes() for x, y in zip(a, b))
+    q = np.concatenate([k0[::3], k1[::2], k1[1::7] + np.uint64(1)])
+    ft, vt = t.find(q)
+    fo, vo = o.find(q)
+    assert np.array_equal(ft, fo) and vt.tobytes() == vo.tobytes()
+    assert_same_state(t, o)
+    assert t.counters.as_dict() == o.counters
+
+
+def test_torch_io_matches_numpy_io(hkv):
+    cap, dim = 2**16, 64
+    t = make_table(hkv, cap, dim)
+    o = OracleTable(cap, dim)
+    rng = np.random.default_rng(3)
+    keys = rng.integers(1, 2**63, size=50_000, dtype=np.uint64)
+    vals = rng.standard_normal((len(keys), dim)).astype(np.float32)
+    kd = torch.from_numpy(keys.view(np.int64)).cuda().view(torch.uint64)
+    vd = torch.from_numpy(vals).cuda()
+    out_t = t.insert_or_assign(kd, vd)
+    out_o = o.insert_or_assign(keys, vals)
+    assert np.array_equal(out_t.cpu().numpy(), out_o)
+    f, v = t.find(kd)
+    fo, vo = o.find(keys)
+    assert np.array_equal(f.cpu().numpy(), fo) and v.cpu().numpy().tobytes() == vo.tobytes()
+    # int64 view of the same keys is accepted bit-identically
+    f2, v2 = t.find(kd.view(torch.int64))
+    assert torch.equal(f, f2) and torch.equal(v, v2)
+
+
+def test_sentinel_keys_raise_without_mutation(hkv):
+    t = make_table(hkv, 1024, 4)
+    good = np.arange(1, 11, dtype=np.uint64)
+    t.insert_or_assign(good, np.ones((10, 4), np.float32))
+    before = t.export_state()
+    bad = torch.tensor([5, -2, 7], dtype=torch.int64, device="cuda")  # -2 == LOCKED
+    with pytest.raises(ValueError):
+        t.insert_or_assign(bad, torch.zeros((3, 4), device="cuda"))
+    with pytest.raises(ValueError):
+        t.erase(bad)
+    with pytest.raises(ValueError):
+        t.insert_or_assign(np.array([1, 2**64 - 1], dtype=np.uint64), np.zeros((2, 4), np.float32))
+    after = t.export_state()
+    for k in ("keys", "digests", "scores", "values"):
+        assert before[k].tobytes() == after[k].tobytes()
+    assert before["clock"] == after["clock"] and before["size"] == after["size"]
+    # the table keeps working afterwards
+    assert np.array_equal(t.contains(good), np.ones(10, bool))
+
+
+def test_empty_batches(hkv):
+    t = make_table(hkv, 1024, 4)
+    e = np.zeros(0, dtype=np.uint64)
+    v = np.zeros((0, 4), np.float32)
+    assert len(t.insert_or_assign(e, v)) == 0
+    o, ek, ev, es = t.insert_and_evict(e, v)
+    assert len(o) == len(ek) == len(ev) == len(es) == 0
+    f, out = t.find(e)
+    assert len(f) == 0 and out.shape == (0, 4)
+    assert len(t.erase(e)) == 0 and len(t.assign(e, v)) == 0
+    assert t.size() == 0
+
+
+def test_tiered_values_pinned_host(hkv):
+    """Values of buckets >= fast_tier_budget live in mapped pinned host memory."""
+    cap, dim = 2**15, 128
+    budget = (cap // 128) // 2
+    t = make_table(hkv, cap, dim, budget=budget)
+    o = OracleTable(cap, dim, fast_tier_budget=budget)
+    rng = np.random.default_rng(9)
+    keys = rng.integers(1, 2**63, size=cap, dtype=np.uint64)
+    vals = rng.standard_normal((cap, dim)).astype(np.float32)
+    assert np.array_equal(t.insert_or_assign(keys, vals), o.insert_or_assign(keys, vals))
+    assert np.array_equal(t.assign(keys[::2], vals[1::2]), o.assign(keys[::2], vals[1::2]))
+    f1, t1, off1 = t.find_ptr(keys)
+    f2, t2, off2 = o.find_ptr(keys)
+    assert np.array_equal(f1, f2) and np.array_equal(t1, t2) and np.array_equal(off1, off2)
+    assert t1.any() and (~t1.astype(bool)[f1]).any()
+    ft, vt = t.find(keys)
+    fo, vo = o.find(keys)
+    assert np.array_equal(ft, fo) and vt.tobytes() == vo.tobytes()
+    assert t.counters.as_dict() == o.counters
+    assert_same_state(t, o)
+
+
+def test_export_native_and_callable_predicates(hkv):
+    cap, dim = 2**14, 4
+    t = make_table(hkv, cap, dim, policy="kCustomized")
+    o = OracleTable(cap, dim, score_policy="kCustomized")
+    rng = np.random.default_rng(5)
+    keys = rng.integers(1, 2**63, size=cap, dtype=np.uint64)
+    vals = rng.standard_normal((cap, dim)).astype(np.float32)
+    sc = rng.integers(0, 100, size=cap, dtype=np.uint64)
+    t.insert_or_assign(keys, vals, sc)
+    o.insert_or_assign(keys, vals, sc)
+    for cursor, mc, ms in ((0, 10**9, None), (0, 777, 50), (5000, 3, 0), (cap - 1, 5, None), (123, 4096, 99)):
+        a = t.export_batch_if(ms, cursor, mc)
+        b = o.export_batch_if(ms, cursor, mc)
+        assert a[3] == b[3]
+        assert all(x.tobytes() == y.tobytes() for x, y in zip(a[:3], b[:3]))
+    # callable predicate (reference contract: numpy (keys, scores) chunk -> mask)
+    a = t.export_batch_if(lambda k, s: (s % np.uint64(3)) == 0, 0, 10**9)
+    full = o.export_batch_if(None, 0, 10**9)
+    m = (full[2] % np.uint64(3)) == 0
+    assert np.array_equal(a[0], full[0][m]) and np.array_equal(a[2], full[2][m])
+    assert a[1].tobytes() == full[1][m].tobytes()
+
+
+def test_snapshot_restore(hkv):
+    cap, dim = 2**14, 16
+    t = make_table(hkv, cap, dim)
+    rng = np.random.default_rng(1)
+    k = rng.integers(1, 2**63, size=cap // 2, dtype=np.uint64)
+    t.insert_or_assign(k, np.ones((len(k), dim), np.float32))
+    t.snapshot()
+    s0 = t.export_state()
+    t.insert_or_assign(k + np.uint64(1), np.ones((len(k), dim), np.float32))
+    t.restore()
+    s1 = t.export_state()
+    for name in ("keys", "digests", "scores", "occupancy"):
+        assert s0[name].tobytes() == s1[name].tobytes()
+    assert s0["size"] == s1["size"] and s0["clock"] == s1["clock"]
+
+
+def test_full_size_properties_dim64(hkv):
+    """C2-shaped (2^24 slots here), dim 64: fill to lambda=1 by 1M batches and
+    check size-independent properties: consistency, every resident key found
+    with the value it was written with, evicted + resident = offered."""
+    cap, dim, batch = 2**24, 64, 2**20
+    t = make_table(hkv, cap, dim)
+    offered = 0
+    total_ev = 0
+    seed_base = 2**40
+    while offered < cap + 2 * batch:
+        keys = torch.arange(seed_base + offered, seed_base + offered + batch, device="cuda", dtype=torch.int64)
+        vals = (keys.to(torch.float32) / 1e12).unsqueeze(1).expand(batch, dim).contiguous()
+        o, ek, ev, es = t.insert_and_evict(keys, vals)
+        oc = torch.bincount(o.long(), minlength=7).cpu()
+        total_ev += int(oc[3])
+        assert int(oc[2]) == 0  # LRU with fresh ticks never rejects
+        assert ek.numel() == int(oc[3])
+        offered += batch
+    assert t.size() == offered - total_ev  # every insert is Inserted or Evicted; nothing lost
+    assert t.check_consistency()
+    res = torch.from_numpy(t.occupied_keys().view(np.int64)).cuda()
+    f, v = t.find(res)
+    assert bool(f.all())
+    expect = (res.to(torch.float32) / 1e12).unsqueeze(1).expand(-1, dim)
+    assert torch.equal(v, expect)
+    assert res.numel() == t.size()
