@@ -102,9 +102,12 @@ int hkv_upsert(hkv_table *t, int32_t op, const uint64_t *keys, float *values,
                const uint64_t *ticks, uint64_t clock_advance, hkv_stream stream);
 
 /* assign (table.py:438-442) when values != NULL; assign_scores (444-449) with
- * explicit scores (kCustomized) or refresh != 0.  Last duplicate wins. */
+ * explicit scores (kCustomized) or refresh != 0.  Last duplicate wins.
+ * Refresh ticks: NULL -> clock + (found keys before i) + 1 and clock += found
+ * (table.py:481-483); else ticks[i] for found keys and clock += clock_advance. */
 int hkv_assign(hkv_table *t, const uint64_t *keys, const float *values, const uint64_t *scores,
-               int32_t refresh, int64_t n, uint8_t *outcomes, hkv_stream stream);
+               int32_t refresh, int64_t n, uint8_t *outcomes, const uint64_t *ticks,
+               uint64_t clock_advance, hkv_stream stream);
 
 /* erase (table.py:553-558, 1006-1023). */
 int hkv_erase(hkv_table *t, const uint64_t *keys, int64_t n, uint8_t *outcomes, hkv_stream stream);
@@ -165,6 +168,14 @@ int hkv_route(const uint64_t *keys, int64_t n, int64_t global_buckets, int32_t w
 
 /* Launch-count instrumentation: number of kernels this library has launched. */
 int64_t hkv_launch_count(void);
+
+/* Live kernel timing for roofline reporting: while enabled, the dominant
+ * kernel of each op (probe / apply / assign-apply) is bracketed by CUDA
+ * events on its launch stream.  hkv_kernel_times() synchronises, returns the
+ * accumulated milliseconds and launch count of the kernel named `name`
+ * ("find", "apply", "dual_rounds", "assign_apply") and resets it. */
+int hkv_set_kernel_timing(int32_t enable);
+int hkv_kernel_times(const char *name, double *ms, int64_t *launches);
 
 #ifdef __cplusplus
 }

@@ -174,14 +174,16 @@ typedef struct {
 static void *find_worker(void *arg) {
     find_job *j = (find_job *)arg;
     ot_table *t = j->t;
+    int64_t ctr[6] = {0}; /* thread-local: no false sharing between jobs */
     for (int64_t i = j->lo; i < j->hi; i++) {
-        int64_t row = lookup_row(t, j->keys[i], j->ctr);
+        int64_t row = lookup_row(t, j->keys[i], ctr);
         j->found[i] = row >= 0;
         if (row >= 0) {
             if (j->out) memcpy(j->out + i * t->dim, t->values + row * t->dim, sizeof(float) * t->dim);
-            count_row(t, row, j->ctr);
+            count_row(t, row, ctr);
         }
     }
+    memcpy(j->ctr, ctr, sizeof(ctr));
     return NULL;
 }
 
@@ -404,7 +406,8 @@ int64_t ot_upsert(ot_table *t, int32_t op, const uint64_t *keys, float *values,
  * key in found order, table.py:481-483). values and scores may be NULL;
  * refresh != 0 requests the policy refresh. */
 void ot_assign(ot_table *t, const uint64_t *keys, const float *values, const uint64_t *scores,
-               int32_t refresh, int64_t n, uint8_t *outcomes) {
+               int32_t refresh, int64_t n, uint8_t *outcomes, const uint64_t *ticks,
+               uint64_t clock_advance) {
     int64_t ctr[6] = {0};
     int64_t *rows = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
     int64_t nfound = 0;
@@ -414,7 +417,7 @@ void ot_assign(ot_table *t, const uint64_t *keys, const float *values, const uin
         if (rows[i] >= 0) nfound++;
     }
     uint64_t clock0 = t->clock;
-    if (refresh && !scores) t->clock += (uint64_t)nfound;
+    if (refresh && !scores) t->clock += ticks ? clock_advance : (uint64_t)nfound;
     int64_t rank = 0;
     for (int64_t i = 0; i < n; i++) {
         int64_t row = rows[i];
@@ -426,7 +429,7 @@ void ot_assign(ot_table *t, const uint64_t *keys, const float *values, const uin
         if (scores) {
             t->scores[row] = scores[i];
         } else if (refresh) {
-            uint64_t tick = clock0 + (uint64_t)rank + 1;
+            uint64_t tick = ticks ? ticks[i] : clock0 + (uint64_t)rank + 1;
             t->scores[row] = hit_score(t->policy, t->scores[row], t->epoch, tick, 0, 0);
         }
         rank++;
@@ -492,3 +495,44 @@ uint64_t ot_epoch(ot_table *t) { return t->epoch; }
 void ot_set_epoch(ot_table *t, uint64_t e) { t->epoch = e; }
 int32_t ot_fel(ot_table *t, double *out) { *out = t->fel; return t->fel_set; }
 void ot_set_fel(ot_table *t, int32_t set, double v) { t->fel_set = set; t->fel = v; }
+
+/* Metadata snapshot / restore for the CPU baseline (keeps lambda fixed
+ * between timed batches; values are payload and not restored). */
+typedef struct {
+    uint64_t *keys, *scores;
+    uint8_t *digests;
+    int64_t *occ;
+    int64_t size;
+    uint64_t clock;
+} ot_snap;
+
+ot_snap *ot_snapshot(const ot_table *t) {
+    ot_snap *s = (ot_snap *)calloc(1, sizeof(ot_snap));
+    if (!s) return NULL;
+    s->keys = (uint64_t *)malloc(sizeof(uint64_t) * t->capacity);
+    s->scores = (uint64_t *)malloc(sizeof(uint64_t) * t->capacity);
+    s->digests = (uint8_t *)malloc(t->capacity);
+    s->occ = (int64_t *)malloc(sizeof(int64_t) * t->buckets);
+    if (!s->keys || !s->scores || !s->digests || !s->occ) return NULL;
+    memcpy(s->keys, t->keys, sizeof(uint64_t) * t->capacity);
+    memcpy(s->scores, t->scores, sizeof(uint64_t) * t->capacity);
+    memcpy(s->digests, t->digests, t->capacity);
+    memcpy(s->occ, t->occ, sizeof(int64_t) * t->buckets);
+    s->size = t->size;
+    s->clock = t->clock;
+    return s;
+}
+
+void ot_restore(ot_table *t, const ot_snap *s) {
+    memcpy(t->keys, s->keys, sizeof(uint64_t) * t->capacity);
+    memcpy(t->scores, s->scores, sizeof(uint64_t) * t->capacity);
+    memcpy(t->digests, s->digests, t->capacity);
+    memcpy(t->occ, s->occ, sizeof(int64_t) * t->buckets);
+    t->size = s->size;
+    t->clock = s->clock;
+}
+
+void ot_snap_free(ot_snap *s) {
+    if (!s) return;
+    free(s->keys); free(s->scores); free(s->digests); free(s->occ); free(s);
+}

@@ -61,7 +61,7 @@ def lib():
         L.ot_upsert.restype = C.c_int64
         L.ot_upsert.argtypes = [C.c_void_p, C.c_int32, _u64p, _f32p, _u64p, C.c_int64, _u8p,
                                 _u64p, _f32p, _u64p, _u64p, C.c_uint64]
-        L.ot_assign.argtypes = [C.c_void_p, _u64p, _f32p, _u64p, C.c_int32, C.c_int64, _u8p]
+        L.ot_assign.argtypes = [C.c_void_p, _u64p, _f32p, _u64p, C.c_int32, C.c_int64, _u8p, _u64p, C.c_uint64]
         L.ot_erase.argtypes = [C.c_void_p, _u64p, C.c_int64, _u8p]
         L.ot_export.restype = C.c_int64
         L.ot_export.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_uint64, _u64p,
@@ -82,6 +82,10 @@ def lib():
         L.ot_fel.restype = C.c_int32
         L.ot_fel.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
         L.ot_set_fel.argtypes = [C.c_void_p, C.c_int32, C.c_double]
+        L.ot_snapshot.restype = C.c_void_p
+        L.ot_snapshot.argtypes = [C.c_void_p]
+        L.ot_restore.argtypes = [C.c_void_p, C.c_void_p]
+        L.ot_snap_free.argtypes = [C.c_void_p]
     return _lib
 
 
@@ -135,6 +139,10 @@ class OracleTable:
 
     def __del__(self):
         h = getattr(self, "_h", None)
+        sn = getattr(self, "_snap", None)
+        if sn:
+            lib().ot_snap_free(sn)
+            self._snap = None
         if h:
             lib().ot_destroy(h)
             self._h = None
@@ -142,6 +150,16 @@ class OracleTable:
     def clone(self) -> "OracleTable":
         return OracleTable(self.capacity, self.dim, self.mode, self.policy, self.fast_tier_budget,
                            self.digest_filter, self.admit_ties_unified, _handle=lib().ot_clone(self._h))
+
+    def snapshot(self):
+        """Metadata snapshot (keys, digests, scores, occupancy, size, clock)."""
+        old = getattr(self, "_snap", None)
+        if old:
+            lib().ot_snap_free(old)
+        self._snap = lib().ot_snapshot(self._h)
+
+    def restore(self):
+        lib().ot_restore(self._h, self._snap)
 
     # ----- raw state views (numpy views into the C arrays) ------------------------
     @property
@@ -303,14 +321,16 @@ class OracleTable:
         k = self._keys(keys)
         v = self._values(values, len(k))
         out = np.zeros(len(k), dtype=np.uint8)
-        lib().ot_assign(self._h, _p(k, _u64p), _p(v, _f32p), None, 0, len(k), _p(out, _u8p))
+        lib().ot_assign(self._h, _p(k, _u64p), _p(v, _f32p), None, 0, len(k), _p(out, _u8p), None, 0)
         return out
 
-    def assign_scores(self, keys, scores=None):
+    def assign_scores(self, keys, scores=None, ticks=None, clock_advance=0):
         k = self._keys(keys)
         s = self._scores(scores, len(k))
         out = np.zeros(len(k), dtype=np.uint8)
-        lib().ot_assign(self._h, _p(k, _u64p), None, _p(s, _u64p), int(scores is None), len(k), _p(out, _u8p))
+        t = None if ticks is None else np.ascontiguousarray(ticks, dtype=np.uint64)
+        lib().ot_assign(self._h, _p(k, _u64p), None, _p(s, _u64p), int(scores is None), len(k), _p(out, _u8p),
+                        _p(t, _u64p), clock_advance)
         return out
 
     def erase(self, keys):

@@ -45,7 +45,7 @@ SIGNATURES = {
     "hkv_contains": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "hkv_find_ptr": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "hkv_upsert": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _u64, _vp]),
-    "hkv_assign": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp]),
+    "hkv_assign": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _u64, _vp]),
     "hkv_erase": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "hkv_export": (C.c_int, [_vp, _i64, _i64, _i32, _u64, _vp, _i64, _vp, _vp, _vp,
                              C.POINTER(_i64), C.POINTER(_i64), _vp]),
@@ -63,6 +63,8 @@ SIGNATURES = {
     "hkv_restore": (C.c_int, [_vp, _vp]),
     "hkv_check_consistency": (C.c_int, [_vp, C.POINTER(_i32), _vp]),
     "hkv_route": (C.c_int, [_vp, _i64, _i64, _i32, _vp, _vp, _vp]),
+    "hkv_set_kernel_timing": (C.c_int, [_i32]),
+    "hkv_kernel_times": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(_i64)]),
 }
 
 _lib = None

@@ -8,13 +8,55 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/hkv_b200.h"
 #include "hkv_kernels.h"
 
 namespace hkv {
 unsigned long long g_launches = 0;
+
+namespace {
+struct KTimer {
+  std::mutex mu;
+  bool enabled = false;
+  struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  std::map<cudaStream_t, std::vector<Pending>> open;  // begun, awaiting end
+  std::vector<Pending> done;
+};
+KTimer& ktimer() {
+  static KTimer k;
+  return k;
 }
+}  // namespace
+
+void ktimer_begin(const char* name, cudaStream_t s) {
+  KTimer& k = ktimer();
+  std::lock_guard<std::mutex> g(k.mu);
+  if (!k.enabled) return;
+  KTimer::Pending p;
+  p.name = name;
+  cudaEventCreate(&p.a);
+  cudaEventCreate(&p.b);
+  cudaEventRecord(p.a, s);
+  k.open[s].push_back(p);
+}
+
+void ktimer_end(const char* name, cudaStream_t s) {
+  KTimer& k = ktimer();
+  std::lock_guard<std::mutex> g(k.mu);
+  if (!k.enabled) return;
+  auto& v = k.open[s];
+  if (v.empty()) return;
+  KTimer::Pending p = v.back();
+  v.pop_back();
+  cudaEventRecord(p.b, s);
+  k.done.push_back(p);
+}
+}  // namespace hkv
 
 using namespace hkv;
 
@@ -115,6 +157,40 @@ extern "C" {
 const char* hkv_last_error(void) { return g_err.c_str(); }
 const char* hkv_version(void) { return "hkv_b200 0.1 sm_100a"; }
 int64_t hkv_launch_count(void) { return (int64_t)g_launches; }
+
+int hkv_set_kernel_timing(int32_t enable) {
+  KTimer& k = ktimer();
+  std::lock_guard<std::mutex> g(k.mu);
+  k.enabled = enable != 0;
+  return HKV_OK;
+}
+
+int hkv_kernel_times(const char* name, double* ms, int64_t* launches) {
+  if (!name || !ms || !launches) return fail(HKV_EINVAL, "null argument");
+  KTimer& k = ktimer();
+  std::lock_guard<std::mutex> g(k.mu);
+  double tot = 0.0;
+  int64_t cnt = 0;
+  std::vector<KTimer::Pending> keep;
+  for (auto& p : k.done) {
+    if (p.name != name) {
+      keep.push_back(p);
+      continue;
+    }
+    cudaError_t e = cudaEventSynchronize(p.b);
+    if (e) return cuda_fail(e, "kernel timing");
+    float f = 0.f;
+    cudaEventElapsedTime(&f, p.a, p.b);
+    tot += f;
+    cnt++;
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  k.done.swap(keep);
+  *ms = tot;
+  *launches = cnt;
+  return HKV_OK;
+}
 
 int hkv_create(const hkv_config* cfg, hkv_table** out) {
   if (!cfg || !out) return fail(HKV_EINVAL, "null argument");
@@ -297,7 +373,7 @@ int hkv_erase(hkv_table* t, const uint64_t* keys, int64_t n, uint8_t* outcomes, 
 }
 
 int hkv_assign(hkv_table* t, const uint64_t* keys, const float* values, const uint64_t* scores, int32_t refresh,
-               int64_t n, uint8_t* outcomes, hkv_stream stream) {
+               int64_t n, uint8_t* outcomes, const uint64_t* ticks, uint64_t clock_advance, hkv_stream stream) {
   CHECK_T();
   const bool custom = t->cfg.score_policy == HKV_CUSTOMIZED;
   if (!values) {
@@ -310,8 +386,8 @@ int hkv_assign(hkv_table* t, const uint64_t* keys, const float* values, const ui
   }
   if (n && (!keys || !outcomes)) return fail(HKV_EINVAL, "null keys/outcomes");
   cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e = run_assign(t->dev, keys, values, scores, refresh, t->epoch, n, outcomes, t->log2b,
-                             t->workspace(s), s, t->num_sms);
+  cudaError_t e = run_assign(t->dev, keys, values, scores, refresh, t->epoch, n, outcomes, ticks, clock_advance,
+                             t->log2b, t->workspace(s), s, t->num_sms);
   return e ? cuda_fail(e, "hkv_assign") : HKV_OK;
 }
 

@@ -142,9 +142,11 @@ static void launch_find_mode(const TableDev& t, const uint64_t* keys, int64_t n,
 void launch_find(const TableDev& t, const uint64_t* keys, int64_t n, float* out, uint8_t* found,
                  uint8_t* tier, int64_t* offset, int mode, cudaStream_t s, int num_sms) {
   if (n <= 0) return;
+  ktimer_begin("find", s);
   if (mode == 0) launch_find_mode<0>(t, keys, n, out, found, tier, offset, s, num_sms);
   else if (mode == 1) launch_find_mode<1>(t, keys, n, out, found, tier, offset, s, num_sms);
   else launch_find_mode<2>(t, keys, n, out, found, tier, offset, s, num_sms);
+  ktimer_end("find", s);
 }
 
 }  // namespace hkv

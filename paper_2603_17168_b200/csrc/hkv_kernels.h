@@ -70,7 +70,8 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
 
 cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* values,
                        const uint64_t* scores, int refresh, uint64_t epoch, int64_t n, uint8_t* outcomes,
-                       int log2_buckets, Workspace& ws, cudaStream_t s, int num_sms);
+                       const uint64_t* ticks, uint64_t clock_advance, int log2_buckets, Workspace& ws,
+                       cudaStream_t s, int num_sms);
 
 cudaError_t run_export(const TableDev& t, int64_t cursor, int64_t max_count, int has_min, uint64_t min_score,
                        const uint8_t* mask, int64_t mask_rows, uint64_t* ok, float* ov, uint64_t* os,
@@ -80,6 +81,10 @@ cudaError_t run_bits_from_keys(const TableDev& t, int64_t buckets, cudaStream_t 
 cudaError_t run_consistency(const TableDev& t, int64_t buckets, int* ok_dev, cudaStream_t s);
 cudaError_t run_route(const uint64_t* keys, int64_t n, int64_t global_buckets, int world, int32_t* perm,
                       int64_t* counts, Workspace& ws, cudaStream_t s);
+
+// Live timing of dominant kernels (hkv_set_kernel_timing).
+void ktimer_begin(const char* name, cudaStream_t s);
+void ktimer_end(const char* name, cudaStream_t s);
 
 cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, bool need_ev, bool dual);
 void ws_free(Workspace& ws);

@@ -398,6 +398,7 @@ __global__ void __launch_bounds__(256) k_assign_apply(TableDev t, const float* _
                                                       const uint64_t* __restrict__ scores, int refresh,
                                                       uint64_t epoch, const uint32_t* __restrict__ rows,
                                                       const uint32_t* __restrict__ ranks,
+                                                      const uint64_t* __restrict__ ticks,
                                                       const uint32_t* __restrict__ sb,
                                                       const uint32_t* __restrict__ sidx,
                                                       const uint32_t* __restrict__ seg, int64_t n, Scalars* sc) {
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(256) k_assign_apply(TableDev t, const float* _
           if (scores) {
             t.scores[row] = scores[i];
           } else if (refresh) {
-            const uint64_t tick = clock0 + (uint64_t)ranks[i] + 1;
+            const uint64_t tick = ticks ? ticks[i] : clock0 + (uint64_t)ranks[i] + 1;
             t.scores[row] = hit_score(t.policy, t.scores[row], epoch, tick, false, 0);
           }
         }
@@ -559,9 +560,11 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
     if (!t.dual) {
       if ((e = sort_segments(ws, n, log2_buckets, s))) return e;
       const int64_t blocks = tile_blocks(n, num_sms);
+      ktimer_begin("apply", s);
       if (vec == 4) k_apply_segments<4><<<(unsigned)blocks, 256, 0, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, n);
       else if (vec == 2) k_apply_segments<2><<<(unsigned)blocks, 256, 0, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, n);
       else k_apply_segments<1><<<(unsigned)blocks, 256, 0, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, n);
+      ktimer_end("apply", s);
       g_launches++;
     } else {
       // cooperative grid: all blocks co-resident
@@ -579,7 +582,9 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       uint32_t* p1 = ws.pend;
       int64_t nn = n;
       void* args[] = {&tt, &a, &b1s, &b2s, &p0, &p1, &lead, &round_ctr, &nn};
+      ktimer_begin("dual_rounds", s);
       if ((e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)blocks), dim3(256), args, 0, s))) return e;
+      ktimer_end("dual_rounds", s);
       g_launches++;
     }
   }
@@ -615,12 +620,12 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
 }
 
 cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* values, const uint64_t* scores,
-                       int refresh, uint64_t epoch, int64_t n, uint8_t* outcomes, int log2_buckets,
-                       Workspace& ws, cudaStream_t s, int num_sms) {
+                       int refresh, uint64_t epoch, int64_t n, uint8_t* outcomes, const uint64_t* ticks,
+                       uint64_t clock_advance, int log2_buckets, Workspace& ws, cudaStream_t s, int num_sms) {
   cudaError_t e;
   if ((e = ws_reserve(ws, n, t.dim, false, false))) return e;
   if ((e = cudaMemsetAsync(ws.sc, 0, sizeof(Scalars), s))) return e;
-  const bool need_ticks = refresh && !scores;
+  const bool need_ticks = refresh && !scores && !ticks;
   if (n > 0) {
     k_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(t, keys, n, ws.bkt, ws.idx, nullptr, ws.sc);
     g_launches++;
@@ -639,18 +644,21 @@ cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* val
     }
     if ((e = sort_segments(ws, n, log2_buckets, s))) return e;
     const int vec = vec_of(t.dim, values, t.vfast, t.vover, nullptr);
+    ktimer_begin("assign_apply", s);
     if (vec == 4)
-      k_assign_apply<4><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ws.sbkt,
+      k_assign_apply<4><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks, ws.sbkt,
                                                          ws.sidx, ws.seg, n, ws.sc);
     else if (vec == 2)
-      k_assign_apply<2><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ws.sbkt,
+      k_assign_apply<2><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks, ws.sbkt,
                                                          ws.sidx, ws.seg, n, ws.sc);
     else
-      k_assign_apply<1><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ws.sbkt,
+      k_assign_apply<1><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks, ws.sbkt,
                                                          ws.sidx, ws.seg, n, ws.sc);
+    ktimer_end("assign_apply", s);
     g_launches++;
   }
-  k_finalize<<<1, 1024, 0, s>>>(t, ws.sc, nullptr, n, 0, need_ticks ? 1 : 0);
+  k_finalize<<<1, 1024, 0, s>>>(t, ws.sc, nullptr, n, (refresh && !scores && ticks) ? clock_advance : 0,
+                                need_ticks ? 1 : 0);
   g_launches++;
   return cudaGetLastError();
 }

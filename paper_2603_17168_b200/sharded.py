@@ -1,0 +1,256 @@
+"""Hash-sharded CacheTable across the GPUs of one box.
+
+The reference leaves sharding to the application;
+this is the B200 build's multi-GPU layer.  One process per GPU.
+
+Layout: contiguous bucket ranges.  A key's global bucket is
+gb = fmix64(key) & (B_global - 1); rank = gb >> log2(B_local); the local bucket
+is gb & (B_local - 1) = fmix64(key) & (B_local - 1), which is exactly what the
+rank's local CacheTable computes.  The sharded table is therefore
+bucket-for-bucket identical to one global table of the same capacity, and
+the CPU oracle at the global capacity checks it bit-exactly.
+
+Global batch order is rank-major (rank 0's batch, then rank 1's, ...).  Each
+op travels to its owner in one all-to-all (keys + values + scores + explicit
+LRU ticks = clock + global index + 1); a shard receives the segments in source
+rank order, each in source batch order, so applying them in received order is
+the global serial order restricted to the shard.  Results return in a second
+all-to-all and are scattered back through the inverse routing permutation.
+Every rank advances its clock by the global batch size, so all shards share
+one logical clock.  size() is an all-reduce.
+
+Dual mode is not sharded (a key's two buckets may live on different ranks):
+run dual-mode tables as per-GPU replicas.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import Callable, Optional
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .table import CacheTable, Mode, Outcome, TableConfig
+
+_EVICTED = int(Outcome.Evicted)
+_UPDATED = int(Outcome.Updated)
+
+
+def cuda_router(keys: torch.Tensor, global_buckets: int, world: int):
+    """Stable grouping of keys by owner rank on the GPU (hkv_route kernel)."""
+    from . import _lib
+
+    lib = _lib.load()
+    n = keys.numel()
+    perm = torch.empty(n, dtype=torch.int32, device=keys.device)
+    counts = torch.empty(world, dtype=torch.int64, device=keys.device)
+    _lib.check(lib.hkv_route(C.c_void_p(keys.data_ptr()), n, global_buckets, world, C.c_void_p(perm.data_ptr()),
+                             C.c_void_p(counts.data_ptr()),
+                             C.c_void_p(torch.cuda.current_stream(keys.device).cuda_stream)))
+    return perm.long(), counts
+
+
+class ShardedCacheTable:
+    def __init__(self, config: TableConfig, group=None, local_factory: Optional[Callable] = None,
+                 router: Optional[Callable] = None):
+        if config.mode is not Mode.single:
+            raise ValueError("sharded tables support single mode only (dual mode: per-GPU replicas)")
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.config = config
+        bg = config.bucket_count
+        if self.world & (self.world - 1) or bg % self.world:
+            raise ValueError("world size must be a power of two dividing the bucket count")
+        self.global_buckets = bg
+        bl = bg // self.world
+        lo = self.rank * bl
+        budget = min(max(config.fast_tier_budget - lo, 0), bl)
+        local_cfg = dataclasses.replace(config, capacity=config.capacity // self.world, fast_tier_budget=budget)
+        self.local = (local_factory or CacheTable)(local_cfg)
+        self.router = router or cuda_router
+        self.clock = 0  # the global logical clock; every rank holds the same value
+
+    # ----- exchange plumbing ----------------------------------------------------
+    def _splits(self, counts: torch.Tensor):
+        recv = torch.empty_like(counts)
+        dist.all_to_all_single(recv, counts, group=self.group)
+        return counts.tolist(), recv.tolist()
+
+    def _a2a(self, x: torch.Tensor, send_splits, recv_splits):
+        out = torch.empty((sum(recv_splits),) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        dist.all_to_all_single(out, x.contiguous(), recv_splits, send_splits, group=self.group)
+        return out
+
+    def _route(self, keys: torch.Tensor):
+        perm, counts = self.router(keys, self.global_buckets, self.world)
+        send, recv = self._splits(counts)
+        return perm, send, recv
+
+    def _unpermute(self, routed_back: torch.Tensor, perm: torch.Tensor):
+        out = torch.empty_like(routed_back)
+        out[perm] = routed_back
+        return out
+
+    def _global_offsets(self, n: int, device):
+        t = torch.tensor([n], dtype=torch.int64, device=device)
+        allv = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(allv, t, group=self.group)
+        sizes = [int(x.item()) for x in allv]
+        return sum(sizes[: self.rank]), sum(sizes)
+
+    @staticmethod
+    def _u8(x: torch.Tensor):
+        return x.to(torch.uint8) if x.dtype == torch.bool else x
+
+    # ----- reader ops -----------------------------------------------------------
+    def find(self, keys: torch.Tensor):
+        perm, send, recv = self._route(keys)
+        rk = self._a2a(keys[perm], send, recv)
+        f, v = self.local.find(rk)
+        fb = self._a2a(self._u8(f), recv, send)
+        vb = self._a2a(v, recv, send)
+        return self._unpermute(fb, perm).bool(), self._unpermute(vb, perm)
+
+    def contains(self, keys: torch.Tensor):
+        perm, send, recv = self._route(keys)
+        rk = self._a2a(keys[perm], send, recv)
+        f = self.local.contains(rk)
+        return self._unpermute(self._a2a(self._u8(f), recv, send), perm).bool()
+
+    def size(self) -> int:
+        s = torch.tensor([self.local.size()], dtype=torch.int64,
+                         device=getattr(self.local, "device", torch.device("cpu")))
+        dist.all_reduce(s, group=self.group)
+        return int(s.item())
+
+    def load_factor(self) -> float:
+        return self.size() / self.config.capacity
+
+    # ----- inserter ops ---------------------------------------------------------
+    def _ticks(self, n: int, device):
+        off, total = self._global_offsets(n, device)
+        ticks = torch.arange(n, dtype=torch.int64, device=device) + (self.clock + off + 1)
+        return ticks, total
+
+    def _upsert(self, op: str, keys, values, scores):
+        n = keys.numel()
+        ticks, total = self._ticks(n, keys.device)
+        perm, send, recv = self._route(keys)
+        rk = self._a2a(keys[perm], send, recv)
+        rv = self._a2a(values[perm], send, recv)
+        rs = None if scores is None else self._a2a(scores[perm], send, recv)
+        rt = self._a2a(ticks[perm], send, recv)
+        res = None
+        if op == "insert_or_assign":
+            o = self.local.insert_or_assign(rk, rv, rs, ticks=rt, clock_advance=total)
+        elif op == "find_or_insert":
+            o = self.local.find_or_insert(rk, rv, rs, ticks=rt, clock_advance=total)
+            vb = self._a2a(rv, recv, send)
+            values[perm] = vb
+        else:  # insert_and_evict
+            o, ek, ev, es = self.local.insert_and_evict(rk, rv, rs, ticks=rt, clock_advance=total)
+            # evicted tuples per source rank, in received (= source batch) order
+            is_ev = (o == _EVICTED)
+            seg = torch.repeat_interleave(torch.arange(self.world, device=o.device),
+                                          torch.tensor(recv, device=o.device), output_size=o.numel())
+            ev_send = torch.bincount(seg[is_ev], minlength=self.world).to(torch.int64)
+            es_split, er_split = self._splits(ev_send)
+            bk = self._a2a(ek.view(torch.int64), es_split, er_split)
+            bv = self._a2a(ev, es_split, er_split)
+            bs = self._a2a(es.view(torch.int64), es_split, er_split)
+            res = (bk, bv, bs)
+        self.clock += total
+        ob = self._a2a(o, recv, send)
+        outcomes = self._unpermute(ob, perm)
+        if res is None:
+            return outcomes
+        # entries arrive grouped by shard in routed order; restore batch order
+        routed_ev = torch.nonzero(ob == _EVICTED).flatten()
+        order = torch.argsort(perm[routed_ev])
+        bk, bv, bs = res
+        return outcomes, bk[order].view(torch.uint64), bv[order], bs[order].view(torch.uint64)
+
+    def insert_or_assign(self, keys, values, scores=None):
+        return self._upsert("insert_or_assign", keys, values, scores)
+
+    def insert_and_evict(self, keys, values, scores=None):
+        return self._upsert("insert_and_evict", keys, values, scores)
+
+    def find_or_insert(self, keys, values_inout, scores=None):
+        return self._upsert("find_or_insert", keys, values_inout, scores)
+
+    def erase(self, keys):
+        perm, send, recv = self._route(keys)
+        rk = self._a2a(keys[perm], send, recv)
+        o = self.local.erase(rk)
+        return self._unpermute(self._a2a(o, recv, send), perm)
+
+    # ----- updater ops ----------------------------------------------------------
+    def assign(self, keys, values):
+        perm, send, recv = self._route(keys)
+        rk = self._a2a(keys[perm], send, recv)
+        rv = self._a2a(values[perm], send, recv)
+        o = self.local.assign(rk, rv)
+        return self._unpermute(self._a2a(o, recv, send), perm)
+
+    def assign_scores(self, keys, scores=None):
+        perm, send, recv = self._route(keys)
+        rk = self._a2a(keys[perm], send, recv)
+        if scores is not None:
+            rs = self._a2a(scores[perm], send, recv)
+            o = self.local.assign_scores(rk, rs)
+            return self._unpermute(self._a2a(o, recv, send), perm)
+        # refresh: ticks follow the GLOBAL found order (table.py:481-483)
+        f = self._unpermute(self._a2a(self._u8(self.local.contains(rk)), recv, send), perm).bool()
+        nf = int(f.sum().item())
+        off, total = self._global_offsets(nf, keys.device)
+        rank_in_batch = torch.cumsum(f.to(torch.int64), 0) - 1
+        ticks = rank_in_batch + (self.clock + off + 1)
+        rt = self._a2a(ticks[perm], send, recv)
+        o = self.local.assign_scores(rk, None, ticks=rt, clock_advance=total)
+        self.clock += total
+        return self._unpermute(self._a2a(o, recv, send), perm)
+
+    # ----- export (global rows are rank-major) ----------------------------------
+    def export_batch_if(self, min_score, cursor, max_count: int):
+        """Global export_batch_if over rank-major rows (table.py:374-434).
+        Ranks answer in order, each with the room the previous ones left."""
+        cap_l = self.config.capacity // self.world
+        cursor = 0 if cursor is None else cursor
+        if not (0 <= cursor < self.config.capacity):
+            raise ValueError("cursor out of range")
+        if max_count < 1:
+            raise ValueError("max_count must be >= 1")
+        ks, vs, ss = [], [], []
+        taken = 0
+        nxt = None
+        for r in range(self.world):
+            lo = r * cap_l
+            if cursor >= lo + cap_l:
+                continue
+            payload = None
+            if self.rank == r:
+                k, v, s, n = self.local.export_batch_if(min_score, max(cursor - lo, 0), max_count - taken)
+                payload = (np.asarray(k), np.asarray(v), np.asarray(s), None if n is None else n + lo)
+            box = [payload]
+            dist.broadcast_object_list(box, src=r, group=self.group)
+            k, v, s, n = box[0]
+            ks.append(k)
+            vs.append(v)
+            ss.append(s)
+            taken += len(k)
+            if taken >= max_count:
+                if n is not None:
+                    nxt = n
+                elif r + 1 < self.world:
+                    nxt = (r + 1) * cap_l  # the last taken row closed rank r's range
+                break
+        dim = self.config.value_dim
+        keys = np.concatenate(ks) if ks else np.zeros(0, np.uint64)
+        vals = np.concatenate(vs) if vs else np.zeros((0, dim), np.float32)
+        scs = np.concatenate(ss) if ss else np.zeros(0, np.uint64)
+        return keys, vals, scs, nxt

@@ -159,18 +159,23 @@ class CacheTable:
         return C.c_void_p(self._stream().cuda_stream)
 
     def _keys_in(self, keys):
-        """-> (device u64-as-int64 tensor, was_numpy).  Host inputs are validated
-        on the host exactly as table.py:164-170."""
+        """-> (device u64-as-int64 tensor, io mode).  io mode is True for numpy
+        inputs (outputs returned as numpy, like the reference), "host" for CPU
+        torch tensors (outputs returned as CPU tensors), False for tensors on the
+        table's device.  Host inputs are validated on the host exactly as
+        table.py:164-170; device inputs on the device (error latch)."""
         if isinstance(keys, torch.Tensor):
             if keys.dim() != 1:
                 raise ValueError("keys must be one-dimensional")
             if keys.dtype not in (torch.int64, torch.uint64):
                 raise ValueError("keys must be uint64 (or bit-identical int64)")
+            mode = False
             if keys.device != self.device:
                 if keys.device.type == "cpu":
                     self._host_key_check(keys.view(torch.int64).numpy().view(np.uint64))
+                    mode = "host"
                 keys = keys.to(self.device, non_blocking=True)
-            return keys.contiguous().view(torch.int64), False
+            return keys.contiguous().view(torch.int64), mode
         k = np.ascontiguousarray(keys, dtype=np.uint64)
         if k.ndim != 1:
             raise ValueError("keys must be one-dimensional")
@@ -217,12 +222,16 @@ class CacheTable:
         if bits.value & 1:
             raise ValueError("keys must not equal a reserved sentinel value")
 
-    @staticmethod
-    def _out(t: torch.Tensor, numpy_mode: bool, dtype=None):
-        if not numpy_mode:
-            return t if dtype is None else t.view(dtype)
-        a = t.cpu().numpy()
-        return a if dtype is None else a.view(dtype)
+    def _out(self, t: torch.Tensor, mode, dtype=None):
+        if mode is True:
+            a = t.cpu().numpy()
+            return a if dtype is None else a.view(dtype)
+        if mode == "host":
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t, non_blocking=True)
+            self._stream().synchronize()
+            return h if dtype is None else h.view(dtype)
+        return t if dtype is None else t.view(dtype)
 
     # ----- reader operations (table.py:304-372) ------------------------------
     def find(self, keys, out=None):
@@ -247,11 +256,18 @@ class CacheTable:
         st = self._stream()
         with self.gate.acquire(Role.Reader, st):
             _lib.check(self._lib.hkv_find(self._h, _ptr(k), n, _ptr(out_d), _ptr(found), self._sp()))
-        if not np_mode:
+        if not np_mode or np_mode == "host":
             self._check_device_error()
             if isinstance(out, torch.Tensor) and out_d is not out:
                 out.copy_(out_d)
-                return found, out
+                return self._out(found, np_mode), out
+            if np_mode == "host":
+                fh = torch.empty(found.shape, dtype=found.dtype, pin_memory=True)
+                vh = torch.empty(out_d.shape, dtype=out_d.dtype, pin_memory=True)
+                fh.copy_(found, non_blocking=True)
+                vh.copy_(out_d, non_blocking=True)
+                self._stream().synchronize()
+                return fh, vh
             return found, out_d
         f = found.cpu().numpy()
         if host_out is not None:
@@ -355,17 +371,18 @@ class CacheTable:
         v = self._values_in(values, k.numel(), np_mode)
         return self._assign_impl(k, v, None, False, np_mode)
 
-    def assign_scores(self, keys, scores=None):
+    def assign_scores(self, keys, scores=None, *, ticks=None, clock_advance: int = 0):
         k, np_mode = self._keys_in(keys)
         s = self._scores_in(scores, k.numel())
-        return self._assign_impl(k, None, s, scores is None, np_mode)
+        return self._assign_impl(k, None, s, scores is None, np_mode, ticks, clock_advance)
 
-    def _assign_impl(self, k, v, s, refresh, np_mode):
+    def _assign_impl(self, k, v, s, refresh, np_mode, ticks=None, clock_advance=0):
         n = k.numel()
         outcomes = torch.empty(n, dtype=torch.uint8, device=self.device)
+        tk = None if ticks is None else ticks.to(self.device).contiguous()
         with self.gate.acquire(Role.Updater, self._stream()):
             _lib.check(self._lib.hkv_assign(self._h, _ptr(k), _ptr(v), _ptr(s), int(refresh), n, _ptr(outcomes),
-                                            self._sp()))
+                                            _ptr(tk), int(clock_advance), self._sp()))
         self._check_device_error()
         return self._out(outcomes, np_mode)
 
@@ -402,9 +419,12 @@ class CacheTable:
                                             _ptr(ev), _ptr(es), _ptr(ne), _ptr(tk), int(clock_advance), self._sp()))
         self._check_device_error()
         e = int(ne.item())
-        if np_mode:
+        if np_mode is True:
             return (outcomes.cpu().numpy(), ek[:e].cpu().numpy().view(np.uint64), ev[:e].cpu().numpy(),
                     es[:e].cpu().numpy().view(np.uint64))
+        if np_mode == "host":
+            return (self._out(outcomes, "host"), self._out(ek[:e], "host", torch.uint64),
+                    self._out(ev[:e], "host"), self._out(es[:e], "host", torch.uint64))
         return outcomes, ek[:e].view(torch.uint64), ev[:e], es[:e].view(torch.uint64)
 
     def find_or_insert(self, keys, values_inout, scores=None, *, ticks=None, clock_advance: int = 0):

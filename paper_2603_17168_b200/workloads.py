@@ -102,3 +102,39 @@ def rank_to_key(ranks: np.ndarray, seed: int) -> np.ndarray:
 def zipf_keys(count: int, universe: int, alpha: float, seed: int) -> np.ndarray:
     """workloads.py:109-110."""
     return rank_to_key(zipf_ranks(count, universe, alpha, seed), seed)
+
+
+# ---- device-side generation (torch int64 carries the uint64 bit pattern) ----
+_C1_S = 0xFF51AFD7ED558CCD - (1 << 64)
+_C2_S = 0xC4CEB9FE1A85EC53 - (1 << 64)
+_M31 = (1 << 31) - 1
+
+
+def _to_i64(v: int) -> int:
+    v &= 0xFFFFFFFFFFFFFFFF
+    return v - (1 << 64) if v >= (1 << 63) else v
+
+
+def fmix64_torch(x):
+    """fmix64 on an int64 tensor holding uint64 bit patterns (logical shifts
+    emulated with arithmetic shift + mask; multiplies wrap mod 2^64)."""
+    x = x ^ ((x >> 33) & _M31)
+    x = x * _C1_S
+    x = x ^ ((x >> 33) & _M31)
+    x = x * _C2_S
+    x = x ^ ((x >> 33) & _M31)
+    return x
+
+
+def uniform_distinct_keys_torch(count: int, seed: int, stream_offset: int = 0, device="cuda"):
+    """Byte-identical to uniform_distinct_keys, generated on `device` (int64 view)."""
+    import torch
+
+    base = _to_i64(_seed_mix(seed) + stream_offset)
+    x = torch.arange(count, dtype=torch.int64, device=device) + base
+    k = fmix64_torch(x)
+    bad = (k == -1) | (k == -2)  # >= LOCKED as uint64
+    while bool(bad.any()):
+        k = torch.where(bad, fmix64_torch(k), k)
+        bad = (k == -1) | (k == -2)
+    return k
