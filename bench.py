@@ -282,17 +282,22 @@ def run_single(a):
     rec = []  # (step, lam, op, ev0, ev1, outcomes)
     clocks = Clocks(0)
 
+    host_s = [0.0]
+
     def one_step(s, timed):
         for lam, t in tables.items():
             e0, e1, e2, e3 = ev(), ev(), ev(), ev()
+            h0 = time.perf_counter()
             e0.record(stream)
             t.find(queries[lam])
             e1.record(stream)
             e2.record(stream)
             o = t.insert_or_assign(ins_keys[s], vals)
             e3.record(stream)
+            h1 = time.perf_counter()
             t.restore()
             if timed:
+                host_s[0] += h1 - h0
                 rec.append((s, lam, e0, e1, e2, e3, o))
 
     for s in range(a.warmup):
@@ -321,6 +326,7 @@ def run_single(a):
 
     find_ms, find_n = ktime("find")
     apply_ms, apply_n = ktime("apply")
+    vw_ms, vw_n = ktime("values_write")
     for s in range(a.warmup):
         pass
     # device times
@@ -364,7 +370,13 @@ def run_single(a):
     if find_n:
         cand.append(("k_find", find_ms, find_n, find_bytes_launch))
     if apply_n:
-        cand.append(("k_apply_segments", apply_ms, apply_n, apply_bytes_launch))
+        # metadata pass: the byte model minus the value-row traffic (moved by k_values_write)
+        v = 4 * dim
+        moved = int(counts_total[[0, 1, 3]].sum()) * 2 * v + int(counts_total[2]) * v
+        meta_bytes = (bytes_upsert(counts_total, dim) - moved) / max(apply_n, 1)
+        cand.append(("k_meta_single", apply_ms, apply_n, meta_bytes))
+    if vw_n:
+        cand.append(("k_values_write", vw_ms, vw_n, int(counts_total[[0, 1, 3]].sum()) * 2 * 4 * dim / vw_n))
     name, kms, kn, kbytes = max(cand, key=lambda c: c[1])
     avg_ms = kms / kn
     achieved = kbytes / (avg_ms / 1e3) / 1e9
@@ -430,6 +442,7 @@ def run_single(a):
         "find_variation_over_lambda": round((max(find_rates) - min(find_rates)) / max(find_rates), 4),
         "insert_variation_over_lambda": round((max(ins_rates) - min(ins_rates)) / max(ins_rates), 4),
         "wall_ms_per_step_incl_restore": round((w1 - w0) * 1e3 / a.steps, 3),
+        "host_issue_us_per_op": round(host_s[0] * 1e6 / (a.steps * len(a.lambdas) * 2), 1),
         "fill_s": round(fill_s, 1),
         "clocks": clk, "gpu_launches": int(launches), "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu_base,
     }

@@ -76,10 +76,13 @@ const char *hkv_version(void);
 int hkv_create(const hkv_config *cfg, hkv_table **out);
 int hkv_destroy(hkv_table *t);
 
-/* find (table.py:304-323): found[i] in {0,1}; out rows of misses untouched;
- * out may be NULL (contains, table.py:344-351). */
+/* find (table.py:304-323): found[i] in {0,1}; out rows of misses untouched
+ * (zero_misses = 0, the reference contract for a caller-provided `out`) or
+ * written with zeros (zero_misses = 1: same result as the reference's freshly
+ * zeroed `out`, without a separate memset pass); out may be NULL (contains,
+ * table.py:344-351). */
 int hkv_find(hkv_table *t, const uint64_t *keys, int64_t n, float *out, uint8_t *found,
-             hkv_stream stream);
+             int32_t zero_misses, hkv_stream stream);
 int hkv_contains(hkv_table *t, const uint64_t *keys, int64_t n, uint8_t *found, hkv_stream stream);
 /* find_ptr (table.py:325-342): tier 0 fast / 1 overflow, element offset in the
  * tier arena, -1 for misses. */

@@ -301,10 +301,19 @@ int hkv_destroy(hkv_table* t) {
   if (n < 0) return fail(HKV_EINVAL, "negative batch size"); \
   DeviceGuard _g(t->cfg.device)
 
-int hkv_find(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uint8_t* found, hkv_stream stream) {
+int hkv_find(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uint8_t* found, int32_t zero_misses,
+             hkv_stream stream) {
   CHECK_T();
   if (n && (!keys || !found)) return fail(HKV_EINVAL, "null keys/found");
-  launch_find(t->dev, keys, n, out, found, nullptr, nullptr, out ? 0 : 1, (cudaStream_t)stream, t->num_sms);
+  uint32_t* rows = nullptr;
+  if (out && n > 0) {
+    Workspace& ws = t->workspace((cudaStream_t)stream);
+    cudaError_t e0 = ws_reserve(ws, n, (int)t->cfg.value_dim, 0, false);
+    if (e0) return cuda_fail(e0, "hkv_find workspace");
+    rows = ws.vrow;
+  }
+  launch_find(t->dev, keys, n, out, found, nullptr, nullptr, out ? (zero_misses ? 3 : 0) : 1, rows,
+              (cudaStream_t)stream, t->num_sms);
   cudaError_t e = cudaGetLastError();
   return e ? cuda_fail(e, "hkv_find") : HKV_OK;
 }
@@ -312,7 +321,7 @@ int hkv_find(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uint8_t*
 int hkv_contains(hkv_table* t, const uint64_t* keys, int64_t n, uint8_t* found, hkv_stream stream) {
   CHECK_T();
   if (n && (!keys || !found)) return fail(HKV_EINVAL, "null keys/found");
-  launch_find(t->dev, keys, n, nullptr, found, nullptr, nullptr, 1, (cudaStream_t)stream, t->num_sms);
+  launch_find(t->dev, keys, n, nullptr, found, nullptr, nullptr, 1, nullptr, (cudaStream_t)stream, t->num_sms);
   cudaError_t e = cudaGetLastError();
   return e ? cuda_fail(e, "hkv_contains") : HKV_OK;
 }
@@ -321,7 +330,7 @@ int hkv_find_ptr(hkv_table* t, const uint64_t* keys, int64_t n, uint8_t* found, 
                  hkv_stream stream) {
   CHECK_T();
   if (n && (!keys || !found || !tier || !offset)) return fail(HKV_EINVAL, "null argument");
-  launch_find(t->dev, keys, n, nullptr, found, tier, offset, 2, (cudaStream_t)stream, t->num_sms);
+  launch_find(t->dev, keys, n, nullptr, found, tier, offset, 2, nullptr, (cudaStream_t)stream, t->num_sms);
   cudaError_t e = cudaGetLastError();
   return e ? cuda_fail(e, "hkv_find_ptr") : HKV_OK;
 }
@@ -352,8 +361,8 @@ int hkv_upsert(hkv_table* t, int32_t op, const uint64_t* keys, float* values, co
   a.collect = collect;
   a.epoch = t->epoch;
   cudaError_t e = run_mutation(t->dev, a, n, t->log2b, t->workspace(s), &t->sc->round, t->lead, n_evicted_dev,
-                               evicted_keys, evicted_values, evicted_scores, ticks ? clock_advance : (uint64_t)n, s,
-                               t->num_sms);
+                               evicted_keys, evicted_values, evicted_scores, ticks ? clock_advance : (uint64_t)n,
+                               s, t->num_sms);
   return e ? cuda_fail(e, "hkv_upsert") : HKV_OK;
 }
 

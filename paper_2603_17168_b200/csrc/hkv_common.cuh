@@ -115,25 +115,19 @@ __device__ __forceinline__ float* value_row(const TableDev& t, uint64_t row) {
                            : t.vover + (row - t.fast_rows) * (uint64_t)t.dim;
 }
 
+// Byte-equality of 4 digests against d as a 4-bit mask: __vcmpeq4 gives 0xFF
+// per equal byte; keeping bit 0 of each byte (positions 0, 8, 16, 24) and
+// multiplying by 2^21 + 2^14 + 2^7 + 1 gathers them into bits 21..24 with no
+// colliding partial products (other partial products land outside 21..24).
+__device__ __forceinline__ uint32_t match4(uint32_t w, uint32_t dd) {
+  const uint32_t x = __vcmpeq4(w, dd) & 0x01010101u;
+  return ((x * 0x00204081u) >> 21) & 0xFu;
+}
+
 // 16 digest bytes (one uint4) vs the query digest -> 16-bit match mask.
 __device__ __forceinline__ uint32_t match16(uint4 w, uint32_t d) {
   const uint32_t dd = d * 0x01010101u;
-  uint32_t m = 0;
-  uint32_t x;
-  x = __vcmpeq4(w.x, dd);
-  m |= (x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u);
-  x = __vcmpeq4(w.y, dd);
-  m |= ((x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u)) << 4;
-  x = __vcmpeq4(w.z, dd);
-  m |= ((x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u)) << 8;
-  x = __vcmpeq4(w.w, dd);
-  m |= ((x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u)) << 12;
-  return m;
-}
-
-__device__ __forceinline__ uint32_t match4(uint32_t w, uint32_t d) {
-  uint32_t x = __vcmpeq4(w, d * 0x01010101u);
-  return (x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u);
+  return match4(w.x, dd) | (match4(w.y, dd) << 4) | (match4(w.z, dd) << 8) | (match4(w.w, dd) << 12);
 }
 
 // Streaming loads/stores for data touched once.
@@ -159,7 +153,7 @@ __device__ __forceinline__ V ld_vec(const V* p) { return *p; }
 template <typename V>
 __device__ __forceinline__ void st_vec(V* p, V v) { *p = v; }
 
-template <int G, int VEC, int U = 4>
+template <int G, int VEC, int U = 2>
 __device__ __forceinline__ void copy_row(float* dst, const float* src, int dim, int rank) {
   using V = typename std::conditional<VEC == 4, uint4, typename std::conditional<VEC == 2, float2, float>::type>::type;
   const V* s = reinterpret_cast<const V*>(src);
@@ -180,9 +174,13 @@ __device__ __forceinline__ void copy_row(float* dst, const float* src, int dim, 
   }
 }
 
+// Per-thread structural counters (TxnCounters) — 32-bit while a kernel runs,
+// widened when flushed.
+using ctr_t = unsigned int;
+
 // Block-level flush of per-thread counters into the table counters.
 template <int NT>
-__device__ __forceinline__ void flush_counters(unsigned long long* dst, unsigned long long* c, int nc) {
+__device__ __forceinline__ void flush_counters(unsigned long long* dst, const ctr_t* c, int nc) {
   __shared__ unsigned long long sh[6];
   if (threadIdx.x < 6) sh[threadIdx.x] = 0;
   __syncthreads();
@@ -193,6 +191,71 @@ __device__ __forceinline__ void flush_counters(unsigned long long* dst, unsigned
   }
   __syncthreads();
   if (threadIdx.x < nc && sh[threadIdx.x]) atomicAdd(&dst[threadIdx.x], sh[threadIdx.x]);
+}
+
+// An 8-lane sub-warp tile with raw warp intrinsics (cheaper than
+// cooperative_groups' tiled_partition bookkeeping).  Lanes [8g, 8g+8).
+struct Tile8 {
+  unsigned lane, base, mask;
+  __device__ __forceinline__ Tile8() {
+    lane = threadIdx.x & 31u;
+    base = lane & ~7u;
+    mask = 0xFFu << base;
+  }
+  __device__ __forceinline__ int thread_rank() const { return (int)(lane & 7u); }
+  __device__ __forceinline__ unsigned ballot(bool p) const { return (__ballot_sync(mask, p) >> base) & 0xFFu; }
+  __device__ __forceinline__ bool any(bool p) const { return __any_sync(mask, p); }
+  template <typename T>
+  __device__ __forceinline__ T shfl(T v, int src) const { return __shfl_sync(mask, v, (int)base + src); }
+  template <typename T>
+  __device__ __forceinline__ T shfl_xor(T v, int o) const { return __shfl_xor_sync(mask, v, o); }
+  template <typename T>
+  __device__ __forceinline__ T shfl_up(T v, int d) const { return __shfl_up_sync(mask, v, d, 8); }
+  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+  __device__ __forceinline__ unsigned sum(unsigned v) const { return __reduce_add_sync(mask, v); }
+};
+
+// Barrier-free block accumulation of TxnCounters and the size delta: each
+// warp adds its totals into shared memory, the last warp of the block
+// publishes them with one global atomic per counter.
+struct BlockCtrs {
+  unsigned long long c[7];
+  unsigned done;
+};
+__device__ __forceinline__ void block_ctrs_init(BlockCtrs& s) {
+  if (threadIdx.x < 7) s.c[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s.done = 0;
+  __syncthreads();
+}
+// c: 6 per-thread counters, sd: size delta; only tile rank-0 lanes carry
+// tile totals, so every lane contributes and non-owners pass zeros.
+__device__ __forceinline__ void block_ctrs_flush(BlockCtrs& s, unsigned long long* dst_ctr,
+                                                 unsigned long long* dst_size, const ctr_t* c, long long sd) {
+  const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+  for (int k = 0; k < 6; k++) {
+    unsigned long long v = c[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && v) atomicAdd(&s.c[k], v);
+  }
+  long long v = sd;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0 && v) atomicAdd(&s.c[6], (unsigned long long)v);
+  if (lane == 0) {
+    __threadfence_block();
+    const unsigned d = atomicAdd(&s.done, 1u);
+    if (d == blockDim.x / 32 - 1) {
+      __threadfence_block();
+      for (int k = 0; k < 6; k++) {
+        const unsigned long long x = *(volatile unsigned long long*)&s.c[k];
+        if (x) atomicAdd(&dst_ctr[k], x);
+      }
+      const unsigned long long x = *(volatile unsigned long long*)&s.c[6];
+      if (x && dst_size) atomicAdd(dst_size, x);
+    }
+  }
 }
 
 extern unsigned long long g_launches;  // host-side launch counter (hkv_api.cu)

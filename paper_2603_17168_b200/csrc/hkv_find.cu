@@ -5,26 +5,31 @@
 // key compares on digest matches only -> value-row gather (store.py:115-123).
 // Dual mode probes the second bucket only for first-bucket misses.
 //
-// One tile of 8 lanes per key: the digest line is read as 8 x 16 B (one
-// coalesced 128-B transaction), the value row is moved 16 B per lane.  Each
-// tile keeps kKPT keys in flight (software pipelined: all keys' digest
-// lines are requested before any is consumed, then all candidate keys, then
-// all value rows) to raise memory-level parallelism on the dependent chain
-// key -> digest line -> key -> value.
+// Two passes.  Probe: one tile of 8 lanes per key, the digest line read as
+// 8 x 16 B (one coalesced 128-B transaction); each tile keeps 4 keys in
+// flight (all digest lines requested before any is consumed, then all first
+// candidate keys) and records the hit row.  Gather: value rows streamed from
+// the recorded rows with 8 x 16-B requests in flight per lane; separating it
+// from the dependent probe chain is what keeps the value traffic near the
+// copy roofline.
 #include "hkv_probe.cuh"
 #include "hkv_kernels.h"
 
 namespace hkv {
 
-template <int VEC, int MODE, int KPT>
+// Probe pass.  MODE 1: contains (found only), 2: find_ptr (found, tier,
+// offset), 4: find (found + the hit row per key for the gather pass).
+template <int MODE, int KPT>
 __global__ void __launch_bounds__(256) k_find(TableDev t, const uint64_t* __restrict__ keys, int64_t n,
-                                              float* __restrict__ out, uint8_t* __restrict__ found,
-                                              uint8_t* __restrict__ tier, int64_t* __restrict__ offset) {
-  auto tile = cg::tiled_partition<kG>(cg::this_thread_block());
+                                              uint8_t* __restrict__ found, uint8_t* __restrict__ tier,
+                                              int64_t* __restrict__ offset, uint32_t* __restrict__ rows) {
+  __shared__ BlockCtrs bc;
+  block_ctrs_init(bc);
+  const Tile8 tile;
   const int r = tile.thread_rank();
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
   const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / kG;
-  unsigned long long ctr[6] = {0, 0, 0, 0, 0, 0};
+  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
   const int dim = t.dim;
   int bad = 0;
 
@@ -45,24 +50,33 @@ __global__ void __launch_bounds__(256) k_find(TableDev t, const uint64_t* __rest
 #pragma unroll
     for (int u = 0; u < KPT; u++) {
       if (live[u] && t.digest_filter)
-        dl[u] = __ldg(reinterpret_cast<const uint4*>(t.digests + b[u] * kSlots) + r);
+        dl[u] = ld_stream(reinterpret_cast<const uint4*>(t.digests + b[u] * kSlots) + r);
       else
         dl[u] = make_uint4(0, 0, 0, 0);
     }
-    // stage 2: candidate keys (usually 0-1 per key)
+    // stage 2: candidate keys (usually 0-1 per key), first candidate of every key issued together
     int slot[KPT];
+    uint32_t cand[KPT];
+    uint64_t k0[KPT];
 #pragma unroll
     for (int u = 0; u < KPT; u++) {
-      uint32_t cand = !live[u] ? 0u : (t.digest_filter ? match16(dl[u], digest_of(h[u])) : 0xFFFFu);
+      cand[u] = !live[u] ? 0u : (t.digest_filter ? match16(dl[u], digest_of(h[u])) : 0xFFFFu);
+      k0[u] = cand[u] ? __ldg(t.keys + b[u] * kSlots + r * kSPL + (__ffs(cand[u]) - 1)) : kEmptyKey;
+    }
+#pragma unroll
+    for (int u = 0; u < KPT; u++) {
       const uint64_t* kp = t.keys + b[u] * kSlots + r * kSPL;
       int hit = -1, ncmp = 0, ncmp_all = 0;
-      while (cand) {
-        const int j = __ffs(cand) - 1;
-        cand &= cand - 1;
-        const uint64_t k = __ldg(kp + j);
-        if (k == kEmptyKey) continue;
-        ncmp_all++;
-        if (k == key[u]) { hit = r * kSPL + j; ncmp = ncmp_all; break; }
+      uint32_t c = cand[u];
+      uint64_t k = k0[u];
+      while (c) {
+        const int j = __ffs(c) - 1;
+        c &= c - 1;
+        if (k != kEmptyKey) {
+          ncmp_all++;
+          if (k == key[u]) { hit = r * kSPL + j; ncmp = ncmp_all; break; }
+        }
+        if (c) k = __ldg(kp + (__ffs(c) - 1));
       }
       const uint32_t hm = tile.ballot(hit >= 0);
       int contrib = ncmp_all;
@@ -86,20 +100,15 @@ __global__ void __launch_bounds__(256) k_find(TableDev t, const uint64_t* __rest
       }
     }
     // stage 3: outputs
+    if (r == 0) {
 #pragma unroll
-    for (int u = 0; u < KPT; u++) {
-      if (!live[u]) continue;
-      const int64_t i = base + u;
-      const bool f = slot[u] >= 0;
-      const uint64_t row = b[u] * kSlots + (uint64_t)(f ? slot[u] : 0);
-      if constexpr (MODE == 0) {
-        if (f) {
-          copy_row<kG, VEC>(out + i * (int64_t)dim, value_row(t, row), dim, r);
-          ctr[row < t.fast_rows ? kVFast : kVOver]++;
-        }
-      }
-      if (r == 0) {
+      for (int u = 0; u < KPT; u++) {
+        if (!live[u]) continue;
+        const int64_t i = base + u;
+        const bool f = slot[u] >= 0;
+        const uint64_t row = b[u] * kSlots + (uint64_t)(f ? slot[u] : 0);
         found[i] = f;
+        if constexpr (MODE == 4) rows[i] = f ? (uint32_t)row : 0xFFFFFFFFu;
         if constexpr (MODE == 2) {
           const bool over = row >= t.fast_rows;
           tier[i] = f ? (uint8_t)over : 0;
@@ -109,43 +118,113 @@ __global__ void __launch_bounds__(256) k_find(TableDev t, const uint64_t* __rest
     }
   }
   if (bad) atomicOr(t.err, 1);
-  // counters: only rank-0 lanes carry tile totals (avoid 8x counting)
   if (r != 0) {
 #pragma unroll
     for (int k = 0; k < 6; k++) ctr[k] = 0;
   }
-  flush_counters<256>(t.counters, ctr, 6);
+  block_ctrs_flush(bc, t.counters, nullptr, ctr, 0);
+}
+
+// Gather pass: out[i] = value row of the hit (rows at random, output
+// sequential), zero rows for misses when requested; KPT keys per tile and
+// 2 vectors per lane per key in flight.
+template <int VEC, int KPT, bool kZero>
+__global__ void __launch_bounds__(256) k_find_gather(TableDev t, const uint32_t* __restrict__ rows, int64_t n,
+                                                     float* __restrict__ out) {
+  using V = typename std::conditional<VEC == 4, uint4, typename std::conditional<VEC == 2, float2, float>::type>::type;
+  __shared__ BlockCtrs bc;
+  block_ctrs_init(bc);
+  const Tile8 tile;
+  const int r = tile.thread_rank();
+  const int64_t tid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
+  const int64_t ntiles = (int64_t)gridDim.x * blockDim.x / kG;
+  const int dim = t.dim;
+  const int nv = dim / VEC;
+  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t base = tid * KPT; base < n; base += ntiles * KPT) {
+    uint32_t row[KPT];
+#pragma unroll
+    for (int u = 0; u < KPT; u++) {
+      row[u] = (base + u < n) ? rows[base + u] : 0xFFFFFFFFu;
+      if (r == 0 && row[u] != 0xFFFFFFFFu) ctr[row[u] < t.fast_rows ? kVFast : kVOver]++;
+    }
+    for (int e0 = r; e0 < nv; e0 += kG * 2) {
+      V v[KPT][2];
+#pragma unroll
+      for (int u = 0; u < KPT; u++) {
+        const V* src = reinterpret_cast<const V*>(row[u] != 0xFFFFFFFFu ? value_row(t, row[u]) : nullptr);
+#pragma unroll
+        for (int w = 0; w < 2; w++) {
+          const int e = e0 + w * kG;
+          if (e < nv) {
+            if (row[u] != 0xFFFFFFFFu) v[u][w] = ld_vec(src + e);
+            else v[u][w] = V{};
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < KPT; u++) {
+        if (base + u >= n) continue;
+        if (!kZero && row[u] == 0xFFFFFFFFu) continue;
+        V* dst = reinterpret_cast<V*>(out + (uint64_t)(base + u) * dim);
+#pragma unroll
+        for (int w = 0; w < 2; w++) {
+          const int e = e0 + w * kG;
+          if (e < nv) st_vec(dst + e, v[u][w]);
+        }
+      }
+    }
+  }
+  block_ctrs_flush(bc, t.counters, nullptr, ctr, 0);
 }
 
 template <int MODE>
-static void launch_find_mode(const TableDev& t, const uint64_t* keys, int64_t n, float* out, uint8_t* found,
-                             uint8_t* tier, int64_t* offset, cudaStream_t s, int num_sms) {
-  constexpr int KPT = 2;
-  const int threads = 256;
-  int64_t groups = (n + KPT - 1) / KPT;
-  int64_t blocks = (groups * kG + threads - 1) / threads;
-  const int64_t max_blocks = (int64_t)num_sms * 8 * 4;  // 8 resident x 4 waves
+static void launch_probe(const TableDev& t, const uint64_t* keys, int64_t n, uint8_t* found, uint8_t* tier,
+                         int64_t* offset, uint32_t* rows, cudaStream_t s, int num_sms) {
+  constexpr int KPT = 4;
+  int64_t blocks = (((n + KPT - 1) / KPT) * kG + 255) / 256;
+  const int64_t max_blocks = (int64_t)num_sms * 8 * 4;
   if (blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
-  const bool al4 = (t.dim % 4 == 0) && (((uintptr_t)out & 15) == 0) && (((uintptr_t)t.vfast & 15) == 0) &&
-                   (((uintptr_t)t.vover & 15) == 0);
-  const bool al2 = (t.dim % 2 == 0) && (((uintptr_t)out & 7) == 0);
-  if (MODE != 0 || al4)
-    k_find<4, MODE, KPT><<<blocks, threads, 0, s>>>(t, keys, n, out, found, tier, offset);
-  else if (al2)
-    k_find<2, MODE, KPT><<<blocks, threads, 0, s>>>(t, keys, n, out, found, tier, offset);
-  else
-    k_find<1, MODE, KPT><<<blocks, threads, 0, s>>>(t, keys, n, out, found, tier, offset);
+  k_find<MODE, KPT><<<(unsigned)blocks, 256, 0, s>>>(t, keys, n, found, tier, offset, rows);
   g_launches++;
 }
 
-void launch_find(const TableDev& t, const uint64_t* keys, int64_t n, float* out, uint8_t* found,
-                 uint8_t* tier, int64_t* offset, int mode, cudaStream_t s, int num_sms) {
+void launch_find(const TableDev& t, const uint64_t* keys, int64_t n, float* out, uint8_t* found, uint8_t* tier,
+                 int64_t* offset, int mode, uint32_t* rows, cudaStream_t s, int num_sms) {
   if (n <= 0) return;
   ktimer_begin("find", s);
-  if (mode == 0) launch_find_mode<0>(t, keys, n, out, found, tier, offset, s, num_sms);
-  else if (mode == 1) launch_find_mode<1>(t, keys, n, out, found, tier, offset, s, num_sms);
-  else launch_find_mode<2>(t, keys, n, out, found, tier, offset, s, num_sms);
+  if (mode == 1) {
+    launch_probe<1>(t, keys, n, found, nullptr, nullptr, nullptr, s, num_sms);
+  } else if (mode == 2) {
+    launch_probe<2>(t, keys, n, found, tier, offset, nullptr, s, num_sms);
+  } else {
+    launch_probe<4>(t, keys, n, found, nullptr, nullptr, rows, s, num_sms);
+    ktimer_end("find", s);
+    ktimer_begin("find_gather", s);
+    const bool al4 = (t.dim % 4 == 0) && (((uintptr_t)out & 15) == 0) && (((uintptr_t)t.vfast & 15) == 0) &&
+                     (((uintptr_t)t.vover & 15) == 0);
+    const bool al2 = (t.dim % 2 == 0) && (((uintptr_t)out & 7) == 0) && (((uintptr_t)t.vfast & 7) == 0) &&
+                     (((uintptr_t)t.vover & 7) == 0);
+    int64_t blocks = (((n + 3) / 4) * kG + 255) / 256;
+    const int64_t cap = (int64_t)num_sms * 8 * 4;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    const bool z = mode == 3;
+    if (al4) {
+      if (z) k_find_gather<4, 4, true><<<(unsigned)blocks, 256, 0, s>>>(t, rows, n, out);
+      else k_find_gather<4, 4, false><<<(unsigned)blocks, 256, 0, s>>>(t, rows, n, out);
+    } else if (al2) {
+      if (z) k_find_gather<2, 4, true><<<(unsigned)blocks, 256, 0, s>>>(t, rows, n, out);
+      else k_find_gather<2, 4, false><<<(unsigned)blocks, 256, 0, s>>>(t, rows, n, out);
+    } else {
+      if (z) k_find_gather<1, 4, true><<<(unsigned)blocks, 256, 0, s>>>(t, rows, n, out);
+      else k_find_gather<1, 4, false><<<(unsigned)blocks, 256, 0, s>>>(t, rows, n, out);
+    }
+    g_launches++;
+    ktimer_end("find_gather", s);
+    return;
+  }
   ktimer_end("find", s);
 }
 

@@ -11,7 +11,8 @@ namespace hkv {
 // Per-batch device scalars (zeroed by the launcher before each batch).
 struct Scalars {
   int err;                       // sentinel key seen in this batch
-  unsigned nseg;                 // bucket segments
+  unsigned nseg;                 // single-op bucket segments
+  unsigned nmulti;               // multi-op bucket segments
   unsigned first_ev;             // lowest batch index with an Evicted outcome
   unsigned npend[2];             // dual-mode pending list sizes (per round parity)
   unsigned pad;
@@ -24,6 +25,7 @@ struct Scalars {
 struct Workspace {
   int64_t cap_n = 0;
   int64_t cap_ev = 0;  // rows of evicted-value scratch
+  int64_t cap_ek = 0;  // entries of evicted key/score scratch
   int dim = 0;
   uint32_t* bkt = nullptr;
   uint32_t* idx = nullptr;
@@ -32,6 +34,10 @@ struct Workspace {
   uint32_t* seg = nullptr;
   uint32_t* aux = nullptr;   // assign: rows / evicted list
   uint32_t* aux2 = nullptr;  // assign: found ranks
+  uint64_t* skey = nullptr;  // single mode: bucket-segment records (3 u64 per item)
+  uint32_t* vrow = nullptr;  // single mode: destination row of final value writers
+  uint32_t* rrow = nullptr;  // single mode: row of a value read
+  int32_t* rsrc = nullptr;   // single mode: provenance of a value read (-1 = pre-batch row)
   uint32_t* b2 = nullptr;    // dual: second bucket
   uint32_t* pend = nullptr;  // dual: second pending list
   uint64_t* ek = nullptr;
@@ -39,6 +45,7 @@ struct Workspace {
   float* ev = nullptr;
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
+  int64_t cub_for_n = -1;
   Scalars* sc = nullptr;
 };
 
@@ -59,8 +66,10 @@ struct OpArgs {
 
 enum { kOpUpsert = 0, kOpFindOrInsert = 1, kOpErase = 2 };
 
+// mode 0: find (misses untouched), 3: find (misses zero-filled), 1: contains, 2: find_ptr.
+// rows: n-entry scratch for modes 0/3.
 void launch_find(const TableDev& t, const uint64_t* keys, int64_t n, float* out, uint8_t* found,
-                 uint8_t* tier, int64_t* offset, int mode, cudaStream_t s, int num_sms);
+                 uint8_t* tier, int64_t* offset, int mode, uint32_t* rows, cudaStream_t s, int num_sms);
 
 // Returns cudaSuccess or the first error.
 cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, Workspace& ws,
@@ -86,7 +95,7 @@ cudaError_t run_route(const uint64_t* keys, int64_t n, int64_t global_buckets, i
 void ktimer_begin(const char* name, cudaStream_t s);
 void ktimer_end(const char* name, cudaStream_t s);
 
-cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, bool need_ev, bool dual);
+cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual);
 void ws_free(Workspace& ws);
 
 }  // namespace hkv

@@ -31,11 +31,11 @@ struct ExportFlag {
 template <int VEC>
 __global__ void k_export_gather(TableDev t, const uint32_t* __restrict__ list, int64_t base, int64_t take,
                                 uint64_t* ok, float* ov, uint64_t* os) {
-  auto tile = cg::tiled_partition<kG>(cg::this_thread_block());
+  const Tile8 tile;
   const int r = tile.thread_rank();
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
   const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / kG;
-  unsigned long long ctr[6] = {0, 0, 0, 0, 0, 0};
+  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
   for (int64_t j = gid; j < take; j += ngroups) {
     const uint64_t row = (uint64_t)(base + list[j]);
     if (r == 0) {
@@ -53,7 +53,7 @@ cudaError_t run_export(const TableDev& t, int64_t cursor, int64_t max_count, int
                        int64_t* count, int64_t* next, Workspace& ws, cudaStream_t s, int num_sms) {
   const int64_t kChunk = 1 << 22;
   cudaError_t e;
-  if ((e = ws_reserve(ws, kChunk, t.dim, false, false))) return e;
+  if ((e = ws_reserve(ws, kChunk, t.dim, 0, false))) return e;
   const int64_t end = mask ? cursor + mask_rows : (int64_t)t.capacity;
   int64_t taken = 0;
   *next = -1;
@@ -102,7 +102,7 @@ cudaError_t run_export(const TableDev& t, int64_t cursor, int64_t max_count, int
 // (check_consistency, table.py:1284-1299)
 // ---------------------------------------------------------------------------
 __global__ void k_bits_from_keys(TableDev t, int64_t buckets) {
-  auto tile = cg::tiled_partition<kG>(cg::this_thread_block());
+  const Tile8 tile;
   const int r = tile.thread_rank();
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
   const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / kG;
@@ -131,7 +131,7 @@ cudaError_t run_bits_from_keys(const TableDev& t, int64_t buckets, cudaStream_t 
 
 // ok_dev[0] = 1 if consistent; ok_dev[1..2] = user-key total (int64 split)
 __global__ void k_consistency(TableDev t, int64_t buckets, int* ok_dev, unsigned long long* total) {
-  auto tile = cg::tiled_partition<kG>(cg::this_thread_block());
+  const Tile8 tile;
   const int r = tile.thread_rank();
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
   const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / kG;
@@ -190,7 +190,7 @@ __global__ void k_route_dest(const uint64_t* __restrict__ keys, int64_t n, uint6
 cudaError_t run_route(const uint64_t* keys, int64_t n, int64_t global_buckets, int world, int32_t* perm,
                       int64_t* counts, Workspace& ws, cudaStream_t s) {
   cudaError_t e;
-  if ((e = ws_reserve(ws, n, 1, false, false))) return e;
+  if ((e = ws_reserve(ws, n, 1, 0, false))) return e;
   if ((e = cudaMemsetAsync(counts, 0, sizeof(int64_t) * world, s))) return e;
   if (n <= 0) return cudaSuccess;
   int shift = 0;

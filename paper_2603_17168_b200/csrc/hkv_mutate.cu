@@ -7,10 +7,12 @@
 //
 //  single mode  -- a key's whole candidate space is one bucket, so ops on
 //    different buckets commute.  k_prep hashes the batch, a stable radix sort
-//    groups ops by bucket (ascending batch index inside a bucket), k_heads
-//    finds the bucket segments, and k_apply_segments gives each segment to one
-//    8-lane tile that applies its ops in order with exclusive ownership of the
-//    bucket: no CAS, no retries, bit-exact at any contention.
+//    groups ops by bucket (ascending batch index inside a bucket), and
+//    k_meta_single gives each bucket segment to one 8-lane tile (the tile
+//    owning the segment's first sorted position) that applies its ops' metadata
+//    in order with exclusive ownership of the bucket: no CAS, no retries,
+//    bit-exact at any contention.  Value rows then move in streaming kernels
+//    (k_values_read / k_values_write) driven by the recorded row plan.
 //  dual mode    -- an op touches two buckets; k_dual_rounds runs the
 //    reference's leader rounds on the device (table.py:945-962): per round
 //    every pending op bids its batch index on both buckets (atomicMax on a
@@ -34,9 +36,9 @@ namespace hkv {
 // ---------------------------------------------------------------------------
 template <int VEC>
 __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
-                                           const cg::thread_block_tile<kG>& tile, uint32_t i,
-                                           uint64_t clock0, bool fel_open, unsigned long long* ctr,
-                                           long long& size_delta) {
+                                           const Tile8& tile, uint32_t i,
+                                           uint64_t clock0, bool fel_open, ctr_t* ctr,
+                                           int& size_delta) {
   const int r = tile.thread_rank();
   const int dim = t.dim;
   const uint64_t key = a.keys[i];
@@ -181,8 +183,8 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
   if (r == 0) a.outcomes[i] = outcome;
 }
 
-__device__ __forceinline__ void flush_tile_counters(const cg::thread_block_tile<kG>& tile, const TableDev& t,
-                                                    unsigned long long* ctr, long long size_delta) {
+__device__ __forceinline__ void flush_tile_counters(const Tile8& tile, const TableDev& t,
+                                                    ctr_t* ctr, int size_delta) {
   if (tile.thread_rank() != 0) {
 #pragma unroll
     for (int k = 0; k < 6; k++) ctr[k] = 0;
@@ -190,7 +192,7 @@ __device__ __forceinline__ void flush_tile_counters(const cg::thread_block_tile<
   }
   flush_counters<256>(t.counters, ctr, 6);
   long long v = size_delta;
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);  // 64-bit warp sum
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(t.size, (unsigned long long)v);
 }
 
@@ -213,42 +215,461 @@ __global__ void k_prep(TableDev t, const uint64_t* __restrict__ keys, int64_t n,
   if (b2) b2[i] = (uint32_t)(second_hash(h) & t.mask);
 }
 
-__global__ void k_heads(const uint32_t* __restrict__ sb, int64_t n, uint32_t* __restrict__ seg, Scalars* sc) {
+// ---------------------------------------------------------------------------
+// Single mode, metadata pass.  One 8-lane tile per bucket segment, ops in
+// batch order.  Only metadata is touched here (digest line, occupancy bits,
+// candidate keys, score row); value rows move in separate streaming kernels
+// (k_values_read / k_values_write) that have far more memory-level
+// parallelism than a tile walking its serial chain.  To stay bit-exact the
+// pass records, per op:
+//   vrow[i]  destination row when op i is the LAST writer of that row in its
+//            segment (a later writer of the same slot retires the earlier one)
+//   rrow[i], rsrc[i]  for value reads (find_or_insert hits, insert_and_evict
+//            victims): the row, and the op whose input currently sits in that
+//            row (-1 = the row's content before the batch)
+// "Last writer of a slot in the current segment" lives in shared memory,
+// tagged with a per-segment generation so no per-segment reset is needed.
+//
+// Warp-synchronous: a warp's four tiles advance in lockstep (a tile whose
+// segment is exhausted idles), every collective uses the full warp mask and
+// outcome branches are predicates, so no divergent-collective emulation.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kNoRow = 0xFFFFFFFFu;
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// Segment records: one per bucket segment of the sorted batch, compacted
+// with one global atomic per block (record order across blocks is arbitrary;
+// segments are independent).  Carries the head op so the metadata pass
+// starts with one coalesced 24-B read instead of a dependent index hop.
+struct SegRec {
+  uint64_t key;    // key of the segment's first op
+  uint32_t p;      // sorted position of the first op
+  uint32_t b;      // bucket
+  uint32_t i;      // batch index of the first op
+  uint32_t flags;  // bit 0: segment has more than one op; bits 8..15: the first op's digest
+};
+
+// Segment records split into two lists: singleton segments from the front
+// of `recs`, multi-op segments from the back (recs[cap-1], recs[cap-2], ...),
+// so the metadata pass can run each class in lockstep without waste.
+__global__ void __launch_bounds__(1024) k_segments(const uint32_t* __restrict__ sb, const uint32_t* __restrict__ sidx,
+                                                   const uint64_t* __restrict__ keys, int64_t n,
+                                                   SegRec* __restrict__ recs, int64_t cap, Scalars* sc) {
+  __shared__ unsigned wcount[2][32];
+  __shared__ unsigned block_base[2];
   if (sc->err) return;
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool head = p < n && (p == 0 || sb[p] != sb[p - 1]);
-  const unsigned mask = __ballot_sync(0xffffffffu, head);
-  if (!mask) return;
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(mask) - 1;
-  unsigned base = 0;
-  if (lane == leader) base = atomicAdd(&sc->nseg, (unsigned)__popc(mask));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  if (head) seg[base + __popc(mask & ((1u << lane) - 1))] = (uint32_t)p;
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t b = kNoRow;
+  bool head = false, multi = false;
+  if (p < n) {
+    b = sb[p];
+    head = (p == 0) || (sb[p - 1] != b);
+    multi = (p + 1 < n) && (sb[p + 1] == b);
+  }
+  const unsigned ms = __ballot_sync(kFull, head && !multi);
+  const unsigned mm = __ballot_sync(kFull, head && multi);
+  if (lane == 0) {
+    wcount[0][warp] = __popc(ms);
+    wcount[1][warp] = __popc(mm);
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    const int c = threadIdx.x;
+    unsigned acc = 0;
+    for (unsigned w = 0; w < blockDim.x / 32; w++) {
+      const unsigned x = wcount[c][w];
+      wcount[c][w] = acc;
+      acc += x;
+    }
+    block_base[c] = acc ? atomicAdd(c == 0 ? &sc->nseg : &sc->nmulti, acc) : 0;
+  }
+  __syncthreads();
+  if (head) {
+    const uint32_t i = sidx[p];
+    SegRec rec;
+    rec.key = keys[i];
+    rec.p = (uint32_t)p;
+    rec.b = b;
+    rec.i = i;
+    rec.flags = (multi ? 1u : 0u) | (digest_of(fmix64(rec.key)) << 8);
+    const int c = multi ? 1 : 0;
+    const unsigned m = multi ? mm : ms;
+    const int64_t slot = block_base[c] + wcount[c][warp] + __popc(m & ((1u << lane) - 1));
+    recs[multi ? cap - 1 - slot : slot] = rec;
+  }
 }
 
-template <int VEC>
-__global__ void __launch_bounds__(256) k_apply_segments(TableDev t, OpArgs a, const uint32_t* __restrict__ sb,
-                                                        const uint32_t* __restrict__ sidx,
-                                                        const uint32_t* __restrict__ seg, int64_t n) {
-  if (a.sc->err) return;
-  auto tile = cg::tiled_partition<kG>(cg::this_thread_block());
-  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
-  const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / kG;
-  const uint64_t clock0 = *t.clock;
-  const bool fel_open = !*t.fel_set;
-  const unsigned nseg = a.sc->nseg;
-  unsigned long long ctr[6] = {0, 0, 0, 0, 0, 0};
-  long long sd = 0;
-  for (int64_t s = gid; s < nseg; s += ngroups) {
-    int64_t p = seg[s];
-    const uint32_t b = sb[p];
-    while (true) {
-      process_op<VEC>(t, a, tile, sidx[p], clock0, fel_open, ctr, sd);
-      if (++p >= n || sb[p] != b) break;
+__device__ __forceinline__ unsigned ws_ballot(bool p, unsigned tb) { return (__ballot_sync(kFull, p) >> tb) & 0xFFu; }
+__device__ __forceinline__ unsigned ws_sum8(unsigned v) {
+  v += __shfl_xor_sync(kFull, v, 1);
+  v += __shfl_xor_sync(kFull, v, 2);
+  v += __shfl_xor_sync(kFull, v, 4);
+  return v;
+}
+
+struct LastWriter {  // per-tile shared-memory view
+  int* op;           // [128] op index of the slot's last writer
+  uint16_t* gen;     // [128] segment generation that wrote it
+  uint16_t cur;      // current segment generation
+  __device__ __forceinline__ int get(int s) const { return gen[s] == cur ? op[s] : -1; }
+  __device__ __forceinline__ void set(int s, int i) {
+    op[s] = i;
+    gen[s] = cur;
+  }
+};
+
+// One op of every active tile of the warp (must be called by all 32 lanes).
+// dw/occ: this lane's digest / occupancy slice of bucket b, already loaded.
+template <int OP, bool COLLECT>
+__device__ __forceinline__ void meta_op_ws(const TableDev& t, const OpArgs& a, unsigned lane, bool active,
+                                           uint32_t i, uint64_t key, uint32_t d, uint64_t b, uint4 dw, uint32_t occ,
+                                           uint64_t clock0, bool fel_open, bool spec, LastWriter& lw,
+                                           uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
+                                           int32_t* __restrict__ rsrc, ctr_t* ctr, int& size_delta) {
+  const int r = (int)(lane & 7u);
+  const unsigned tb = lane & ~7u;
+  const uint64_t rowbase = b * kSlots;
+  uint64_t lmin = kMaxScore;
+  int lm = r * kSPL;
+  auto scan_scores = [&]() {
+    const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(t.scores + rowbase + r * kSPL);
+    ulonglong2 sv[kSPL / 2];
+#pragma unroll
+    for (int k = 0; k < kSPL / 2; k++) sv[k] = sp[k];
+    lmin = sv[0].x;
+    lm = r * kSPL;
+#pragma unroll
+    for (int k = 0; k < kSPL / 2; k++) {
+      if (k > 0 && sv[k].x < lmin) { lmin = sv[k].x; lm = r * kSPL + 2 * k; }
+      if (sv[k].y < lmin) { lmin = sv[k].y; lm = r * kSPL + 2 * k + 1; }
+    }
+  };
+  // candidate keys (first one issued before the score row so both are in flight)
+  uint32_t cand = active ? ((t.digest_filter ? match16(dw, d) : 0xFFFFu) & occ) : 0u;
+  const uint64_t* kp = t.keys + rowbase + r * kSPL;
+  uint64_t kc = cand ? kp[__ffs(cand) - 1] : 0;
+  if (OP != kOpErase && spec && active) scan_scores();
+  int hit = -1;
+  unsigned ncmp = 0, ncmp_all = 0;
+  while (cand) {
+    const int j = __ffs(cand) - 1;
+    cand &= cand - 1;
+    ncmp_all++;
+    if (kc == key) { hit = r * kSPL + j; ncmp = ncmp_all; break; }
+    if (cand) kc = kp[__ffs(cand) - 1];
+  }
+  const unsigned hm = ws_ballot(hit >= 0, tb);
+  const int hl = hm ? __ffs(hm) - 1 : 0;
+  int slot = __shfl_sync(kFull, hit, (int)tb + hl);
+  if (!hm) slot = -1;
+  unsigned contrib = ncmp_all;
+  if (hm) contrib = r < hl ? ncmp_all : (r == hl ? ncmp : 0u);
+  contrib = ws_sum8(contrib);
+  if (active && r == 0) {
+    ctr[kCompares] += contrib;
+    ctr[kLoads]++;
+  }
+  if constexpr (OP == kOpErase) {  // _round_erase, table.py:1017-1023
+    if (active && slot >= 0) {
+      if (slot / kSPL == r) {
+        t.keys[rowbase + slot] = kEmptyKey;
+        store_occ(t, b, r, occ & ~(1u << (slot % kSPL)));
+      }
+      if (r == 0) size_delta--;
+    }
+    if (active && r == 0) a.outcomes[i] = slot >= 0 ? kErased : kNotFound;
+    return;
+  }
+  const bool is_hit = active && slot >= 0;
+  const bool miss = active && slot < 0;
+  uint64_t tick = 0, cs = 0;
+  if (active) {
+    tick = a.ticks ? a.ticks[i] : clock0 + (uint64_t)i + 1;
+    cs = a.scores ? a.scores[i] : 0;
+  }
+  const uint64_t s_in = insert_score(t.policy, a.epoch, tick, cs);
+  uint8_t outcome = kRejected;
+  int wslot = -1;  // slot this op's value goes to
+  int rslot = -1;  // slot whose value this op reads
+  if (is_hit && slot / kSPL == r) {  // table.py:1045-1062
+    const uint64_t row = rowbase + slot;
+    const uint64_t old = hit_needs_old(t.policy) ? t.scores[row] : 0;
+    t.scores[row] = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
+  }
+  if (is_hit) {
+    if constexpr (OP == kOpFindOrInsert) {
+      outcome = kFound;
+      rslot = slot;
+    } else {
+      outcome = kUpdated;
+      wslot = slot;
     }
   }
-  flush_tile_counters(tile, t, ctr, sd);
+  const unsigned occ_total = ws_sum8(__popc(occ));
+  const bool free_ins = miss && occ_total < kSlots;
+  const bool full = miss && occ_total >= kSlots;
+  // _bulk_insert_free, table.py:1165-1181: lowest EMPTY slot = lowest clear bit
+  const unsigned hasfree = ws_ballot(occ != 0xFFFFu, tb);
+  const int fl = hasfree ? __ffs(hasfree) - 1 : 0;
+  int sl = 0;
+  if (free_ins && r == fl) {
+    const int j = __ffs(~occ & 0xFFFFu) - 1;
+    sl = r * kSPL + j;
+    t.keys[rowbase + sl] = key;
+    t.digests[rowbase + sl] = (uint8_t)d;
+    t.scores[rowbase + sl] = s_in;
+    store_occ(t, b, r, occ | (1u << j));
+  }
+  sl = __shfl_sync(kFull, sl, (int)tb + fl);
+  if (free_ins) {
+    wslot = sl;
+    outcome = kInserted;
+    if (r == 0) size_delta++;
+  }
+  // full bucket: tile argmin over the score row, admission, eviction (table.py:1079-1083, 1121-1163)
+  if (__any_sync(kFull, full)) {
+    if (!spec && full) scan_scores();
+#pragma unroll
+    for (int o = kG / 2; o > 0; o >>= 1) {
+      const uint64_t ov = __shfl_xor_sync(kFull, lmin, o);
+      const int om = __shfl_xor_sync(kFull, lm, o);
+      if (ov < lmin || (ov == lmin && om < lm)) { lmin = ov; lm = om; }
+    }
+    if (full) {
+      if (r == 0) ctr[kScans]++;
+      if (s_in >= lmin) {  // the single-bucket path admits ties (table.py:1083)
+        const uint64_t row = rowbase + lm;
+        if (lm / kSPL == r) {
+          if constexpr (COLLECT) {
+            a.ek[i] = t.keys[row];
+            a.es[i] = lmin;
+          }
+          t.keys[row] = key;
+          t.digests[row] = (uint8_t)d;
+          t.scores[row] = s_in;
+        }
+        wslot = lm;
+        if constexpr (COLLECT) rslot = lm;
+        outcome = kEvicted;
+        if (fel_open && r == 0) atomicMin(&a.sc->first_ev, i);
+      }
+    }
+  }
+  if (!active) return;
+  // value plan (provenance read BEFORE this op's own write is recorded)
+  if (rslot >= 0) {
+    if (r == 0) ctr[rowbase + rslot < t.fast_rows ? kVFast : kVOver]++;
+    if (rslot / kSPL == r) {
+      rrow[i] = (uint32_t)(rowbase + rslot);
+      rsrc[i] = lw.get(rslot);
+    }
+  }
+  if (wslot >= 0) {
+    if (r == 0) ctr[rowbase + wslot < t.fast_rows ? kVFast : kVOver]++;
+    if (wslot / kSPL == r) {
+      const int prev = lw.get(wslot);
+      if (prev >= 0) vrow[prev] = kNoRow;  // retired: a later op of this segment rewrites the slot
+      lw.set(wslot, (int)i);
+      vrow[i] = (uint32_t)(rowbase + wslot);
+    }
+  } else if (r == 0) {
+    vrow[i] = kNoRow;
+  }
+  if (r == 0) a.outcomes[i] = outcome;
+}
+
+__device__ __forceinline__ void load_slices(const TableDev& t, bool active, uint64_t b, int r, uint4& dw,
+                                            uint32_t& occ) {
+  if (active) {
+    dw = reinterpret_cast<const uint4*>(t.digests + b * kSlots)[r];
+    occ = load_occ(t, b, r);
+  } else {
+    dw = make_uint4(0, 0, 0, 0);
+    occ = 0;
+  }
+}
+
+// Metadata pass over one record list (singletons, or multi-op segments).
+// The next group's record and digest/occupancy slices are requested one
+// iteration ahead: segments own distinct buckets, so a prefetched slice can
+// never be stale.
+template <int OP, bool COLLECT>
+__device__ __forceinline__ void meta_pass(const TableDev& t, const OpArgs& a, const uint32_t* __restrict__ sb,
+                                          const uint32_t* __restrict__ sidx, const SegRec* __restrict__ recs,
+                                          int64_t nrec, int64_t dir, int64_t n, uint32_t* __restrict__ vrow,
+                                          uint32_t* __restrict__ rrow, int32_t* __restrict__ rsrc, LastWriter& lw,
+                                          uint64_t clock0, bool fel_open, bool spec, ctr_t* ctr, int& sd) {
+  const unsigned lane = threadIdx.x & 31u;
+  const int r = (int)(lane & 7u);
+  const int tile_in_warp = (int)(lane >> 3);
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t stride = nwarps * 4;
+  auto rec_at = [&](int64_t sg) -> SegRec {
+    if (sg < nrec) return recs[dir > 0 ? sg : -sg];
+    return SegRec{0, 0, 0, 0, 0};
+  };
+  int64_t sg = warp * 4 + tile_in_warp;
+  SegRec rec = rec_at(sg);
+  uint4 dw;
+  uint32_t occ;
+  load_slices(t, sg < nrec, rec.b, r, dw, occ);
+  SegRec rec_n = rec_at(sg + stride);
+  for (int64_t sg0 = warp * 4; sg0 < nrec; sg0 += stride, sg += stride) {
+    bool active = sg < nrec;
+    // prefetch: next group's slices (its record arrived last iteration), the record after
+    uint4 dw_n;
+    uint32_t occ_n;
+    load_slices(t, sg + stride < nrec, rec_n.b, r, dw_n, occ_n);
+    const SegRec rec_nn = rec_at(sg + 2 * stride);
+    const uint64_t b = rec.b;
+    const bool multi = (rec.flags & 1u) != 0;
+    uint32_t i = rec.i, d = rec.flags >> 8;
+    uint64_t key = rec.key;
+    int64_t q = rec.p;
+    if (lw.cur == 0xFFFEu) {  // generation wrap: forget all
+#pragma unroll
+      for (int j = 0; j < kSPL; j++) lw.gen[r * kSPL + j] = 0xFFFFu;
+      lw.cur = 0;
+    }
+    lw.cur++;
+    __syncwarp();
+    while (true) {
+      meta_op_ws<OP, COLLECT>(t, a, lane, active, i, key, d, b, dw, occ, clock0, fel_open, spec, lw, vrow, rrow,
+                              rsrc, ctr, sd);
+      if (active) {
+        if (multi && ++q < n && sb[q] == (uint32_t)b) {
+          i = sidx[q];
+          key = a.keys[i];
+          d = digest_of(fmix64(key));
+          __syncwarp();
+          load_slices(t, true, b, r, dw, occ);  // re-read after this tile's own writes
+        } else {
+          active = false;
+        }
+      }
+      if (!__any_sync(kFull, active)) break;
+    }
+    rec = rec_n;
+    rec_n = rec_nn;
+    dw = dw_n;
+    occ = occ_n;
+  }
+}
+
+template <int OP, bool COLLECT>
+__global__ void __launch_bounds__(256, 3) k_meta_single(TableDev t, OpArgs a, const uint32_t* __restrict__ sb,
+                                                        const uint32_t* __restrict__ sidx,
+                                                        const SegRec* __restrict__ recs, int64_t cap, int64_t n,
+                                                        uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
+                                                        int32_t* __restrict__ rsrc) {
+  __shared__ int lw_op[256 / kG][kSlots];
+  __shared__ uint16_t lw_gen[256 / kG][kSlots];
+  __shared__ BlockCtrs bc;
+  if (a.sc->err) return;
+  const unsigned lane = threadIdx.x & 31u;
+  const int r = (int)(lane & 7u);
+  LastWriter lw{lw_op[threadIdx.x / kG], lw_gen[threadIdx.x / kG], 0};
+#pragma unroll
+  for (int j = 0; j < kSPL; j++) lw.gen[r * kSPL + j] = 0xFFFFu;
+  block_ctrs_init(bc);
+  const uint64_t clock0 = *t.clock;
+  const bool fel_open = !*t.fel_set;
+  // speculative score-row read with the digest line when buckets are almost surely full
+  const unsigned long long sz = *t.size;
+  const bool spec = sz * 100ull > t.capacity * 97ull;
+  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
+  int sd = 0;
+  meta_pass<OP, COLLECT>(t, a, sb, sidx, recs, (int64_t)a.sc->nseg, 1, n, vrow, rrow, rsrc, lw, clock0, fel_open, spec,
+                         ctr, sd);
+  meta_pass<OP, COLLECT>(t, a, sb, sidx, recs + (cap - 1), (int64_t)a.sc->nmulti, -1, n, vrow, rrow, rsrc, lw, clock0,
+                         fel_open, spec, ctr, sd);
+  block_ctrs_flush(bc, t.counters, t.size, ctr, sd);
+}
+
+// Value rows for the final writers: table[vrow[i]] = values[i].  Inputs are
+// read sequentially (consecutive i), destination rows at random; KPT ops per
+// tile keep 2*KPT 16-B loads in flight per lane.
+template <int VEC, int KPT>
+__global__ void __launch_bounds__(256) k_values_write(TableDev t, const float* __restrict__ values,
+                                                      const uint32_t* __restrict__ vrow, int64_t n,
+                                                      const Scalars* sc) {
+  if (sc->err) return;
+  using V = typename std::conditional<VEC == 4, uint4, typename std::conditional<VEC == 2, float2, float>::type>::type;
+  const Tile8 tile;
+  const int r = tile.thread_rank();
+  const int64_t tid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
+  const int64_t ntiles = (int64_t)gridDim.x * blockDim.x / kG;
+  const int dim = t.dim;
+  const int nv = dim / VEC;
+  for (int64_t base = tid * KPT; base < n; base += ntiles * KPT) {
+    uint32_t row[KPT];
+#pragma unroll
+    for (int u = 0; u < KPT; u++) row[u] = (base + u < n) ? vrow[base + u] : kNoRow;
+    for (int e0 = r; e0 < nv; e0 += kG * 2) {
+      V v[KPT][2];
+#pragma unroll
+      for (int u = 0; u < KPT; u++) {
+        const V* src = reinterpret_cast<const V*>(values + (uint64_t)(base + u) * dim);
+#pragma unroll
+        for (int w = 0; w < 2; w++) {
+          const int e = e0 + w * kG;
+          if (row[u] != kNoRow && e < nv) v[u][w] = ld_vec(src + e);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < KPT; u++) {
+        if (row[u] == kNoRow) continue;
+        V* dst = reinterpret_cast<V*>(value_row(t, row[u]));
+#pragma unroll
+        for (int w = 0; w < 2; w++) {
+          const int e = e0 + w * kG;
+          if (e < nv) st_vec(dst + e, v[u][w]);
+        }
+      }
+    }
+  }
+}
+
+// Value reads resolved through the recorded provenance: the row's pre-batch
+// content (rsrc < 0) or the input of the op that wrote it earlier in the batch.
+//   list == nullptr: find_or_insert hits -> values[i] for outcome Found
+//   list != nullptr: insert_and_evict victims, j-th evicted op -> ev[j], ek/es
+template <int VEC>
+__global__ void __launch_bounds__(256) k_values_read(TableDev t, float* __restrict__ values,
+                                                     const uint8_t* __restrict__ outcomes,
+                                                     const uint32_t* __restrict__ rrow,
+                                                     const int32_t* __restrict__ rsrc, const uint32_t* list,
+                                                     const long long* n_list, const uint64_t* __restrict__ ek_tmp,
+                                                     const uint64_t* __restrict__ es_tmp, uint64_t* ek, uint64_t* es,
+                                                     float* ev, int64_t n, const Scalars* sc) {
+  if (sc->err) return;
+  const Tile8 tile;
+  const int r = tile.thread_rank();
+  const int64_t tid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
+  const int64_t ntiles = (int64_t)gridDim.x * blockDim.x / kG;
+  const int dim = t.dim;
+  const int64_t m = list ? (int64_t)*n_list : n;
+  for (int64_t j = tid; j < m; j += ntiles) {
+    uint32_t i;
+    float* dst;
+    if (list) {
+      i = list[j];
+      dst = ev + j * (int64_t)dim;
+      if (r == 0) {
+        ek[j] = ek_tmp[i];
+        es[j] = es_tmp[i];
+      }
+    } else {
+      i = (uint32_t)j;
+      if (outcomes[i] != kFound) continue;
+      dst = values + (uint64_t)i * dim;
+    }
+    const int32_t src = rsrc[i];
+    const float* from = src < 0 ? value_row(t, rrow[i]) : values + (uint64_t)src * dim;
+    copy_row<kG, VEC>(dst, from, dim, r);
+  }
 }
 
 // Dual mode: device-side leader rounds (table.py:945-962).
@@ -259,7 +680,7 @@ __global__ void __launch_bounds__(256) k_dual_rounds(TableDev t, OpArgs a, const
                                                      unsigned long long* round_ctr, int64_t n) {
   cg::grid_group grid = cg::this_grid();
   if (a.sc->err) return;
-  auto tile = cg::tiled_partition<kG>(cg::this_thread_block());
+  const Tile8 tile;
   const int r = tile.thread_rank();
   const int64_t tid = grid.thread_rank();
   const int64_t nthreads = grid.size();
@@ -268,8 +689,8 @@ __global__ void __launch_bounds__(256) k_dual_rounds(TableDev t, OpArgs a, const
   const uint64_t clock0 = *t.clock;
   const bool fel_open = !*t.fel_set;
   const unsigned long long round_base = *round_ctr;
-  unsigned long long ctr[6] = {0, 0, 0, 0, 0, 0};
-  long long sd = 0;
+  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
+  int sd = 0;
   unsigned m = (unsigned)n;
   uint32_t* cur = pend0;
   uint32_t* nxt = pend1;
@@ -338,7 +759,7 @@ __global__ void k_evict_gather(const Scalars* sc, const uint32_t* __restrict__ l
                                const uint64_t* __restrict__ ek_tmp, const uint64_t* __restrict__ es_tmp,
                                const float* __restrict__ ev_tmp, uint64_t* ek, uint64_t* es, float* ev,
                                int dim, int64_t n) {
-  auto tile = cg::tiled_partition<kG>(cg::this_thread_block());
+  const Tile8 tile;
   const int r = tile.thread_rank();
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
   const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / kG;
@@ -364,11 +785,11 @@ __global__ void __launch_bounds__(256) k_assign_find(TableDev t, const uint64_t*
                                                      uint32_t* __restrict__ rows, uint8_t* __restrict__ outcomes,
                                                      Scalars* sc) {
   if (sc->err) return;
-  auto tile = cg::tiled_partition<kG>(cg::this_thread_block());
+  const Tile8 tile;
   const int r = tile.thread_rank();
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
   const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / kG;
-  unsigned long long ctr[6] = {0, 0, 0, 0, 0, 0};
+  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
   for (int64_t i = gid; i < n; i += ngroups) {
     const uint64_t key = keys[i];
     const uint64_t h = fmix64(key);
@@ -400,18 +821,24 @@ __global__ void __launch_bounds__(256) k_assign_apply(TableDev t, const float* _
                                                       const uint32_t* __restrict__ ranks,
                                                       const uint64_t* __restrict__ ticks,
                                                       const uint32_t* __restrict__ sb,
-                                                      const uint32_t* __restrict__ sidx,
-                                                      const uint32_t* __restrict__ seg, int64_t n, Scalars* sc) {
+                                                      const uint32_t* __restrict__ sidx, int64_t n,
+                                                      Scalars* sc) {
   if (sc->err) return;
-  auto tile = cg::tiled_partition<kG>(cg::this_thread_block());
+  const Tile8 tile;
   const int r = tile.thread_rank();
-  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
-  const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / kG;
+  const int64_t tid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
+  const int64_t ntiles = (int64_t)gridDim.x * blockDim.x / kG;
   const uint64_t clock0 = *t.clock;
-  const unsigned nseg = sc->nseg;
-  unsigned long long ctr[6] = {0, 0, 0, 0, 0, 0};
-  for (int64_t s = gid; s < nseg; s += ngroups) {
-    int64_t p = seg[s];
+  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t base = tid * kG; base < n; base += ntiles * kG) {
+   const int64_t pp = base + r;
+   bool head = false;
+   if (pp < n) head = (pp == 0) || (sb[pp - 1] != sb[pp]);
+   uint32_t hm = tile.ballot(head);
+   while (hm) {
+    const int hl = __ffs(hm) - 1;
+    hm &= hm - 1;
+    int64_t p = base + hl;
     const uint32_t b = sb[p];
     while (true) {
       const uint32_t i = sidx[p];
@@ -432,6 +859,7 @@ __global__ void __launch_bounds__(256) k_assign_apply(TableDev t, const float* _
       }
       if (++p >= n || sb[p] != b) break;
     }
+   }
   }
   if (r != 0) {
 #pragma unroll
@@ -461,7 +889,7 @@ static cudaError_t grow(T*& p, int64_t count) {
   return cudaMalloc((void**)&p, sizeof(T) * (size_t)count);
 }
 
-cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, bool need_ev, bool dual) {
+cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual) {
   cudaError_t e = cudaSuccess;
   if (!ws.sc) {
     e = cudaMalloc((void**)&ws.sc, sizeof(Scalars));
@@ -470,7 +898,8 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, bool need_ev, bool dua
   if (n > ws.cap_n) {
     const int64_t c = n + n / 4 + 1024;
     if ((e = grow(ws.bkt, c)) || (e = grow(ws.idx, c)) || (e = grow(ws.sbkt, c)) || (e = grow(ws.sidx, c)) ||
-        (e = grow(ws.seg, c)) || (e = grow(ws.aux, c)) || (e = grow(ws.aux2, c)))
+        (e = grow(ws.seg, c)) || (e = grow(ws.aux, c)) || (e = grow(ws.aux2, c)) || (e = grow(ws.skey, 3 * c)) ||
+        (e = grow(ws.vrow, c)) || (e = grow(ws.rrow, c)) || (e = grow(ws.rsrc, c)))
       return e;
     if (ws.b2) { cudaFree(ws.b2); ws.b2 = nullptr; }
     if (ws.pend) { cudaFree(ws.pend); ws.pend = nullptr; }
@@ -479,34 +908,44 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, bool need_ev, bool dua
   if (dual && !ws.b2) {
     if ((e = grow(ws.b2, ws.cap_n)) || (e = grow(ws.pend, ws.cap_n))) return e;
   }
-  if (need_ev && (ws.cap_ev < n || ws.dim != dim)) {
-    const int64_t c = ws.cap_n;
-    if ((e = grow(ws.ek, c)) || (e = grow(ws.es, c)) || (e = grow(ws.ev, c * dim))) return e;
-    ws.cap_ev = c;
+  // ev_mode: 1 = per-op victim key/score scratch, 2 = also victim value rows (dual mode)
+  if (ev_mode >= 1 && ws.cap_ek < n) {
+    if ((e = grow(ws.ek, ws.cap_n)) || (e = grow(ws.es, ws.cap_n))) return e;
+    ws.cap_ek = ws.cap_n;
+  }
+  if (ev_mode >= 2 && (ws.cap_ev < n || ws.dim != dim)) {
+    if ((e = grow(ws.ev, ws.cap_n * dim))) return e;
+    ws.cap_ev = ws.cap_n;
     ws.dim = dim;
   }
   // CUB temp storage: the largest of sort / select / scan for cap_n items
-  size_t b_sort = 0, b_sel = 0, b_scan = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, b_sort, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                  (uint32_t*)nullptr, (int)ws.cap_n, 0, 32);
-  cub::CountingInputIterator<int64_t> cnt(0);
-  cub::TransformInputIterator<bool, IsEvicted, cub::CountingInputIterator<int64_t>> fl(cnt, IsEvicted{nullptr});
-  cub::DeviceSelect::Flagged(nullptr, b_sel, cnt, fl, (uint32_t*)nullptr, (long long*)nullptr, (int)ws.cap_n);
-  cub::TransformInputIterator<uint32_t, IsUpdated, cub::CountingInputIterator<int64_t>> up(cnt, IsUpdated{nullptr});
-  cub::DeviceScan::ExclusiveSum(nullptr, b_scan, up, (uint32_t*)nullptr, (int)ws.cap_n);
-  size_t need = b_sort > b_sel ? b_sort : b_sel;
-  if (b_scan > need) need = b_scan;
-  if (need > ws.cub_bytes) {
-    if (ws.cub_tmp) cudaFree(ws.cub_tmp);
-    ws.cub_tmp = nullptr;
-    if ((e = cudaMalloc(&ws.cub_tmp, need))) return e;
-    ws.cub_bytes = need;
+  // (queried only when the capacity changes: the queries cost host time)
+  if (ws.cub_for_n != ws.cap_n) {
+    size_t b_sort = 0, b_sel = 0, b_scan = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b_sort, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, (int)ws.cap_n, 0, 32);
+    cub::CountingInputIterator<int64_t> cnt(0);
+    cub::TransformInputIterator<bool, IsEvicted, cub::CountingInputIterator<int64_t>> fl(cnt, IsEvicted{nullptr});
+    cub::DeviceSelect::Flagged(nullptr, b_sel, cnt, fl, (uint32_t*)nullptr, (long long*)nullptr, (int)ws.cap_n);
+    cub::TransformInputIterator<uint32_t, IsUpdated, cub::CountingInputIterator<int64_t>> up(cnt,
+                                                                                            IsUpdated{nullptr});
+    cub::DeviceScan::ExclusiveSum(nullptr, b_scan, up, (uint32_t*)nullptr, (int)ws.cap_n);
+    size_t need = b_sort > b_sel ? b_sort : b_sel;
+    if (b_scan > need) need = b_scan;
+    if (need > ws.cub_bytes) {
+      if (ws.cub_tmp) cudaFree(ws.cub_tmp);
+      ws.cub_tmp = nullptr;
+      if ((e = cudaMalloc(&ws.cub_tmp, need))) return e;
+      ws.cub_bytes = need;
+    }
+    ws.cub_for_n = ws.cap_n;
   }
   return cudaSuccess;
 }
 
 void ws_free(Workspace& ws) {
-  void* ptrs[] = {ws.bkt, ws.idx, ws.sbkt, ws.sidx, ws.seg, ws.aux, ws.aux2, ws.b2, ws.pend,
+  void* ptrs[] = {ws.bkt, ws.idx, ws.sbkt, ws.sidx, ws.seg, ws.aux, ws.aux2, ws.skey, ws.vrow, ws.rrow, ws.rsrc,
+                  ws.b2, ws.pend,
                   ws.ek, ws.es, ws.ev, ws.cub_tmp, ws.sc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -535,8 +974,6 @@ static cudaError_t sort_segments(Workspace& ws, int64_t n, int log2_buckets, cud
                                                   end_bit, s);
   if (e) return e;
   g_launches += 4;  // onesweep: histogram + up to 3 passes (approximate)
-  k_heads<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ws.sbkt, n, ws.seg, ws.sc);
-  g_launches++;
   return cudaGetLastError();
 }
 
@@ -546,7 +983,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
                          cudaStream_t s, int num_sms) {
   cudaError_t e;
   const bool collect = a.collect != 0;
-  if ((e = ws_reserve(ws, n, t.dim, collect, t.dual != 0))) return e;
+  if ((e = ws_reserve(ws, n, t.dim, collect ? (t.dual ? 2 : 1) : 0, t.dual != 0))) return e;
   a.sc = ws.sc;
   a.ek = ws.ek;
   a.es = ws.es;
@@ -559,11 +996,16 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
     const int vec = vec_of(t.dim, a.values, t.vfast, t.vover, collect ? ws.ev : nullptr);
     if (!t.dual) {
       if ((e = sort_segments(ws, n, log2_buckets, s))) return e;
-      const int64_t blocks = tile_blocks(n, num_sms);
+      SegRec* recs = reinterpret_cast<SegRec*>(ws.skey);
+      k_segments<<<(unsigned)((n + 1023) / 1024), 1024, 0, s>>>(ws.sbkt, ws.sidx, a.keys, n, recs, n, ws.sc);
+      g_launches++;
+      int64_t blocks = (((n + kG - 1) / kG) * kG + 255) / 256;
+      if (blocks > (int64_t)num_sms * 3) blocks = (int64_t)num_sms * 3;  // one resident wave (3 blocks/SM)
       ktimer_begin("apply", s);
-      if (vec == 4) k_apply_segments<4><<<(unsigned)blocks, 256, 0, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, n);
-      else if (vec == 2) k_apply_segments<2><<<(unsigned)blocks, 256, 0, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, n);
-      else k_apply_segments<1><<<(unsigned)blocks, 256, 0, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, n);
+      auto* fn = a.op == kOpErase ? k_meta_single<kOpErase, false>
+                 : a.op == kOpFindOrInsert ? k_meta_single<kOpFindOrInsert, false>
+                 : a.collect ? k_meta_single<kOpUpsert, true> : k_meta_single<kOpUpsert, false>;
+      fn<<<(unsigned)blocks, 256, 0, s>>>(t, a, ws.sbkt, ws.sidx, recs, n, n, ws.vrow, ws.rrow, ws.rsrc);
       ktimer_end("apply", s);
       g_launches++;
     } else {
@@ -590,30 +1032,60 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
   }
   k_finalize<<<1, 1024, 0, s>>>(t, ws.sc, a.op == kOpErase ? nullptr : a.outcomes, n, clock_advance, 0);
   g_launches++;
-  if (collect) {
+  long long* nev = reinterpret_cast<long long*>(n_evicted);
+  if (collect && n > 0) {
     size_t bytes = ws.cub_bytes;
     cub::CountingInputIterator<int64_t> cnt(0);
     cub::TransformInputIterator<bool, IsEvicted, cub::CountingInputIterator<int64_t>> fl(cnt, IsEvicted{a.outcomes});
-    long long* nev = reinterpret_cast<long long*>(n_evicted);
-    if (n > 0) {
-      if ((e = cub::DeviceSelect::Flagged(ws.cub_tmp, bytes, cnt, fl, ws.aux, nev, (int)n, s))) return e;
-      g_launches += 2;
-      const int vec = vec_of(t.dim, ev_out, ws.ev, nullptr, nullptr);
-      const int64_t blocks = tile_blocks(n, num_sms);
-      if (vec == 4)
-        k_evict_gather<4><<<(unsigned)blocks, 256, 0, s>>>(ws.sc, ws.aux, nev, ws.ek, ws.es, ws.ev, ek_out, es_out,
-                                                           ev_out, t.dim, n);
-      else if (vec == 2)
-        k_evict_gather<2><<<(unsigned)blocks, 256, 0, s>>>(ws.sc, ws.aux, nev, ws.ek, ws.es, ws.ev, ek_out, es_out,
-                                                           ev_out, t.dim, n);
+    if ((e = cub::DeviceSelect::Flagged(ws.cub_tmp, bytes, cnt, fl, ws.aux, nev, (int)n, s))) return e;
+    g_launches += 2;
+  }
+  const int64_t vblocks = tile_blocks(n, num_sms);
+  if (!t.dual && n > 0 && a.op != kOpErase) {
+    // value reads (provenance-resolved) strictly before value writes
+    const int vr = vec_of(t.dim, a.values, t.vfast, t.vover, collect ? ev_out : nullptr);
+    if (collect || a.op == kOpFindOrInsert) {
+      const uint32_t* list = collect ? ws.aux : nullptr;
+      if (vr == 4)
+        k_values_read<4><<<(unsigned)vblocks, 256, 0, s>>>(t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
+                                                           ws.ek, ws.es, ek_out, es_out, ev_out, n, ws.sc);
+      else if (vr == 2)
+        k_values_read<2><<<(unsigned)vblocks, 256, 0, s>>>(t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
+                                                           ws.ek, ws.es, ek_out, es_out, ev_out, n, ws.sc);
       else
-        k_evict_gather<1><<<(unsigned)blocks, 256, 0, s>>>(ws.sc, ws.aux, nev, ws.ek, ws.es, ws.ev, ek_out, es_out,
-                                                           ev_out, t.dim, n);
+        k_values_read<1><<<(unsigned)vblocks, 256, 0, s>>>(t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
+                                                           ws.ek, ws.es, ek_out, es_out, ev_out, n, ws.sc);
       g_launches++;
+    }
+    ktimer_begin("values_write", s);
+    const int64_t wblocks = (((n + 3) / 4) * kG + 255) / 256;
+    const int64_t wcap = (int64_t)num_sms * 8 * 4;
+    const unsigned wb = (unsigned)(wblocks < wcap ? (wblocks < 1 ? 1 : wblocks) : wcap);
+    if (vr == 4) k_values_write<4, 4><<<wb, 256, 0, s>>>(t, a.values, ws.vrow, n, ws.sc);
+    else if (vr == 2) k_values_write<2, 4><<<wb, 256, 0, s>>>(t, a.values, ws.vrow, n, ws.sc);
+    else k_values_write<1, 4><<<wb, 256, 0, s>>>(t, a.values, ws.vrow, n, ws.sc);
+    ktimer_end("values_write", s);
+    g_launches++;
+  }
+  if (collect) {
+    if (n > 0 && t.dual) {
+      const int vec = vec_of(t.dim, ev_out, ws.ev, nullptr, nullptr);
+      if (vec == 4)
+        k_evict_gather<4><<<(unsigned)vblocks, 256, 0, s>>>(ws.sc, ws.aux, nev, ws.ek, ws.es, ws.ev, ek_out, es_out,
+                                                            ev_out, t.dim, n);
+      else if (vec == 2)
+        k_evict_gather<2><<<(unsigned)vblocks, 256, 0, s>>>(ws.sc, ws.aux, nev, ws.ek, ws.es, ws.ev, ek_out, es_out,
+                                                            ev_out, t.dim, n);
+      else
+        k_evict_gather<1><<<(unsigned)vblocks, 256, 0, s>>>(ws.sc, ws.aux, nev, ws.ek, ws.es, ws.ev, ek_out, es_out,
+                                                            ev_out, t.dim, n);
+      g_launches++;
+    }
+    if (n > 0) {
       k_zero_count<<<1, 1, 0, s>>>(ws.sc, nev);
       g_launches++;
-    } else {
-      if ((e = cudaMemsetAsync(n_evicted, 0, sizeof(int64_t), s))) return e;
+    } else if ((e = cudaMemsetAsync(n_evicted, 0, sizeof(int64_t), s))) {
+      return e;
     }
   }
   return cudaGetLastError();
@@ -623,7 +1095,7 @@ cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* val
                        int refresh, uint64_t epoch, int64_t n, uint8_t* outcomes, const uint64_t* ticks,
                        uint64_t clock_advance, int log2_buckets, Workspace& ws, cudaStream_t s, int num_sms) {
   cudaError_t e;
-  if ((e = ws_reserve(ws, n, t.dim, false, false))) return e;
+  if ((e = ws_reserve(ws, n, t.dim, 0, false))) return e;
   if ((e = cudaMemsetAsync(ws.sc, 0, sizeof(Scalars), s))) return e;
   const bool need_ticks = refresh && !scores && !ticks;
   if (n > 0) {
@@ -647,13 +1119,13 @@ cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* val
     ktimer_begin("assign_apply", s);
     if (vec == 4)
       k_assign_apply<4><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks, ws.sbkt,
-                                                         ws.sidx, ws.seg, n, ws.sc);
+                                                         ws.sidx, n, ws.sc);
     else if (vec == 2)
       k_assign_apply<2><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks, ws.sbkt,
-                                                         ws.sidx, ws.seg, n, ws.sc);
+                                                         ws.sidx, n, ws.sc);
     else
       k_assign_apply<1><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks, ws.sbkt,
-                                                         ws.sidx, ws.seg, n, ws.sc);
+                                                         ws.sidx, n, ws.sc);
     ktimer_end("assign_apply", s);
     g_launches++;
   }

@@ -19,9 +19,9 @@ constexpr int kSPL = kSlots / kG;     // slots per lane (16)
 // compares exactly as table.py:243-268: one per candidate (digest equal and
 // key != EMPTY) in slot order, stopping at the match.
 template <bool kUseBits, bool kReadOnly>
-__device__ __forceinline__ int probe_bucket(const TableDev& t, const cg::thread_block_tile<kG>& tile,
+__device__ __forceinline__ int probe_bucket(const TableDev& t, const Tile8& tile,
                                             uint64_t b, uint64_t key, uint32_t d, uint32_t occ,
-                                            unsigned long long& n_compares) {
+                                            ctr_t& n_compares) {
   const int r = tile.thread_rank();
   uint32_t cand;
   if (t.digest_filter) {
@@ -60,16 +60,13 @@ __device__ __forceinline__ int probe_bucket(const TableDev& t, const cg::thread_
   } else {
     contrib = ncmp_all;
   }
-  // tile sum of compares
-#pragma unroll
-  for (int o = kG / 2; o > 0; o >>= 1) contrib += tile.shfl_xor(contrib, o);
-  n_compares += contrib;
+  n_compares += tile.sum((unsigned)contrib);
   return slot;
 }
 
 // Lowest (score, slot) over the bucket — np.argmin semantics (first index on
 // ties), table.py:1080.  Each lane scans its 16 scores (128 contiguous bytes).
-__device__ __forceinline__ void bucket_min(const TableDev& t, const cg::thread_block_tile<kG>& tile,
+__device__ __forceinline__ void bucket_min(const TableDev& t, const Tile8& tile,
                                            uint64_t b, uint64_t& minv, int& mslot) {
   const int r = tile.thread_rank();
   const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(t.scores + b * kSlots + r * kSPL);
@@ -101,10 +98,8 @@ __device__ __forceinline__ void store_occ(const TableDev& t, uint64_t b, int r, 
 }
 
 template <int G>
-__device__ __forceinline__ int tile_sum(const cg::thread_block_tile<G>& tile, int v) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) v += tile.shfl_xor(v, o);
-  return v;
+__device__ __forceinline__ int tile_sum(const Tile8& tile, int v) {
+  return (int)tile.sum((unsigned)v);  // REDUX over the tile's 8 lanes
 }
 
 }  // namespace hkv

@@ -241,8 +241,10 @@ class CacheTable:
         n = k.numel()
         dim = self.config.value_dim
         host_out = None
+        zero_misses = 0
         if out is None:
-            out_d = torch.zeros((n, dim), dtype=torch.float32, device=self.device)
+            out_d = torch.empty((n, dim), dtype=torch.float32, device=self.device)
+            zero_misses = 1  # the kernel zero-fills miss rows (== reference's np.zeros out)
         elif isinstance(out, torch.Tensor):
             if tuple(out.shape) != (n, dim) or out.dtype != torch.float32:
                 raise ValueError("out must be float32 with shape (len(keys), value_dim)")
@@ -255,7 +257,7 @@ class CacheTable:
         found = torch.empty(n, dtype=torch.bool, device=self.device)
         st = self._stream()
         with self.gate.acquire(Role.Reader, st):
-            _lib.check(self._lib.hkv_find(self._h, _ptr(k), n, _ptr(out_d), _ptr(found), self._sp()))
+            _lib.check(self._lib.hkv_find(self._h, _ptr(k), n, _ptr(out_d), _ptr(found), zero_misses, self._sp()))
         if not np_mode or np_mode == "host":
             self._check_device_error()
             if isinstance(out, torch.Tensor) and out_d is not out:
