@@ -119,6 +119,12 @@ class Clocks:
         except Exception:
             self.proc = None
 
+    def wait_first_sample(self, timeout=10.0):
+        t0 = time.time()
+        while self.proc is not None and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.05)
+        time.sleep(0.2)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
@@ -296,23 +302,28 @@ def run_single(a):
             e3.record(stream)
             h1 = time.perf_counter()
             t.restore()
+            if os.environ.get("BENCH_DEBUG"):
+                print(f"host step {s} lam {lam}: {1e3*(h1-h0):.3f} ms", file=sys.stderr)
             if timed:
                 host_s[0] += h1 - h0
                 rec.append((s, lam, e0, e1, e2, e3, o))
 
+    # the sampler starts before the warm-up (nvidia-smi start-up must not land in the timed region)
+    clocks.start()
+    clocks.wait_first_sample()
     for s in range(a.warmup):
         one_step(s, False)
     torch.cuda.synchronize()
     lib.hkv_set_kernel_timing(1)
     launches0 = lib.hkv_launch_count()
-    clocks.start()
-    time.sleep(0.3)
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push("timed")
     w0 = time.perf_counter()
     for s in range(a.warmup, n_steps):
         one_step(s, True)
     torch.cuda.synchronize()
     w1 = time.perf_counter()
+    torch.cuda.nvtx.range_pop()
     clk = clocks.stop()
     launches = lib.hkv_launch_count() - launches0
     lib.hkv_set_kernel_timing(0)
@@ -327,8 +338,6 @@ def run_single(a):
     find_ms, find_n = ktime("find")
     apply_ms, apply_n = ktime("apply")
     vw_ms, vw_n = ktime("values_write")
-    for s in range(a.warmup):
-        pass
     # device times
     per = {}
     tot_ms = 0.0
@@ -337,6 +346,8 @@ def run_single(a):
     for (s, lam, e0, e1, e2, e3, o) in rec:
         f_ms = e0.elapsed_time(e1)
         i_ms = e2.elapsed_time(e3)
+        if os.environ.get("BENCH_DEBUG"):
+            print(f"step {s} lam {lam}: find {f_ms:.3f} ms insert {i_ms:.3f} ms", file=sys.stderr)
         d = per.setdefault(lam, {"find_ms": [], "insert_ms": []})
         d["find_ms"].append(f_ms)
         d["insert_ms"].append(i_ms)

@@ -543,13 +543,14 @@ __device__ __forceinline__ void meta_pass(const TableDev& t, const OpArgs& a, co
           i = sidx[q];
           key = a.keys[i];
           d = digest_of(fmix64(key));
-          __syncwarp();
-          load_slices(t, true, b, r, dw, occ);  // re-read after this tile's own writes
         } else {
           active = false;
         }
       }
+      // full-warp fence (every lane reaches it), then re-read after this tile's own writes
       if (!__any_sync(kFull, active)) break;
+      __syncwarp();
+      if (active) load_slices(t, true, b, r, dw, occ);
     }
     rec = rec_n;
     rec_n = rec_nn;
