@@ -25,6 +25,7 @@
 // bucket, tile-wide argmin over the score row, admission test and eviction
 // (_finish_admission, table.py:1121-1163).
 #include <cub/cub.cuh>
+#include <thrust/iterator/reverse_iterator.h>
 
 #include "hkv_kernels.h"
 #include "hkv_probe.cuh"
@@ -252,20 +253,47 @@ struct SegRec {
 // Segment records split into two lists: singleton segments from the front
 // of `recs`, multi-op segments from the back (recs[cap-1], recs[cap-2], ...),
 // so the metadata pass can run each class in lockstep without waste.
+//
+// Same-key runs (zipf batches: one key can fill tens of thousands of
+// consecutive sorted positions of its bucket): for every
+// position p inside a multi-op segment, brk[p] = p unless the op at p+1 has the
+// same key (then ~0), so a reverse min-scan gives run_end[p] = the last
+// position of p's run.  Followers (p-1 has the same key) get the collapsed
+// outcome `fcode` and no value row up front; apply_run writes the exceptions.
 __global__ void __launch_bounds__(1024) k_segments(const uint32_t* __restrict__ sb, const uint32_t* __restrict__ sidx,
                                                    const uint64_t* __restrict__ keys, int64_t n,
-                                                   SegRec* __restrict__ recs, int64_t cap, Scalars* sc) {
+                                                   SegRec* __restrict__ recs, int64_t cap, Scalars* sc,
+                                                   uint32_t* __restrict__ brk, uint8_t* __restrict__ outcomes,
+                                                   uint32_t* __restrict__ vrow, uint8_t fcode) {
   __shared__ unsigned wcount[2][32];
   __shared__ unsigned block_base[2];
   if (sc->err) return;
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   uint32_t b = kNoRow;
-  bool head = false, multi = false;
+  bool head = false, multi = false, prev_same_b = false;
+  uint32_t i = 0;
   if (p < n) {
     b = sb[p];
-    head = (p == 0) || (sb[p - 1] != b);
+    i = sidx[p];
+    prev_same_b = (p > 0) && (sb[p - 1] == b);
+    head = !prev_same_b;
     multi = (p + 1 < n) && (sb[p + 1] == b);
+  }
+  // same-key test with both neighbours (keys of multi-op segments only)
+  const bool in_multi = multi || prev_same_b;
+  const uint64_t k = in_multi ? keys[i] : 0;
+  uint64_t k_next = __shfl_down_sync(kFull, k, 1);
+  uint64_t k_prev = __shfl_up_sync(kFull, k, 1);
+  if (lane == 31 && multi) k_next = keys[sidx[p + 1]];
+  if (lane == 0 && prev_same_b) k_prev = keys[sidx[p - 1]];
+  if (p < n) {
+    const bool same_next = multi && k_next == k;
+    brk[p] = same_next ? 0xFFFFFFFFu : (uint32_t)p;
+    if (prev_same_b && k_prev == k) {
+      outcomes[i] = fcode;
+      vrow[i] = kNoRow;
+    }
   }
   const unsigned ms = __ballot_sync(kFull, head && !multi);
   const unsigned mm = __ballot_sync(kFull, head && multi);
@@ -286,9 +314,8 @@ __global__ void __launch_bounds__(1024) k_segments(const uint32_t* __restrict__ 
   }
   __syncthreads();
   if (head) {
-    const uint32_t i = sidx[p];
     SegRec rec;
-    rec.key = keys[i];
+    rec.key = in_multi ? k : keys[i];
     rec.p = (uint32_t)p;
     rec.b = b;
     rec.i = i;
@@ -321,8 +348,9 @@ struct LastWriter {  // per-tile shared-memory view
 
 // One op of every active tile of the warp (must be called by all 32 lanes).
 // dw/occ: this lane's digest / occupancy slice of bucket b, already loaded.
+// Returns (tile-uniform) the slot holding `key` after the op, -1 if absent.
 template <int OP, bool COLLECT>
-__device__ __forceinline__ void meta_op_ws(const TableDev& t, const OpArgs& a, unsigned lane, bool active,
+__device__ __forceinline__ int meta_op_ws(const TableDev& t, const OpArgs& a, unsigned lane, bool active,
                                            uint32_t i, uint64_t key, uint32_t d, uint64_t b, uint4 dw, uint32_t occ,
                                            uint64_t clock0, bool fel_open, bool spec, LastWriter& lw,
                                            uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
@@ -379,7 +407,7 @@ __device__ __forceinline__ void meta_op_ws(const TableDev& t, const OpArgs& a, u
       if (r == 0) size_delta--;
     }
     if (active && r == 0) a.outcomes[i] = slot >= 0 ? kErased : kNotFound;
-    return;
+    return -1;
   }
   const bool is_hit = active && slot >= 0;
   const bool miss = active && slot < 0;
@@ -456,7 +484,7 @@ __device__ __forceinline__ void meta_op_ws(const TableDev& t, const OpArgs& a, u
       }
     }
   }
-  if (!active) return;
+  if (!active) return -1;
   // value plan (provenance read BEFORE this op's own write is recorded)
   if (rslot >= 0) {
     if (r == 0) ctr[rowbase + rslot < t.fast_rows ? kVFast : kVOver]++;
@@ -477,6 +505,86 @@ __device__ __forceinline__ void meta_op_ws(const TableDev& t, const OpArgs& a, u
     vrow[i] = kNoRow;
   }
   if (r == 0) a.outcomes[i] = outcome;
+  return rslot >= 0 ? rslot : wslot;
+}
+
+// Score after `cnt` consecutive hits of one key, the last one with tick tl /
+// custom score cs (scoring.py:79-102 applied cnt times; Lfu / EpochLfu
+// saturate exactly like the one-at-a-time loop).
+__device__ __forceinline__ uint64_t run_hit_score(int policy, uint64_t old, uint64_t epoch, uint64_t tl,
+                                                  bool has_custom, uint64_t cs, uint32_t cnt) {
+  switch (policy) {
+    case kLfu: return (kMaxScore - old < cnt) ? kMaxScore : old + cnt;
+    case kEpochLfu: {
+      uint64_t low;
+      if ((old >> 32) == epoch) {
+        low = old & kLow32;
+        low = (kLow32 - low < cnt) ? kLow32 : low + cnt;
+      } else {
+        low = (uint64_t)cnt;  // first hit resets to 1, the rest add 1 each
+        if (low > kLow32) low = kLow32;
+      }
+      return (epoch << 32) | low;
+    }
+    default: return hit_score(policy, old, epoch, tl, has_custom, cs);
+  }
+}
+
+// A run of consecutive ops on one key inside a bucket segment (sorted
+// positions q+1 .. qe, all after the op at q).  Under serial semantics
+// every one of them sees the bucket exactly as the
+// op at q left it, so the run applies in O(1):
+//   key resident at slot `res`  -> cnt hits: Updated / Found, one aggregated
+//                                  score refresh, the last op's value wins
+//   erase                       -> key absent: NotFound
+//   absent, Lfu / EpochLfu      -> same admission score, same bucket: Rejected
+// Followers' outcome / vrow were pre-set by k_segments (Updated / Found /
+// NotFound, no value row); only the exceptions are written here.  TxnCounters
+// are exactly those of cnt individual probes.  Per-tile code, no collectives.
+template <int OP>
+__device__ __forceinline__ void apply_run(const TableDev& t, const OpArgs& a, int r, int64_t q, int64_t qe, int res,
+                                          uint64_t b, uint32_t d, uint4 dw, uint32_t occ, uint64_t clock0,
+                                          const uint32_t* __restrict__ sidx, LastWriter& lw,
+                                          uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
+                                          int32_t* __restrict__ rsrc, ctr_t* ctr) {
+  const uint32_t cnt = (uint32_t)(qe - q);
+  const uint64_t rowbase = b * kSlots;
+  uint32_t cand = (t.digest_filter ? match16(dw, d) : 0xFFFFu) & occ;
+  if (res >= 0) {  // compares stop at the match (table.py:243-268)
+    const int ol = res / kSPL;
+    if (r > ol) cand = 0;
+    else if (r == ol) cand &= (2u << (res % kSPL)) - 1u;
+  }
+  ctr[kCompares] += cnt * (uint32_t)__popc(cand);
+  if (r == 0) ctr[kLoads] += cnt;
+  if constexpr (OP == kOpErase) return;
+  if (res < 0) {  // rejected run
+    if (r == 0) ctr[kScans] += cnt;
+    for (int64_t p = q + 1 + r; p <= qe; p += kG) a.outcomes[sidx[p]] = kRejected;
+    return;
+  }
+  const uint64_t row = rowbase + res;
+  if (r == 0) ctr[row < t.fast_rows ? kVFast : kVOver] += cnt;
+  const uint32_t il = sidx[qe];
+  if (res / kSPL == r) {
+    const uint64_t tl = a.ticks ? a.ticks[il] : clock0 + (uint64_t)il + 1;
+    const uint64_t cs = a.scores ? a.scores[il] : 0;
+    t.scores[row] = run_hit_score(t.policy, t.scores[row], a.epoch, tl, a.scores != nullptr, cs, cnt);
+    if constexpr (OP == kOpUpsert) {
+      const int prev = lw.get(res);
+      if (prev >= 0) vrow[prev] = kNoRow;
+      lw.set(res, (int)il);
+      vrow[il] = (uint32_t)row;
+    }
+  }
+  if constexpr (OP == kOpFindOrInsert) {  // every follower reads what the run head left in the row
+    const int src = lw.get(res);
+    for (int64_t p = q + 1 + r; p <= qe; p += kG) {
+      const uint32_t i = sidx[p];
+      rrow[i] = (uint32_t)row;
+      rsrc[i] = src;
+    }
+  }
 }
 
 __device__ __forceinline__ void load_slices(const TableDev& t, bool active, uint64_t b, int r, uint4& dw,
@@ -496,16 +604,18 @@ __device__ __forceinline__ void load_slices(const TableDev& t, bool active, uint
 // never be stale.
 template <int OP, bool COLLECT>
 __device__ __forceinline__ void meta_pass(const TableDev& t, const OpArgs& a, const uint32_t* __restrict__ sb,
-                                          const uint32_t* __restrict__ sidx, const SegRec* __restrict__ recs,
-                                          int64_t nrec, int64_t dir, int64_t n, uint32_t* __restrict__ vrow,
-                                          uint32_t* __restrict__ rrow, int32_t* __restrict__ rsrc, LastWriter& lw,
-                                          uint64_t clock0, bool fel_open, bool spec, ctr_t* ctr, int& sd) {
+                                          const uint32_t* __restrict__ sidx, const uint32_t* __restrict__ run_end,
+                                          const SegRec* __restrict__ recs, int64_t nrec, int64_t dir, int64_t n,
+                                          uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
+                                          int32_t* __restrict__ rsrc, LastWriter& lw, uint64_t clock0, bool fel_open,
+                                          bool spec, ctr_t* ctr, int& sd) {
   const unsigned lane = threadIdx.x & 31u;
   const int r = (int)(lane & 7u);
   const int tile_in_warp = (int)(lane >> 3);
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t stride = nwarps * 4;
+  const bool lfu_like = t.policy == kLfu || t.policy == kEpochLfu;
   auto rec_at = [&](int64_t sg) -> SegRec {
     if (sg < nrec) return recs[dir > 0 ? sg : -sg];
     return SegRec{0, 0, 0, 0, 0};
@@ -536,13 +646,14 @@ __device__ __forceinline__ void meta_pass(const TableDev& t, const OpArgs& a, co
     lw.cur++;
     __syncwarp();
     while (true) {
-      meta_op_ws<OP, COLLECT>(t, a, lane, active, i, key, d, b, dw, occ, clock0, fel_open, spec, lw, vrow, rrow,
-                              rsrc, ctr, sd);
+      const int res = meta_op_ws<OP, COLLECT>(t, a, lane, active, i, key, d, b, dw, occ, clock0, fel_open, spec, lw,
+                                              vrow, rrow, rsrc, ctr, sd);
+      // next op of the segment; a same-key run after it collapses (apply_run)
+      int64_t run_to = -1;
       if (active) {
-        if (multi && ++q < n && sb[q] == (uint32_t)b) {
-          i = sidx[q];
-          key = a.keys[i];
-          d = digest_of(fmix64(key));
+        if (multi && q + 1 < n && sb[q + 1] == (uint32_t)b) {
+          const int64_t qe = (int64_t)run_end[q];
+          if (qe > q && (OP == kOpErase || res >= 0 || lfu_like)) run_to = qe;
         } else {
           active = false;
         }
@@ -550,7 +661,21 @@ __device__ __forceinline__ void meta_pass(const TableDev& t, const OpArgs& a, co
       // full-warp fence (every lane reaches it), then re-read after this tile's own writes
       if (!__any_sync(kFull, active)) break;
       __syncwarp();
-      if (active) load_slices(t, true, b, r, dw, occ);
+      if (active) {
+        load_slices(t, true, b, r, dw, occ);
+        if (run_to >= 0) {
+          apply_run<OP>(t, a, r, q, run_to, res, b, d, dw, occ, clock0, sidx, lw, vrow, rrow, rsrc, ctr);
+          q = run_to;  // a run changes one score only: digest / occupancy slices stay valid
+          if (!(q + 1 < n && sb[q + 1] == (uint32_t)b)) active = false;
+        }
+        if (active) {
+          ++q;
+          i = sidx[q];
+          key = a.keys[i];
+          d = digest_of(fmix64(key));
+        }
+      }
+      if (!__any_sync(kFull, active)) break;
     }
     rec = rec_n;
     rec_n = rec_nn;
@@ -562,6 +687,7 @@ __device__ __forceinline__ void meta_pass(const TableDev& t, const OpArgs& a, co
 template <int OP, bool COLLECT>
 __global__ void __launch_bounds__(256, 3) k_meta_single(TableDev t, OpArgs a, const uint32_t* __restrict__ sb,
                                                         const uint32_t* __restrict__ sidx,
+                                                        const uint32_t* __restrict__ run_end,
                                                         const SegRec* __restrict__ recs, int64_t cap, int64_t n,
                                                         uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
                                                         int32_t* __restrict__ rsrc) {
@@ -582,10 +708,10 @@ __global__ void __launch_bounds__(256, 3) k_meta_single(TableDev t, OpArgs a, co
   const bool spec = sz * 100ull > t.capacity * 97ull;
   ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
   int sd = 0;
-  meta_pass<OP, COLLECT>(t, a, sb, sidx, recs, (int64_t)a.sc->nseg, 1, n, vrow, rrow, rsrc, lw, clock0, fel_open, spec,
-                         ctr, sd);
-  meta_pass<OP, COLLECT>(t, a, sb, sidx, recs + (cap - 1), (int64_t)a.sc->nmulti, -1, n, vrow, rrow, rsrc, lw, clock0,
+  meta_pass<OP, COLLECT>(t, a, sb, sidx, run_end, recs, (int64_t)a.sc->nseg, 1, n, vrow, rrow, rsrc, lw, clock0,
                          fel_open, spec, ctr, sd);
+  meta_pass<OP, COLLECT>(t, a, sb, sidx, run_end, recs + (cap - 1), (int64_t)a.sc->nmulti, -1, n, vrow, rrow, rsrc,
+                         lw, clock0, fel_open, spec, ctr, sd);
   block_ctrs_flush(bc, t.counters, t.size, ctr, sd);
 }
 
@@ -931,8 +1057,13 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual
     cub::TransformInputIterator<uint32_t, IsUpdated, cub::CountingInputIterator<int64_t>> up(cnt,
                                                                                             IsUpdated{nullptr});
     cub::DeviceScan::ExclusiveSum(nullptr, b_scan, up, (uint32_t*)nullptr, (int)ws.cap_n);
+    size_t b_min = 0;
+    thrust::reverse_iterator<const uint32_t*> rin(nullptr);
+    thrust::reverse_iterator<uint32_t*> rout(nullptr);
+    cub::DeviceScan::InclusiveScan(nullptr, b_min, rin, rout, cub::Min(), (int)ws.cap_n);
     size_t need = b_sort > b_sel ? b_sort : b_sel;
     if (b_scan > need) need = b_scan;
+    if (b_min > need) need = b_min;
     if (need > ws.cub_bytes) {
       if (ws.cub_tmp) cudaFree(ws.cub_tmp);
       ws.cub_tmp = nullptr;
@@ -978,6 +1109,17 @@ static cudaError_t sort_segments(Workspace& ws, int64_t n, int log2_buckets, cud
   return cudaGetLastError();
 }
 
+// run_end[p] = min{p' >= p : brk[p'] != ~0} — a reverse inclusive min-scan
+// over brk (k_segments) giving the last position of p's same-key run.
+static cudaError_t run_ends(Workspace& ws, int64_t n, cudaStream_t s) {
+  size_t bytes = ws.cub_bytes;
+  thrust::reverse_iterator<const uint32_t*> in(ws.aux2 + n);
+  thrust::reverse_iterator<uint32_t*> out(ws.seg + n);
+  cudaError_t e = cub::DeviceScan::InclusiveScan(ws.cub_tmp, bytes, in, out, cub::Min(), (int)n, s);
+  g_launches += 2;
+  return e ? e : cudaGetLastError();
+}
+
 cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, Workspace& ws,
                          unsigned long long* round_ctr, unsigned long long* lead, int64_t* n_evicted,
                          uint64_t* ek_out, float* ev_out, uint64_t* es_out, uint64_t clock_advance,
@@ -998,15 +1140,18 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
     if (!t.dual) {
       if ((e = sort_segments(ws, n, log2_buckets, s))) return e;
       SegRec* recs = reinterpret_cast<SegRec*>(ws.skey);
-      k_segments<<<(unsigned)((n + 1023) / 1024), 1024, 0, s>>>(ws.sbkt, ws.sidx, a.keys, n, recs, n, ws.sc);
+      const uint8_t fcode = a.op == kOpErase ? kNotFound : a.op == kOpFindOrInsert ? kFound : kUpdated;
+      k_segments<<<(unsigned)((n + 1023) / 1024), 1024, 0, s>>>(ws.sbkt, ws.sidx, a.keys, n, recs, n, ws.sc, ws.aux2,
+                                                                 a.outcomes, ws.vrow, fcode);
       g_launches++;
+      if ((e = run_ends(ws, n, s))) return e;
       int64_t blocks = (((n + kG - 1) / kG) * kG + 255) / 256;
       if (blocks > (int64_t)num_sms * 3) blocks = (int64_t)num_sms * 3;  // one resident wave (3 blocks/SM)
       ktimer_begin("apply", s);
       auto* fn = a.op == kOpErase ? k_meta_single<kOpErase, false>
                  : a.op == kOpFindOrInsert ? k_meta_single<kOpFindOrInsert, false>
                  : a.collect ? k_meta_single<kOpUpsert, true> : k_meta_single<kOpUpsert, false>;
-      fn<<<(unsigned)blocks, 256, 0, s>>>(t, a, ws.sbkt, ws.sidx, recs, n, n, ws.vrow, ws.rrow, ws.rsrc);
+      fn<<<(unsigned)blocks, 256, 0, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, recs, n, n, ws.vrow, ws.rrow, ws.rsrc);
       ktimer_end("apply", s);
       g_launches++;
     } else {

@@ -253,3 +253,39 @@ def test_full_size_properties_dim64(hkv):
     expect = (res.to(torch.float32) / 1e12).unsqueeze(1).expand(-1, dim)
     assert torch.equal(v, expect)
     assert res.numel() == t.size()
+
+
+@pytest.mark.parametrize("policy", POLICIES)
+def test_zipf_same_key_runs(hkv, policy):
+    """Zipf batches (alpha 0.99, small universe): one key fills thousands of
+    consecutive sorted positions of its bucket, so the collapsed same-key
+    runs (hits, rejections under Lfu, erase misses, find_or_insert reads) are
+    exercised against the one-at-a-time oracle, bit-exact incl. counters."""
+    from paper_2603_17168_b200.workloads import zipf_keys
+
+    cap, dim = 128 * 32, 4
+    t = make_table(hkv, cap, dim, policy=policy)
+    o = OracleTable(cap, dim, "single", policy)
+    rng = np.random.default_rng(11)
+    custom = policy == "kCustomized"
+    for j in range(14):
+        keys = zipf_keys(20_000, 6 * cap, 0.99, seed=j)
+        vals = rng.standard_normal((len(keys), dim)).astype(np.float32)
+        sc = rng.integers(0, 60, size=len(keys), dtype=np.uint64) if custom else None
+        op = ["insert_or_assign", "insert_and_evict", "find_or_insert", "insert_and_evict", "erase", "assign",
+              "insert_or_assign"][j % 7]
+        if op == "erase":
+            args = {"keys": keys[: len(keys) // 2]}
+        elif op == "assign":
+            args = {"keys": keys, "values": vals}
+        else:
+            args = {"keys": keys, "values": vals, "scores": sc}
+        r_t = run_impl(t, op, args)
+        r_o = run_impl(o, op, args)
+        assert outputs_equal(r_o, r_t), f"batch {j} {op}"
+        if policy in ("kEpochLru", "kEpochLfu") and j % 4 == 3:
+            t.set_epoch(j)
+            o.set_epoch(j)
+    assert_same_state(t, o)
+    assert t.counters.as_dict() == o.counters
+    assert t.check_consistency()
