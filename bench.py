@@ -39,7 +39,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -50,6 +49,7 @@ sys.path.insert(0, ROOT)
 METRIC = "find and insert_or_assign B-KV/s at λ=0.50/0.75/1.00, dim=64 fp32"
 UNIT = "B-KV/s"
 SLOTS = 128
+SPIN_CYCLES = 400_000  # ~0.2 ms at 1.965 GHz
 
 
 def parse():
@@ -108,26 +108,37 @@ class Clocks:
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
+        self.path = None
 
     def start(self):
+        # nvidia-smi writes to a file: no reader thread in this process (a
+        # Python thread competing for the GIL stalls the host mid-op)
+        import tempfile
+
         try:
+            fd, self.path = tempfile.mkstemp(prefix="hkv_clocks_", suffix=".csv")
+            self.fh = os.fdopen(fd, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+                                         stdout=self.fh, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
 
+    def _load(self):
+        try:
+            with open(self.path) as f:
+                self.lines = [ln.strip() for ln in f if ln.strip()]
+        except Exception:
+            self.lines = []
+
     def wait_first_sample(self, timeout=10.0):
         t0 = time.time()
-        while self.proc is not None and not self.lines and time.time() - t0 < timeout:
+        while self.proc is not None and time.time() - t0 < timeout:
+            self._load()
+            if self.lines:
+                break
             time.sleep(0.05)
         time.sleep(0.2)
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
 
     def stop(self):
         if self.proc is None:
@@ -137,6 +148,12 @@ class Clocks:
             self.proc.wait(2)
         except Exception:
             self.proc.kill()
+        self.fh.close()
+        self._load()
+        try:
+            os.unlink(self.path)
+        except OSError:
+            pass
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -280,52 +297,97 @@ def run_single(a):
         queries[lam] = res[idx].contiguous()
         del res
     vals = torch.randn((B, dim), device="cuda", generator=gen)
+    find_out = torch.empty((B, dim), device="cuda")  # caller-owned output (find(keys, out=...), table.py:304)
+    # pre-grow torch's caching allocator for every output the timed ops will
+    # allocate (found masks, retained outcome arrays): a cudaMalloc inside a
+    # timed pair was seen to stall the host for up to ~100 ms
+    _warm = [torch.empty(B, dtype=torch.uint8, device="cuda") for _ in range(2 * len(a.lambdas) * (a.steps + a.warmup) + 16)]
+    del _warm
     n_steps = a.warmup + a.steps
+    if os.environ.get("BENCH_DEBUG"):
+        free, total = torch.cuda.mem_get_info()
+        print(f"device memory free {free / 2**30:.1f} GiB of {total / 2**30:.1f}; torch reserved "
+              f"{torch.cuda.memory_reserved() / 2**30:.1f} GiB", file=sys.stderr)
     ins_keys = [W.uniform_distinct_keys_torch(B, 0, stream_offset=2**44 + s * B) for s in range(n_steps)]
 
     stream = torch.cuda.current_stream()
-    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    # events are created (first record) before the timed region: creating one
+    # inside it can stall the host while the GPU drains, i.e. idle time
+    # inside a timed pair
+    ev_pool = [torch.cuda.Event(enable_timing=True) for _ in range(4 * len(a.lambdas) * (a.steps + 1))]
+    for e in ev_pool:
+        e.record(stream)
+    torch.cuda.synchronize()
+    ev = ev_pool.pop  # noqa: E731
     rec = []  # (step, lam, op, ev0, ev1, outcomes)
     clocks = Clocks(0)
 
     host_s = [0.0]
 
-    def one_step(s, timed):
-        for lam, t in tables.items():
+    def one_op(lam, s, timed):
+        """find + insert_or_assign of step s on the lambda table, then restore."""
+        t = tables[lam]
+        if timed:
             e0, e1, e2, e3 = ev(), ev(), ev(), ev()
-            h0 = time.perf_counter()
-            e0.record(stream)
-            t.find(queries[lam])
-            e1.record(stream)
-            e2.record(stream)
-            o = t.insert_or_assign(ins_keys[s], vals)
-            e3.record(stream)
-            h1 = time.perf_counter()
-            t.restore()
-            if os.environ.get("BENCH_DEBUG"):
-                print(f"host step {s} lam {lam}: {1e3*(h1-h0):.3f} ms", file=sys.stderr)
-            if timed:
-                host_s[0] += h1 - h0
-                rec.append((s, lam, e0, e1, e2, e3, o))
+        else:
+            e0 = e1 = e2 = e3 = torch.cuda.Event()
+        # keep the launch queue shallow, then hold the stream ~0.2 ms so
+        # both ops are fully enqueued before e0 runs: the event pairs then
+        # time device work only, never host issue or queue back-pressure
+        torch.cuda.synchronize()
+        torch.cuda._sleep(SPIN_CYCLES)
+        h0 = time.perf_counter()
+        e0.record(stream)
+        t.find(queries[lam], out=find_out)
+        e1.record(stream)
+        e2.record(stream)
+        o = t.insert_or_assign(ins_keys[s], vals)
+        e3.record(stream)
+        h1 = time.perf_counter()
+        t.restore()
+        if os.environ.get("BENCH_DEBUG"):
+            print(f"host step {s} lam {lam}: {1e3*(h1-h0):.3f} ms", file=sys.stderr)
+        if timed:
+            host_s[0] += h1 - h0
+            rec.append((s, lam, e0, e1, e2, e3, o))
 
     # the sampler starts before the warm-up (nvidia-smi start-up must not land in the timed region)
     clocks.start()
     clocks.wait_first_sample()
-    for s in range(a.warmup):
-        one_step(s, False)
-    torch.cuda.synchronize()
-    lib.hkv_set_kernel_timing(1)
-    launches0 = lib.hkv_launch_count()
-    torch.cuda.synchronize()
-    torch.cuda.nvtx.range_push("timed")
-    w0 = time.perf_counter()
-    for s in range(a.warmup, n_steps):
-        one_step(s, True)
-    torch.cuda.synchronize()
-    w1 = time.perf_counter()
-    torch.cuda.nvtx.range_pop()
+    # lambda-major order: each table's warm-up and timed steps run back to
+    # back (switching between three 34 GB tables between ops measures TLB
+    # refill, not the table); only the timed steps are recorded
+    prof = None
+    if os.environ.get("BENCH_PROFILE"):
+        import cProfile
+
+        prof = cProfile.Profile()
+    wall = 0.0
+    launches = 0
+    for li, lam in enumerate(a.lambdas):
+        for s in range(a.warmup):
+            one_op(lam, s, False)
+        torch.cuda.synchronize()
+        lib.hkv_set_kernel_timing(1)
+        launches0 = lib.hkv_launch_count()
+        torch.cuda.nvtx.range_push("timed")
+        if prof is not None:
+            prof.enable()
+        w0 = time.perf_counter()
+        for s in range(a.warmup, n_steps):
+            one_op(lam, s, True)
+        torch.cuda.synchronize()
+        wall += time.perf_counter() - w0
+        if prof is not None:
+            prof.disable()
+        torch.cuda.nvtx.range_pop()
+        lib.hkv_set_kernel_timing(0)
+        launches += lib.hkv_launch_count() - launches0
+    if prof is not None:
+        import pstats
+
+        pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime").print_stats(15)
     clk = clocks.stop()
-    launches = lib.hkv_launch_count() - launches0
     lib.hkv_set_kernel_timing(0)
 
     import ctypes as C
@@ -446,13 +508,15 @@ def run_single(a):
                    "capacity": cap, "dim": dim, "batch": B, "lambdas": a.lambdas,
                    "l2": "inputs larger than L2 (34 GB table per lambda, 256 MB batch values); metadata restore "
                          "between batches (outside the timed region)",
-                   "timing": "CUDA events around each op on its stream; sum over ops"},
+                   "timing": "CUDA events around each op on its stream (ops fully enqueued behind a 0.2 ms spin before "
+                             "the first event, so host issue is never inside a timed pair); value = keys / sum of op "
+                             "times"},
         "breakdown": breakdown,
         "find_bkvs_mean": round(statistics.mean(find_rates), 4),
         "insert_or_assign_bkvs_mean": round(statistics.mean(ins_rates), 4),
         "find_variation_over_lambda": round((max(find_rates) - min(find_rates)) / max(find_rates), 4),
         "insert_variation_over_lambda": round((max(ins_rates) - min(ins_rates)) / max(ins_rates), 4),
-        "wall_ms_per_step_incl_restore": round((w1 - w0) * 1e3 / a.steps, 3),
+        "wall_ms_per_step_incl_restore": round(wall * 1e3 / a.steps, 3),
         "host_issue_us_per_op": round(host_s[0] * 1e6 / (a.steps * len(a.lambdas) * 2), 1),
         "fill_s": round(fill_s, 1),
         "clocks": clk, "gpu_launches": int(launches), "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu_base,

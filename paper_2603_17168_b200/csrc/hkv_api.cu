@@ -26,6 +26,20 @@ struct KTimer {
   };
   std::map<cudaStream_t, std::vector<Pending>> open;  // begun, awaiting end
   std::vector<Pending> done;
+  // Events are created up front (hkv_set_kernel_timing) and recycled: creating
+  // an event inside a timed region can block the host while the GPU drains its
+  // queue, which shows up as idle time inside the caller's own event pairs.
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t take() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
 };
 KTimer& ktimer() {
   static KTimer k;
@@ -39,8 +53,8 @@ void ktimer_begin(const char* name, cudaStream_t s) {
   if (!k.enabled) return;
   KTimer::Pending p;
   p.name = name;
-  cudaEventCreate(&p.a);
-  cudaEventCreate(&p.b);
+  p.a = k.take();
+  p.b = k.take();
   cudaEventRecord(p.a, s);
   k.open[s].push_back(p);
 }
@@ -162,6 +176,11 @@ int hkv_set_kernel_timing(int32_t enable) {
   KTimer& k = ktimer();
   std::lock_guard<std::mutex> g(k.mu);
   k.enabled = enable != 0;
+  while (k.enabled && k.pool.size() < 8192) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) break;
+    k.pool.push_back(e);
+  }
   return HKV_OK;
 }
 
@@ -183,8 +202,8 @@ int hkv_kernel_times(const char* name, double* ms, int64_t* launches) {
     cudaEventElapsedTime(&f, p.a, p.b);
     tot += f;
     cnt++;
-    cudaEventDestroy(p.a);
-    cudaEventDestroy(p.b);
+    k.pool.push_back(p.a);
+    k.pool.push_back(p.b);
   }
   k.done.swap(keep);
   *ms = tot;

@@ -35,6 +35,7 @@ struct Workspace {
   uint32_t* aux = nullptr;   // assign: rows / evicted list
   uint32_t* aux2 = nullptr;  // assign: found ranks
   uint64_t* skey = nullptr;  // single mode: bucket-segment records (3 u64 per item)
+  uint64_t* skeys = nullptr; // single mode: keys in sorted (bucket, batch index) order
   uint32_t* vrow = nullptr;  // single mode: destination row of final value writers
   uint32_t* rrow = nullptr;  // single mode: row of a value read
   int32_t* rsrc = nullptr;   // single mode: provenance of a value read (-1 = pre-batch row)

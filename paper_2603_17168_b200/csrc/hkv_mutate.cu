@@ -264,7 +264,8 @@ __global__ void __launch_bounds__(1024) k_segments(const uint32_t* __restrict__ 
                                                    const uint64_t* __restrict__ keys, int64_t n,
                                                    SegRec* __restrict__ recs, int64_t cap, Scalars* sc,
                                                    uint32_t* __restrict__ brk, uint8_t* __restrict__ outcomes,
-                                                   uint32_t* __restrict__ vrow, uint8_t fcode) {
+                                                   uint32_t* __restrict__ vrow, uint8_t fcode,
+                                                   uint64_t* __restrict__ skeys) {
   __shared__ unsigned wcount[2][32];
   __shared__ unsigned block_base[2];
   if (sc->err) return;
@@ -290,6 +291,7 @@ __global__ void __launch_bounds__(1024) k_segments(const uint32_t* __restrict__ 
   if (p < n) {
     const bool same_next = multi && k_next == k;
     brk[p] = same_next ? 0xFFFFFFFFu : (uint32_t)p;
+    if (in_multi) skeys[p] = k;
     if (prev_same_b && k_prev == k) {
       outcomes[i] = fcode;
       vrow[i] = kNoRow;
@@ -346,12 +348,25 @@ struct LastWriter {  // per-tile shared-memory view
   }
 };
 
+// Byte j (0..15) of a lane's 16-B digest slice.
+__device__ __forceinline__ void set_digest_byte(uint4& w, int j, uint32_t d) {
+  const uint32_t sh = (uint32_t)(j & 3) * 8u;
+  const uint32_t m = ~(0xFFu << sh);
+  const uint32_t v = (d & 0xFFu) << sh;
+  switch (j >> 2) {
+    case 0: w.x = (w.x & m) | v; break;
+    case 1: w.y = (w.y & m) | v; break;
+    case 2: w.z = (w.z & m) | v; break;
+    default: w.w = (w.w & m) | v; break;
+  }
+}
+
 // One op of every active tile of the warp (must be called by all 32 lanes).
 // dw/occ: this lane's digest / occupancy slice of bucket b, already loaded.
 // Returns (tile-uniform) the slot holding `key` after the op, -1 if absent.
 template <int OP, bool COLLECT>
 __device__ __forceinline__ int meta_op_ws(const TableDev& t, const OpArgs& a, unsigned lane, bool active,
-                                           uint32_t i, uint64_t key, uint32_t d, uint64_t b, uint4 dw, uint32_t occ,
+                                           uint32_t i, uint64_t key, uint32_t d, uint64_t b, uint4& dw, uint32_t& occ,
                                            uint64_t clock0, bool fel_open, bool spec, LastWriter& lw,
                                            uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
                                            int32_t* __restrict__ rsrc, ctr_t* ctr, int& size_delta) {
@@ -402,7 +417,8 @@ __device__ __forceinline__ int meta_op_ws(const TableDev& t, const OpArgs& a, un
     if (active && slot >= 0) {
       if (slot / kSPL == r) {
         t.keys[rowbase + slot] = kEmptyKey;
-        store_occ(t, b, r, occ & ~(1u << (slot % kSPL)));
+        occ &= ~(1u << (slot % kSPL));
+        store_occ(t, b, r, occ);
       }
       if (r == 0) size_delta--;
     }
@@ -447,7 +463,9 @@ __device__ __forceinline__ int meta_op_ws(const TableDev& t, const OpArgs& a, un
     t.keys[rowbase + sl] = key;
     t.digests[rowbase + sl] = (uint8_t)d;
     t.scores[rowbase + sl] = s_in;
-    store_occ(t, b, r, occ | (1u << j));
+    occ |= 1u << j;
+    store_occ(t, b, r, occ);
+    set_digest_byte(dw, j, d);
   }
   sl = __shfl_sync(kFull, sl, (int)tb + fl);
   if (free_ins) {
@@ -476,6 +494,7 @@ __device__ __forceinline__ int meta_op_ws(const TableDev& t, const OpArgs& a, un
           t.keys[row] = key;
           t.digests[row] = (uint8_t)d;
           t.scores[row] = s_in;
+          set_digest_byte(dw, lm % kSPL, d);
         }
         wslot = lm;
         if constexpr (COLLECT) rslot = lm;
@@ -605,7 +624,8 @@ __device__ __forceinline__ void load_slices(const TableDev& t, bool active, uint
 template <int OP, bool COLLECT>
 __device__ __forceinline__ void meta_pass(const TableDev& t, const OpArgs& a, const uint32_t* __restrict__ sb,
                                           const uint32_t* __restrict__ sidx, const uint32_t* __restrict__ run_end,
-                                          const SegRec* __restrict__ recs, int64_t nrec, int64_t dir, int64_t n,
+                                          const uint64_t* __restrict__ skeys, const SegRec* __restrict__ recs,
+                                          int64_t nrec, int64_t dir, int64_t n,
                                           uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
                                           int32_t* __restrict__ rsrc, LastWriter& lw, uint64_t clock0, bool fel_open,
                                           bool spec, ctr_t* ctr, int& sd) {
@@ -646,34 +666,47 @@ __device__ __forceinline__ void meta_pass(const TableDev& t, const OpArgs& a, co
     lw.cur++;
     __syncwarp();
     while (true) {
+      // the next sorted position's inputs do not depend on this op: in flight while it runs
+      uint32_t nb_ = kNoRow, ni = 0;
+      uint64_t nk = 0;
+      int64_t qe = q;
+      if (active && multi && q + 1 < n) {
+        nb_ = sb[q + 1];
+        ni = sidx[q + 1];
+        nk = skeys[q + 1];
+        qe = (int64_t)run_end[q];
+      }
       const int res = meta_op_ws<OP, COLLECT>(t, a, lane, active, i, key, d, b, dw, occ, clock0, fel_open, spec, lw,
                                               vrow, rrow, rsrc, ctr, sd);
-      // next op of the segment; a same-key run after it collapses (apply_run)
+      // a same-key run after this op collapses (apply_run)
       int64_t run_to = -1;
       if (active) {
-        if (multi && q + 1 < n && sb[q + 1] == (uint32_t)b) {
-          const int64_t qe = (int64_t)run_end[q];
+        if (nb_ == (uint32_t)b) {
           if (qe > q && (OP == kOpErase || res >= 0 || lfu_like)) run_to = qe;
         } else {
           active = false;
         }
       }
-      // full-warp fence (every lane reaches it), then re-read after this tile's own writes
       if (!__any_sync(kFull, active)) break;
-      __syncwarp();
+      __syncwarp();  // LastWriter (shared memory) written by one lane, read by the tile
       if (active) {
-        load_slices(t, true, b, r, dw, occ);
+        // dw / occ already reflect this tile's own writes (meta_op_ws keeps them in sync)
         if (run_to >= 0) {
           apply_run<OP>(t, a, r, q, run_to, res, b, d, dw, occ, clock0, sidx, lw, vrow, rrow, rsrc, ctr);
-          q = run_to;  // a run changes one score only: digest / occupancy slices stay valid
-          if (!(q + 1 < n && sb[q + 1] == (uint32_t)b)) active = false;
-        }
-        if (active) {
+          q = run_to;  // a run changes one score only
+          if (q + 1 < n && sb[q + 1] == (uint32_t)b) {
+            ++q;
+            i = sidx[q];
+            key = skeys[q];
+          } else {
+            active = false;
+          }
+        } else {
           ++q;
-          i = sidx[q];
-          key = a.keys[i];
-          d = digest_of(fmix64(key));
+          i = ni;
+          key = nk;
         }
+        if (active) d = digest_of(fmix64(key));
       }
       if (!__any_sync(kFull, active)) break;
     }
@@ -688,6 +721,7 @@ template <int OP, bool COLLECT>
 __global__ void __launch_bounds__(256, 3) k_meta_single(TableDev t, OpArgs a, const uint32_t* __restrict__ sb,
                                                         const uint32_t* __restrict__ sidx,
                                                         const uint32_t* __restrict__ run_end,
+                                                        const uint64_t* __restrict__ skeys,
                                                         const SegRec* __restrict__ recs, int64_t cap, int64_t n,
                                                         uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
                                                         int32_t* __restrict__ rsrc) {
@@ -708,9 +742,9 @@ __global__ void __launch_bounds__(256, 3) k_meta_single(TableDev t, OpArgs a, co
   const bool spec = sz * 100ull > t.capacity * 97ull;
   ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
   int sd = 0;
-  meta_pass<OP, COLLECT>(t, a, sb, sidx, run_end, recs, (int64_t)a.sc->nseg, 1, n, vrow, rrow, rsrc, lw, clock0,
+  meta_pass<OP, COLLECT>(t, a, sb, sidx, run_end, skeys, recs, (int64_t)a.sc->nseg, 1, n, vrow, rrow, rsrc, lw, clock0,
                          fel_open, spec, ctr, sd);
-  meta_pass<OP, COLLECT>(t, a, sb, sidx, run_end, recs + (cap - 1), (int64_t)a.sc->nmulti, -1, n, vrow, rrow, rsrc,
+  meta_pass<OP, COLLECT>(t, a, sb, sidx, run_end, skeys, recs + (cap - 1), (int64_t)a.sc->nmulti, -1, n, vrow, rrow, rsrc,
                          lw, clock0, fel_open, spec, ctr, sd);
   block_ctrs_flush(bc, t.counters, t.size, ctr, sd);
 }
@@ -1026,7 +1060,7 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual
     const int64_t c = n + n / 4 + 1024;
     if ((e = grow(ws.bkt, c)) || (e = grow(ws.idx, c)) || (e = grow(ws.sbkt, c)) || (e = grow(ws.sidx, c)) ||
         (e = grow(ws.seg, c)) || (e = grow(ws.aux, c)) || (e = grow(ws.aux2, c)) || (e = grow(ws.skey, 3 * c)) ||
-        (e = grow(ws.vrow, c)) || (e = grow(ws.rrow, c)) || (e = grow(ws.rsrc, c)))
+        (e = grow(ws.vrow, c)) || (e = grow(ws.rrow, c)) || (e = grow(ws.rsrc, c)) || (e = grow(ws.skeys, c)))
       return e;
     if (ws.b2) { cudaFree(ws.b2); ws.b2 = nullptr; }
     if (ws.pend) { cudaFree(ws.pend); ws.pend = nullptr; }
@@ -1076,7 +1110,8 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual
 }
 
 void ws_free(Workspace& ws) {
-  void* ptrs[] = {ws.bkt, ws.idx, ws.sbkt, ws.sidx, ws.seg, ws.aux, ws.aux2, ws.skey, ws.vrow, ws.rrow, ws.rsrc,
+  void* ptrs[] = {ws.bkt, ws.idx, ws.sbkt, ws.sidx, ws.seg, ws.aux, ws.aux2, ws.skey, ws.skeys, ws.vrow, ws.rrow,
+                  ws.rsrc,
                   ws.b2, ws.pend,
                   ws.ek, ws.es, ws.ev, ws.cub_tmp, ws.sc};
   for (void* p : ptrs)
@@ -1142,7 +1177,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       SegRec* recs = reinterpret_cast<SegRec*>(ws.skey);
       const uint8_t fcode = a.op == kOpErase ? kNotFound : a.op == kOpFindOrInsert ? kFound : kUpdated;
       k_segments<<<(unsigned)((n + 1023) / 1024), 1024, 0, s>>>(ws.sbkt, ws.sidx, a.keys, n, recs, n, ws.sc, ws.aux2,
-                                                                 a.outcomes, ws.vrow, fcode);
+                                                                 a.outcomes, ws.vrow, fcode, ws.skeys);
       g_launches++;
       if ((e = run_ends(ws, n, s))) return e;
       int64_t blocks = (((n + kG - 1) / kG) * kG + 255) / 256;
@@ -1151,7 +1186,8 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       auto* fn = a.op == kOpErase ? k_meta_single<kOpErase, false>
                  : a.op == kOpFindOrInsert ? k_meta_single<kOpFindOrInsert, false>
                  : a.collect ? k_meta_single<kOpUpsert, true> : k_meta_single<kOpUpsert, false>;
-      fn<<<(unsigned)blocks, 256, 0, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, recs, n, n, ws.vrow, ws.rrow, ws.rsrc);
+      fn<<<(unsigned)blocks, 256, 0, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, recs, n, n, ws.vrow, ws.rrow,
+                                          ws.rsrc);
       ktimer_end("apply", s);
       g_launches++;
     } else {

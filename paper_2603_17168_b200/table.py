@@ -20,6 +20,9 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
+import sys
+import time
 from dataclasses import dataclass
 from typing import Callable, Optional
 
@@ -35,6 +38,7 @@ BUCKET_SLOTS = 128
 EMPTY_KEY = 0xFFFFFFFFFFFFFFFF
 LOCKED_KEY = 0xFFFFFFFFFFFFFFFE
 _LOCKED = np.uint64(LOCKED_KEY)
+_TRACE = bool(os.environ.get("HKV_TRACE"))
 
 
 class Mode(enum.Enum):  # table.py:63-65
@@ -254,10 +258,19 @@ class CacheTable:
                 raise ValueError("out must be float32 with shape (len(keys), value_dim)")
             host_out = out
             out_d = torch.from_numpy(np.ascontiguousarray(out)).to(self.device)
+        _t0 = time.perf_counter() if _TRACE else 0.0
         found = torch.empty(n, dtype=torch.bool, device=self.device)
+        _t1 = time.perf_counter() if _TRACE else 0.0
         st = self._stream()
         with self.gate.acquire(Role.Reader, st):
+            _t2 = time.perf_counter() if _TRACE else 0.0
             _lib.check(self._lib.hkv_find(self._h, _ptr(k), n, _ptr(out_d), _ptr(found), zero_misses, self._sp()))
+            _t3 = time.perf_counter() if _TRACE else 0.0
+        if _TRACE:
+            _t4 = time.perf_counter()
+            if _t4 - _t0 > 5e-4:
+                print(f"[trace find] empty {1e3*(_t1-_t0):.3f} acquire {1e3*(_t2-_t1):.3f} hkv_find "
+                      f"{1e3*(_t3-_t2):.3f} release {1e3*(_t4-_t3):.3f} ms", file=sys.stderr)
         if not np_mode or np_mode == "host":
             self._check_device_error()
             if isinstance(out, torch.Tensor) and out_d is not out:

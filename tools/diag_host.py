@@ -34,6 +34,12 @@ torch.cuda.synchronize()
 st = torch.cuda.current_stream()
 if "--ktimer" in sys.argv:
     hkv._lib.load().hkv_set_kernel_timing(1)
+if "--smi" in sys.argv:
+    import bench
+
+    _clk = bench.Clocks(0)
+    _clk.start()
+    _clk.wait_first_sample()
 
 
 def it(i, log):
@@ -56,6 +62,8 @@ def it(i, log):
 
 
 for i in range(5):
+    it(i, True)
+for i in range(20):
     it(i, True)
 pr = cProfile.Profile()
 pr.enable()
