@@ -113,6 +113,8 @@ struct hkv_table {
   uint8_t* digests = nullptr;
   uint64_t* scores = nullptr;
   uint32_t* bits = nullptr;
+  uint64_t* smin = nullptr;     // [B][8] per-16-slot-group score minima (eviction summary)
+  uint32_t* svalid = nullptr;   // [B] bit g: smin[b][g] is exact
   float* vfast = nullptr;
   float* vover = nullptr;       // device pointer of the overflow arena
   float* vover_host = nullptr;  // pinned host allocation (mapped), if used
@@ -123,6 +125,8 @@ struct hkv_table {
   uint8_t* snap_digests = nullptr;
   uint64_t* snap_scores = nullptr;
   uint32_t* snap_bits = nullptr;
+  uint64_t* snap_smin = nullptr;
+  uint32_t* snap_svalid = nullptr;
   TableScalars* snap_sc = nullptr;
   std::mutex mu;
   std::map<cudaStream_t, Workspace> ws;
@@ -154,8 +158,9 @@ struct DeviceGuard {
 void free_table(hkv_table* t) {
   if (!t) return;
   DeviceGuard g(t->cfg.device);
-  void* dptrs[] = {t->keys, t->digests, t->scores, t->bits, t->vfast, t->sc, t->lead,
-                   t->snap_keys, t->snap_digests, t->snap_scores, t->snap_bits, t->snap_sc};
+  void* dptrs[] = {t->keys, t->digests, t->scores, t->bits, t->smin, t->svalid, t->vfast, t->sc, t->lead,
+                   t->snap_keys, t->snap_digests, t->snap_scores, t->snap_bits, t->snap_smin, t->snap_svalid,
+                   t->snap_sc};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   if (t->vover_host) cudaFreeHost(t->vover_host);
@@ -241,6 +246,7 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
   cudaError_t e;
   if ((e = cudaMalloc((void**)&t->keys, cap * 8)) || (e = cudaMalloc((void**)&t->digests, cap)) ||
       (e = cudaMalloc((void**)&t->scores, cap * 8)) || (e = cudaMalloc((void**)&t->bits, (size_t)bc * 16)) ||
+      (e = cudaMalloc((void**)&t->smin, (size_t)bc * 64)) || (e = cudaMalloc((void**)&t->svalid, (size_t)bc * 4)) ||
       (e = cudaMalloc((void**)&t->sc, sizeof(TableScalars)))) {
     free_table(t);
     return fail(HKV_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e));
@@ -269,6 +275,7 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
   // initial state, table.py:143-149 / store.py:36-37
   if ((e = cudaMemset(t->keys, 0xFF, cap * 8)) || (e = cudaMemset(t->digests, 0, cap)) ||
       (e = cudaMemset(t->scores, 0, cap * 8)) || (e = cudaMemset(t->bits, 0, (size_t)bc * 16)) ||
+      (e = cudaMemset(t->smin, 0, (size_t)bc * 64)) || (e = cudaMemset(t->svalid, 0, (size_t)bc * 4)) ||
       (e = cudaMemset(t->sc, 0, sizeof(TableScalars))) ||
       (t->vfast && (e = cudaMemset(t->vfast, 0, t->fast_rows * dim * 4))) ||
       (t->vover && (e = cudaMemset(t->vover, 0, over_rows * dim * 4))) ||
@@ -285,6 +292,8 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
   d.digests = t->digests;
   d.scores = t->scores;
   d.bits = t->bits;
+  d.smin = t->smin;
+  d.svalid = t->svalid;
   d.vfast = t->vfast;
   d.vover = t->vover;
   d.fast_rows = t->fast_rows;
@@ -534,6 +543,7 @@ int hkv_import_state(hkv_table* t, const uint64_t* keys, const uint8_t* digests,
       (e = cudaMemcpy(t->vover, values + t->fast_rows * dim, (cap - t->fast_rows) * dim * 4, cudaMemcpyDefault)))
     return cuda_fail(e, "import overflow values");
   if ((e = run_bits_from_keys(t->dev, t->buckets, 0))) return cuda_fail(e, "import bits");
+  if ((e = cudaMemset(t->svalid, 0, (size_t)t->buckets * 4))) return cuda_fail(e, "import summary");
   TableScalars h;
   if ((e = cudaMemcpy(&h, t->sc, sizeof(h), cudaMemcpyDeviceToHost))) return cuda_fail(e, "import scalars");
   h.clock = clock;
@@ -585,6 +595,8 @@ int hkv_snapshot(hkv_table* t, hkv_stream stream) {
     if ((e = cudaMalloc((void**)&t->snap_keys, cap * 8)) || (e = cudaMalloc((void**)&t->snap_digests, cap)) ||
         (e = cudaMalloc((void**)&t->snap_scores, cap * 8)) ||
         (e = cudaMalloc((void**)&t->snap_bits, (size_t)t->buckets * 16)) ||
+        (e = cudaMalloc((void**)&t->snap_smin, (size_t)t->buckets * 64)) ||
+        (e = cudaMalloc((void**)&t->snap_svalid, (size_t)t->buckets * 4)) ||
         (e = cudaMalloc((void**)&t->snap_sc, sizeof(TableScalars))))
       return fail(HKV_ENOMEM, std::string("snapshot allocation failed: ") + cudaGetErrorString(e));
   }
@@ -593,6 +605,8 @@ int hkv_snapshot(hkv_table* t, hkv_stream stream) {
       (e = cudaMemcpyAsync(t->snap_digests, t->digests, cap, cudaMemcpyDeviceToDevice, s)) ||
       (e = cudaMemcpyAsync(t->snap_scores, t->scores, cap * 8, cudaMemcpyDeviceToDevice, s)) ||
       (e = cudaMemcpyAsync(t->snap_bits, t->bits, (size_t)t->buckets * 16, cudaMemcpyDeviceToDevice, s)) ||
+      (e = cudaMemcpyAsync(t->snap_smin, t->smin, (size_t)t->buckets * 64, cudaMemcpyDeviceToDevice, s)) ||
+      (e = cudaMemcpyAsync(t->snap_svalid, t->svalid, (size_t)t->buckets * 4, cudaMemcpyDeviceToDevice, s)) ||
       (e = cudaMemcpyAsync(t->snap_sc, t->sc, sizeof(TableScalars), cudaMemcpyDeviceToDevice, s)))
     return cuda_fail(e, "snapshot");
   return HKV_OK;
@@ -609,6 +623,8 @@ int hkv_restore(hkv_table* t, hkv_stream stream) {
       (e = cudaMemcpyAsync(t->digests, t->snap_digests, cap, cudaMemcpyDeviceToDevice, s)) ||
       (e = cudaMemcpyAsync(t->scores, t->snap_scores, cap * 8, cudaMemcpyDeviceToDevice, s)) ||
       (e = cudaMemcpyAsync(t->bits, t->snap_bits, (size_t)t->buckets * 16, cudaMemcpyDeviceToDevice, s)) ||
+      (e = cudaMemcpyAsync(t->smin, t->snap_smin, (size_t)t->buckets * 64, cudaMemcpyDeviceToDevice, s)) ||
+      (e = cudaMemcpyAsync(t->svalid, t->snap_svalid, (size_t)t->buckets * 4, cudaMemcpyDeviceToDevice, s)) ||
       (e = cudaMemcpyAsync(t->sc, t->snap_sc, sizeof(TableScalars), cudaMemcpyDeviceToDevice, s)))
     return cuda_fail(e, "restore");
   return HKV_OK;

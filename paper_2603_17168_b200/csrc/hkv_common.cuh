@@ -9,6 +9,9 @@
 //                         counter + argmax(keys==EMPTY) scan (table.py:1171)
 //   keys    [B][128] u64  8 lines per bucket
 //   scores  [B][128] u64  8 lines per bucket (read only on full-bucket decisions)
+//   smin    [B][8]   u64  eviction summary: min score of each 16-slot group, so
+//   svalid  [B]      u32  a full-bucket argmin reads 64 B + one group's 128 B
+//                         instead of the 1-KB score row (bit g: group g exact)
 //   values  rows [capacity][dim] f32: rows < fast_rows in HBM, the rest in the
 //           overflow arena (mapped pinned host memory, or HBM)
 #pragma once
@@ -39,6 +42,8 @@ struct TableDev {
   uint8_t* digests;
   uint64_t* scores;
   uint32_t* bits;
+  uint64_t* smin;     // [B][8] min score of each 16-slot group (exact where svalid says so)
+  uint32_t* svalid;   // [B] bit g set <=> smin[b][g] == min(scores[b][16g .. 16g+15])
   float* vfast;       // rows [0, fast_rows)
   float* vover;       // rows [fast_rows, capacity), indexed row - fast_rows
   uint64_t fast_rows;

@@ -25,6 +25,8 @@
 // bucket, tile-wide argmin over the score row, admission test and eviction
 // (_finish_admission, table.py:1121-1163).
 #include <cub/cub.cuh>
+#include <cstdlib>
+#include <string>
 #include <thrust/iterator/reverse_iterator.h>
 
 #include "hkv_kernels.h"
@@ -88,6 +90,7 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
     if (slot / kSPL == r) {
       const uint64_t old = hit_needs_old(t.policy) ? t.scores[row] : 0;
       t.scores[row] = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
+      summ_invalidate(t, hb, slot);
     }
     float* vr = value_row(t, row);
     if (a.op == kOpFindOrInsert) {
@@ -149,6 +152,7 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
       t.keys[row] = key;
       t.digests[row] = (uint8_t)d;
       t.scores[row] = s_in;
+      summ_invalidate(t, tb, s);
       store_occ(t, tb, r, occ | (1u << j));
     }
     s = tile.shfl(s, fl);
@@ -175,6 +179,7 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
       t.keys[row] = key;
       t.digests[row] = (uint8_t)d;
       t.scores[row] = s_in;
+      summ_invalidate(t, tb, m);
     }
     copy_row<kG, VEC>(vr, vin, dim, r);
     ctr[row < t.fast_rows ? kVFast : kVOver]++;
@@ -440,6 +445,7 @@ __device__ __forceinline__ int meta_op_ws(const TableDev& t, const OpArgs& a, un
     const uint64_t row = rowbase + slot;
     const uint64_t old = hit_needs_old(t.policy) ? t.scores[row] : 0;
     t.scores[row] = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
+    summ_invalidate(t, b, slot);
   }
   if (is_hit) {
     if constexpr (OP == kOpFindOrInsert) {
@@ -463,6 +469,7 @@ __device__ __forceinline__ int meta_op_ws(const TableDev& t, const OpArgs& a, un
     t.keys[rowbase + sl] = key;
     t.digests[rowbase + sl] = (uint8_t)d;
     t.scores[rowbase + sl] = s_in;
+    summ_invalidate(t, b, sl);
     occ |= 1u << j;
     store_occ(t, b, r, occ);
     set_digest_byte(dw, j, d);
@@ -494,6 +501,7 @@ __device__ __forceinline__ int meta_op_ws(const TableDev& t, const OpArgs& a, un
           t.keys[row] = key;
           t.digests[row] = (uint8_t)d;
           t.scores[row] = s_in;
+          summ_invalidate(t, b, lm);
           set_digest_byte(dw, lm % kSPL, d);
         }
         wslot = lm;
@@ -589,6 +597,7 @@ __device__ __forceinline__ void apply_run(const TableDev& t, const OpArgs& a, in
     const uint64_t tl = a.ticks ? a.ticks[il] : clock0 + (uint64_t)il + 1;
     const uint64_t cs = a.scores ? a.scores[il] : 0;
     t.scores[row] = run_hit_score(t.policy, t.scores[row], a.epoch, tl, a.scores != nullptr, cs, cnt);
+    summ_invalidate(t, b, res);
     if constexpr (OP == kOpUpsert) {
       const int prev = lw.get(res);
       if (prev >= 0) vrow[prev] = kNoRow;
@@ -746,6 +755,493 @@ __global__ void __launch_bounds__(256, 3) k_meta_single(TableDev t, OpArgs a, co
                          fel_open, spec, ctr, sd);
   meta_pass<OP, COLLECT>(t, a, sb, sidx, run_end, skeys, recs + (cap - 1), (int64_t)a.sc->nmulti, -1, n, vrow, rrow, rsrc,
                          lw, clock0, fel_open, spec, ctr, sd);
+  block_ctrs_flush(bc, t.counters, t.size, ctr, sd);
+}
+
+// ---------------------------------------------------------------------------
+// Single mode, metadata pass, one THREAD per bucket segment (the default).
+//
+// A thread owns its segment's bucket for the whole batch, keeps the bucket's
+// digest line (128 B) and occupancy bitmap (16 B) in registers, updates them
+// in place after its own writes, and applies the segment's ops in batch order
+// (same per-op restatement of _round_upsert as meta_op_ws, table.py:1025-1163).
+// Full-bucket decisions use the per-group eviction summary (smin / svalid):
+// argmin over 8 group minima (64 B), then the chosen group's 16 scores
+// (128 B) to find the slot — np.argmin's first-index tie rule holds because
+// groups are in slot order and the first equal slot inside the group is
+// taken.  Invalid groups are rescanned (and become valid) on the way.
+// Compared with a tile per segment this has 8x the segments in flight and no
+// cross-lane collectives, which is what the metadata pass is bound by
+// (dependent random loads, profiles/r01).
+// ---------------------------------------------------------------------------
+struct TpsState {
+  uint4* L;          // digest line (shared memory, 8 x 16 B)
+  uint32_t* O;       // occupancy bitmap words (shared memory, slots 32w .. 32w+31)
+  uint32_t wm[4];    // slots already written by an earlier op of this segment
+  uint64_t sm[8];    // group minima (register copy, valid where sv says so)
+  uint32_t sv;       // summary valid bits (register copy)
+  uint32_t smdirty;  // sm entries to write back
+  bool sloaded;      // sm / sv loaded
+  bool svdirty;
+};
+
+// Register-array helpers written as masked arithmetic over every element:
+// an `if (k == idx)` chain gets folded back into a computed index by the
+// compiler, which demotes the whole bucket state to local memory.
+__device__ __forceinline__ uint32_t eqmask(int a, int b) { return 0u - (uint32_t)(a == b); }
+__device__ __forceinline__ uint32_t sel4(const uint32_t (&a)[4], int w) {
+  return (a[0] & eqmask(w, 0)) | (a[1] & eqmask(w, 1)) | (a[2] & eqmask(w, 2)) | (a[3] & eqmask(w, 3));
+}
+__device__ __forceinline__ bool bit128(const uint32_t (&m)[4], int s) { return (sel4(m, s >> 5) >> (s & 31)) & 1u; }
+__device__ __forceinline__ void setbit128(uint32_t (&m)[4], int s) {
+  const uint32_t bit = 1u << (s & 31);
+#pragma unroll
+  for (int w = 0; w < 4; w++) m[w] |= bit & eqmask(w, s >> 5);
+}
+__device__ __forceinline__ void clrbit128(uint32_t (&m)[4], int s) {
+  const uint32_t bit = 1u << (s & 31);
+#pragma unroll
+  for (int w = 0; w < 4; w++) m[w] &= ~(bit & eqmask(w, s >> 5));
+}
+__device__ __forceinline__ void set_line_byte(uint4 (&dg)[8], int s, uint32_t d) {
+  const int j = s & 15;
+  const uint32_t sh = (uint32_t)(j & 3) * 8u;
+  const uint32_t bm = 0xFFu << sh, bv = (d & 0xFFu) << sh;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const uint32_t on = eqmask(k, s >> 4);
+    const uint32_t mx = bm & on & eqmask(j >> 2, 0), my = bm & on & eqmask(j >> 2, 1);
+    const uint32_t mz = bm & on & eqmask(j >> 2, 2), mw = bm & on & eqmask(j >> 2, 3);
+    dg[k].x = (dg[k].x & ~mx) | (bv & mx);
+    dg[k].y = (dg[k].y & ~my) | (bv & my);
+    dg[k].z = (dg[k].z & ~mz) | (bv & mz);
+    dg[k].w = (dg[k].w & ~mw) | (bv & mw);
+  }
+}
+__device__ __forceinline__ uint64_t eqmask64(int a, int b) { return 0ull - (uint64_t)(a == b); }
+__device__ __forceinline__ uint64_t sel8(const uint64_t (&a)[8], int g) {
+  uint64_t v = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) v |= a[k] & eqmask64(k, g);
+  return v;
+}
+__device__ __forceinline__ void put8(uint64_t (&a)[8], int g, uint64_t v) {
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const uint64_t m = eqmask64(k, g);
+    a[k] = (a[k] & ~m) | (v & m);
+  }
+}
+
+// candidates of digest d: digest-equal and occupied (table.py:243-247)
+__device__ __forceinline__ void tps_cand(const TableDev& t, const TpsState& S, uint32_t d, uint32_t (&c)[4]) {
+#pragma unroll
+  for (int w = 0; w < 4; w++) {
+    const uint32_t m = t.digest_filter ? (match16(S.L[2 * w], d) | (match16(S.L[2 * w + 1], d) << 16)) : ~0u;
+    c[w] = m & S.O[w];
+  }
+}
+
+// the 16 scores of group g: min and first slot holding it
+__device__ __forceinline__ void tps_group_scan(const TableDev& t, uint64_t rowbase, int g, uint64_t (&v)[16],
+                                               uint64_t& mn, int& ms) {
+  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(t.scores + rowbase + 16 * g);
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const ulonglong2 x = p[k];
+    v[2 * k] = x.x;
+    v[2 * k + 1] = x.y;
+  }
+  mn = v[0];
+  ms = 0;
+#pragma unroll
+  for (int k = 1; k < 16; k++)
+    if (v[k] < mn) { mn = v[k]; ms = k; }
+}
+
+__device__ __forceinline__ void tps_load_summary(const TableDev& t, uint64_t b, TpsState& S) {
+  if (S.sloaded) return;
+  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(t.smin + b * 8);
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const ulonglong2 x = p[k];
+    S.sm[2 * k] = x.x;
+    S.sm[2 * k + 1] = x.y;
+  }
+  S.sv = t.svalid[b];
+  S.sloaded = true;
+}
+
+// a score write of value v at slot s outside an eviction: keep the group
+// minimum exact when v becomes the minimum, otherwise mark it unknown
+__device__ __forceinline__ void tps_score_written(const TableDev& t, uint64_t b, TpsState& S, int s, uint64_t v) {
+  const int g = s >> 4;
+  if (S.sloaded) {
+    if (((S.sv >> g) & 1u) && v <= sel8(S.sm, g)) {
+      put8(S.sm, g, v);
+      S.smdirty |= 1u << g;
+    } else if ((S.sv >> g) & 1u) {
+      S.sv &= ~(1u << g);
+      S.svdirty = true;
+    }
+  } else {
+    atomicAnd(t.svalid + b, ~(1u << g));
+  }
+}
+
+// The op of this segment that last wrote `row` at or before sorted position
+// `from` (the segment starts at p0).  Only called when the slot's bit in
+// S.wm says some earlier op of the segment wrote it, which is rare: retired
+// writers hold kNoRow, so the latest writer is the one whose vrow == row.
+__device__ __forceinline__ int tps_last_writer(const uint32_t* __restrict__ sidx, const uint32_t* vrow, uint32_t row,
+                                               int64_t p0, int64_t from) {
+  for (int64_t p = from; p >= p0; p--) {
+    const uint32_t j = sidx[p];
+    if (vrow[j] == row) return (int)j;
+  }
+  return -1;
+}
+
+template <int OP, bool COLLECT>
+__device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsState& S, uint64_t b, uint32_t i,
+                                      uint64_t key, uint32_t d, uint64_t clock0, bool fel_open, int64_t p0,
+                                      int64_t q, const uint32_t* __restrict__ sidx,
+                                      uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
+                                      int32_t* __restrict__ rsrc, ctr_t* ctr, int& sd, uint32_t& fe_min) {
+  const uint64_t rowbase = b * kSlots;
+  uint32_t c[4];
+  tps_cand(t, S, d, c);
+  int hit = -1;
+  unsigned ncmp = 0;
+#pragma unroll
+  for (int w = 0; w < 4; w++) {
+    uint32_t m = hit < 0 ? c[w] : 0u;
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      ncmp++;
+      if (t.keys[rowbase + 32 * w + j] == key) {
+        hit = 32 * w + j;
+        m = 0;
+      }
+    }
+  }
+  ctr[kLoads]++;
+  ctr[kCompares] += ncmp;
+  if constexpr (OP == kOpErase) {  // _round_erase, table.py:1017-1023
+    if (hit >= 0) {
+      t.keys[rowbase + hit] = kEmptyKey;
+      const uint32_t o = S.O[hit >> 5] & ~(1u << (hit & 31));
+      S.O[hit >> 5] = o;
+      t.bits[b * 4 + (hit >> 5)] = o;
+      sd--;
+    }
+    a.outcomes[i] = hit >= 0 ? kErased : kNotFound;
+    return -1;
+  }
+  const uint64_t tick = a.ticks ? a.ticks[i] : clock0 + (uint64_t)i + 1;
+  const uint64_t cs = a.scores ? a.scores[i] : 0;
+  uint8_t outcome = kRejected;
+  int wslot = -1, rslot = -1;
+  if (hit >= 0) {  // table.py:1045-1062
+    const uint64_t row = rowbase + hit;
+    const uint64_t old = hit_needs_old(t.policy) ? t.scores[row] : 0;
+    const uint64_t ns = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
+    t.scores[row] = ns;
+    tps_score_written(t, b, S, hit, ns);
+    if constexpr (OP == kOpFindOrInsert) {
+      outcome = kFound;
+      rslot = hit;
+    } else {
+      outcome = kUpdated;
+      wslot = hit;
+    }
+  } else {
+    const uint64_t s_in = insert_score(t.policy, a.epoch, tick, cs);  // scoring.py:105-127
+    const uint4 ow = *reinterpret_cast<const uint4*>(S.O);
+    const uint32_t oc[4] = {ow.x, ow.y, ow.z, ow.w};
+    const int occ_total = __popc(oc[0]) + __popc(oc[1]) + __popc(oc[2]) + __popc(oc[3]);
+    if (occ_total < kSlots) {
+      // _bulk_insert_free, table.py:1165-1181: lowest EMPTY slot
+      int s = 0;
+#pragma unroll
+      for (int w = 3; w >= 0; w--)
+        if (oc[w] != 0xFFFFFFFFu) s = 32 * w + __ffs(~oc[w]) - 1;
+      const uint64_t row = rowbase + s;
+      t.keys[row] = key;
+      t.digests[row] = (uint8_t)d;
+      t.scores[row] = s_in;
+      const uint32_t o = S.O[s >> 5] | (1u << (s & 31));
+      S.O[s >> 5] = o;
+      t.bits[b * 4 + (s >> 5)] = o;
+      reinterpret_cast<uint8_t*>(S.L)[s] = (uint8_t)d;
+      tps_score_written(t, b, S, s, s_in);
+      wslot = s;
+      outcome = kInserted;
+      sd++;
+    } else {
+      // full bucket: argmin (table.py:1079-1083) through the group summary
+      ctr[kScans]++;
+      tps_load_summary(t, b, S);
+      uint64_t v[16];
+      uint64_t mn;
+      int ms;
+      uint32_t inv = ~S.sv & 0xFFu;
+      while (inv) {
+        const int g = __ffs(inv) - 1;
+        inv &= inv - 1;
+        tps_group_scan(t, rowbase, g, v, mn, ms);
+        put8(S.sm, g, mn);
+        S.smdirty |= 1u << g;
+      }
+      if (S.sv != 0xFFu) {
+        S.sv = 0xFFu;
+        S.svdirty = true;
+      }
+      int gi = 0;
+      uint64_t gmin = S.sm[0];
+#pragma unroll
+      for (int k = 1; k < 8; k++)
+        if (S.sm[k] < gmin) { gmin = S.sm[k]; gi = k; }
+      tps_group_scan(t, rowbase, gi, v, mn, ms);  // mn == gmin; ms = first slot holding it
+      if (s_in >= gmin) {  // the single-bucket path admits ties (table.py:1083)
+        const int m = 16 * gi + ms;
+        const uint64_t row = rowbase + m;
+        if constexpr (COLLECT) {
+          a.ek[i] = t.keys[row];
+          a.es[i] = gmin;
+        }
+        t.keys[row] = key;
+        t.digests[row] = (uint8_t)d;
+        t.scores[row] = s_in;
+        reinterpret_cast<uint8_t*>(S.L)[m] = (uint8_t)d;
+        // the group's new minimum, exactly (its 16 scores are in registers)
+        uint64_t nm = kMaxScore;
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+          const uint64_t x = (k == ms) ? s_in : v[k];
+          nm = x < nm ? x : nm;
+        }
+        put8(S.sm, gi, nm);
+        S.smdirty |= 1u << gi;
+        wslot = m;
+        if constexpr (COLLECT) rslot = m;
+        outcome = kEvicted;
+        if (fel_open) fe_min = i < fe_min ? i : fe_min;
+      }
+    }
+  }
+  // value plan (provenance read BEFORE this op's own write is recorded)
+  if (rslot >= 0) {
+    ctr[rowbase + rslot < t.fast_rows ? kVFast : kVOver]++;
+    rrow[i] = (uint32_t)(rowbase + rslot);
+    rsrc[i] = bit128(S.wm, rslot) ? tps_last_writer(sidx, vrow, (uint32_t)(rowbase + rslot), p0, q - 1) : -1;
+  }
+  if (wslot >= 0) {
+    ctr[rowbase + wslot < t.fast_rows ? kVFast : kVOver]++;
+    if (bit128(S.wm, wslot)) {  // retired: this op rewrites the slot
+      const int prev = tps_last_writer(sidx, vrow, (uint32_t)(rowbase + wslot), p0, q - 1);
+      if (prev >= 0) vrow[prev] = kNoRow;
+    }
+    setbit128(S.wm, wslot);
+    vrow[i] = (uint32_t)(rowbase + wslot);
+  } else {
+    vrow[i] = kNoRow;
+  }
+  a.outcomes[i] = outcome;
+  return rslot >= 0 ? rslot : wslot;
+}
+
+// same-key run q+1 .. qe after the op at q (see apply_run): thread version
+template <int OP>
+__device__ __forceinline__ void tps_run(const TableDev& t, const OpArgs& a, TpsState& S, int64_t q, int64_t qe,
+                                        int res, uint64_t b, uint32_t d, uint64_t clock0,
+                                        const uint32_t* __restrict__ sidx, int64_t p0, uint32_t* __restrict__ vrow,
+                                        uint32_t* __restrict__ rrow, int32_t* __restrict__ rsrc, ctr_t* ctr) {
+  const uint32_t cnt = (uint32_t)(qe - q);
+  const uint64_t rowbase = b * kSlots;
+  uint32_t c[4];
+  tps_cand(t, S, d, c);
+  if (res >= 0) {  // compares stop at the match (table.py:243-268)
+#pragma unroll
+    for (int w = 0; w < 4; w++) {
+      if (32 * w > res) c[w] = 0;
+      else if (32 * w + 31 > res) c[w] &= (2u << (res & 31)) - 1u;
+    }
+  }
+  ctr[kCompares] += cnt * (uint32_t)(__popc(c[0]) + __popc(c[1]) + __popc(c[2]) + __popc(c[3]));
+  ctr[kLoads] += cnt;
+  if constexpr (OP == kOpErase) return;
+  if (res < 0) {  // rejected run (Lfu / EpochLfu: same score, same bucket)
+    ctr[kScans] += cnt;
+    for (int64_t p = q + 1; p <= qe; p++) a.outcomes[sidx[p]] = kRejected;
+    return;
+  }
+  const uint64_t row = rowbase + res;
+  ctr[row < t.fast_rows ? kVFast : kVOver] += cnt;
+  const uint32_t il = sidx[qe];
+  const uint64_t tl = a.ticks ? a.ticks[il] : clock0 + (uint64_t)il + 1;
+  const uint64_t cs = a.scores ? a.scores[il] : 0;
+  const uint64_t ns = run_hit_score(t.policy, t.scores[row], a.epoch, tl, a.scores != nullptr, cs, cnt);
+  t.scores[row] = ns;
+  tps_score_written(t, b, S, res, ns);
+  if constexpr (OP == kOpUpsert) {
+    if (bit128(S.wm, res)) {
+      const int prev = tps_last_writer(sidx, vrow, (uint32_t)row, p0, q);
+      if (prev >= 0) vrow[prev] = kNoRow;
+    }
+    setbit128(S.wm, res);
+    vrow[il] = (uint32_t)row;
+  }
+  if constexpr (OP == kOpFindOrInsert) {
+    const int src = bit128(S.wm, res) ? tps_last_writer(sidx, vrow, (uint32_t)row, p0, q) : -1;
+    for (int64_t p = q + 1; p <= qe; p++) {
+      const uint32_t j = sidx[p];
+      rrow[j] = (uint32_t)row;
+      rsrc[j] = src;
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int kTpsThreads = 256;
+constexpr int kTpsStageU4 = 9;  // per thread and stage: 8 x 16 B digest line + 16 B occupancy (odd stride: no bank conflicts)
+
+// stage buffer of this thread: [stage][thread][9 x uint4]
+__device__ __forceinline__ uint4* tps_buf(uint4* smem, int stage) {
+  return smem + ((size_t)stage * kTpsThreads + threadIdx.x) * kTpsStageU4;
+}
+__device__ __forceinline__ void tps_fetch(const TableDev& t, uint4* buf, uint64_t b) {
+  const uint4* dp = reinterpret_cast<const uint4*>(t.digests + b * kSlots);
+#pragma unroll
+  for (int k = 0; k < 8; k++) cp_async16(buf + k, dp + k);
+  cp_async16(buf + 8, reinterpret_cast<const uint4*>(t.bits) + b);
+}
+
+template <int OP, bool COLLECT>
+__device__ __forceinline__ void tps_segment(const TableDev& t, const OpArgs& a, const SegRec& rec, uint4* buf,
+                                            const uint32_t* __restrict__ sb, const uint32_t* __restrict__ sidx,
+                                            const uint32_t* __restrict__ run_end, const uint64_t* __restrict__ skeys,
+                                            int64_t n, uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
+                                            int32_t* __restrict__ rsrc, uint64_t clock0, bool fel_open,
+                                            bool spec, bool lfu_like, ctr_t* ctr, int& sd, uint32_t& fe_min) {
+  const uint64_t b = rec.b;
+  TpsState S;
+  S.L = buf;
+  S.O = reinterpret_cast<uint32_t*>(buf + 8);
+#pragma unroll
+  for (int w = 0; w < 4; w++) S.wm[w] = 0;
+  S.sloaded = false;
+  S.svdirty = false;
+  S.smdirty = 0;
+  if (OP != kOpErase && spec) tps_load_summary(t, b, S);
+  const bool multi = (rec.flags & 1u) != 0;
+  uint32_t i = rec.i, d = rec.flags >> 8;
+  uint64_t key = rec.key;
+  int64_t q = rec.p;
+  while (true) {
+    uint32_t nb_ = kNoRow, ni = 0;
+    uint64_t nk = 0;
+    int64_t qe = q;
+    if (multi && q + 1 < n) {  // next sorted position: independent of this op, in flight during it
+      nb_ = sb[q + 1];
+      ni = sidx[q + 1];
+      nk = skeys[q + 1];
+      qe = (int64_t)run_end[q];
+    }
+    const int res = tps_op<OP, COLLECT>(t, a, S, b, i, key, d, clock0, fel_open, rec.p, q, sidx, vrow, rrow, rsrc,
+                                        ctr, sd, fe_min);
+    if (nb_ != (uint32_t)b) break;
+    if (qe > q && (OP == kOpErase || res >= 0 || lfu_like)) {
+      tps_run<OP>(t, a, S, q, qe, res, b, d, clock0, sidx, rec.p, vrow, rrow, rsrc, ctr);
+      q = qe;
+      if (!(q + 1 < n && sb[q + 1] == (uint32_t)b)) break;
+      ++q;
+      i = sidx[q];
+      key = skeys[q];
+    } else {
+      ++q;
+      i = ni;
+      key = nk;
+    }
+    d = digest_of(fmix64(key));
+  }
+  // write back the summary changes kept in registers
+  if (S.smdirty) {
+#pragma unroll
+    for (int k = 0; k < 8; k++)
+      if ((S.smdirty >> k) & 1u) t.smin[b * 8 + k] = S.sm[k];
+  }
+  if (S.svdirty || S.smdirty) t.svalid[b] = S.sv;
+}
+
+// Two-stage cp.async pipeline per thread: while segment k is processed, the
+// digest line + occupancy of segment k+1 are in flight into shared memory
+// and the record of segment k+2 into registers.
+template <int OP, bool COLLECT>
+__global__ void __launch_bounds__(kTpsThreads, 2) k_meta_tps(TableDev t, OpArgs a, const uint32_t* __restrict__ sb,
+                                                            const uint32_t* __restrict__ sidx,
+                                                            const uint32_t* __restrict__ run_end,
+                                                            const uint64_t* __restrict__ skeys,
+                                                            const SegRec* __restrict__ recs, int64_t cap, int64_t n,
+                                                            uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
+                                                            int32_t* __restrict__ rsrc) {
+  extern __shared__ uint4 tps_smem[];
+  __shared__ BlockCtrs bc;
+  if (a.sc->err) return;
+  block_ctrs_init(bc);
+  const uint64_t clock0 = *t.clock;
+  const bool fel_open = !*t.fel_set;
+  // at lambda > 0.97 a full bucket is the rule: fetch the summary with the first op
+  const bool spec = *t.size * 100ull > t.capacity * 97ull;
+  const bool lfu_like = t.policy == kLfu || t.policy == kEpochLfu;
+  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
+  int sd = 0;
+  uint32_t fe_min = 0xFFFFFFFFu;
+  const int64_t nseg = (int64_t)a.sc->nseg;
+  const int64_t nall = nseg + (int64_t)a.sc->nmulti;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  auto rec_at = [&](int64_t j) -> SegRec {
+    if (j >= nall) return SegRec{0, 0, 0, 0, 0};
+    return j < nseg ? recs[j] : recs[cap - 1 - (j - nseg)];
+  };
+  uint4* b0 = tps_buf(tps_smem, 0);
+  uint4* b1 = tps_buf(tps_smem, 1);
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  SegRec ra = rec_at(j), rb = rec_at(j + stride);
+  if (j < nall) tps_fetch(t, b0, ra.b);
+  cp_async_commit();
+  if (j + stride < nall) tps_fetch(t, b1, rb.b);
+  cp_async_commit();
+  for (; j < nall; j += 2 * stride) {
+    SegRec rn = rec_at(j + 2 * stride);
+    cp_async_wait<1>();
+    tps_segment<OP, COLLECT>(t, a, ra, b0, sb, sidx, run_end, skeys, n, vrow, rrow, rsrc, clock0, fel_open,
+                             spec, lfu_like, ctr, sd, fe_min);
+    ra = rn;
+    if (j + 2 * stride < nall) tps_fetch(t, b0, ra.b);
+    cp_async_commit();
+    if (j + stride >= nall) break;
+    rn = rec_at(j + 3 * stride);
+    cp_async_wait<1>();
+    tps_segment<OP, COLLECT>(t, a, rb, b1, sb, sidx, run_end, skeys, n, vrow, rrow, rsrc, clock0, fel_open,
+                             spec, lfu_like, ctr, sd, fe_min);
+    rb = rn;
+    if (j + 3 * stride < nall) tps_fetch(t, b1, rb.b);
+    cp_async_commit();
+  }
+  cp_async_wait<0>();
+  if (fel_open) {
+    unsigned m = __reduce_min_sync(kFull, fe_min);
+    if ((threadIdx.x & 31) == 0 && m != 0xFFFFFFFFu) atomicMin(&a.sc->first_ev, m);
+  }
   block_ctrs_flush(bc, t.counters, t.size, ctr, sd);
 }
 
@@ -1012,9 +1508,11 @@ __global__ void __launch_bounds__(256) k_assign_apply(TableDev t, const float* _
         if (r == 0) {
           if (scores) {
             t.scores[row] = scores[i];
+            summ_invalidate(t, row / kSlots, (int)(row % kSlots));
           } else if (refresh) {
             const uint64_t tick = ticks ? ticks[i] : clock0 + (uint64_t)ranks[i] + 1;
             t.scores[row] = hit_score(t.policy, t.scores[row], epoch, tick, false, 0);
+            summ_invalidate(t, row / kSlots, (int)(row % kSlots));
           }
         }
       }
@@ -1183,11 +1681,31 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       int64_t blocks = (((n + kG - 1) / kG) * kG + 255) / 256;
       if (blocks > (int64_t)num_sms * 3) blocks = (int64_t)num_sms * 3;  // one resident wave (3 blocks/SM)
       ktimer_begin("apply", s);
-      auto* fn = a.op == kOpErase ? k_meta_single<kOpErase, false>
-                 : a.op == kOpFindOrInsert ? k_meta_single<kOpFindOrInsert, false>
-                 : a.collect ? k_meta_single<kOpUpsert, true> : k_meta_single<kOpUpsert, false>;
-      fn<<<(unsigned)blocks, 256, 0, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, recs, n, n, ws.vrow, ws.rrow,
-                                          ws.rsrc);
+      static const bool tile_meta = getenv("HKV_META") && std::string(getenv("HKV_META")) == "tile";
+      if (tile_meta) {
+        auto* fn = a.op == kOpErase ? k_meta_single<kOpErase, false>
+                   : a.op == kOpFindOrInsert ? k_meta_single<kOpFindOrInsert, false>
+                   : a.collect ? k_meta_single<kOpUpsert, true> : k_meta_single<kOpUpsert, false>;
+        fn<<<(unsigned)blocks, 256, 0, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, recs, n, n, ws.vrow, ws.rrow,
+                                            ws.rsrc);
+      } else {
+        auto* fn = a.op == kOpErase ? k_meta_tps<kOpErase, false>
+                   : a.op == kOpFindOrInsert ? k_meta_tps<kOpFindOrInsert, false>
+                   : a.collect ? k_meta_tps<kOpUpsert, true> : k_meta_tps<kOpUpsert, false>;
+        const size_t smem = 2 * kTpsThreads * kTpsStageU4 * sizeof(uint4);
+        static bool attr_set = false;
+        if (!attr_set) {
+          for (auto* f : {k_meta_tps<kOpErase, false>, k_meta_tps<kOpFindOrInsert, false>, k_meta_tps<kOpUpsert, true>,
+                          k_meta_tps<kOpUpsert, false>})
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          attr_set = true;
+        }
+        int64_t tb = (n + kTpsThreads - 1) / kTpsThreads;
+        const int64_t tcap = (int64_t)num_sms * 2;  // one resident wave
+        if (tb > tcap) tb = tcap;
+        fn<<<(unsigned)(tb < 1 ? 1 : tb), kTpsThreads, smem, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, recs, n, n,
+                                                                 ws.vrow, ws.rrow, ws.rsrc);
+      }
       ktimer_end("apply", s);
       g_launches++;
     } else {

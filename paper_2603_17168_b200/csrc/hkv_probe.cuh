@@ -97,6 +97,12 @@ __device__ __forceinline__ void store_occ(const TableDev& t, uint64_t b, int r, 
   reinterpret_cast<uint16_t*>(t.bits + b * 4)[r] = (uint16_t)v;
 }
 
+// Any score write at `slot` of bucket b outside the summary-maintaining
+// single-mode pass: the group's minimum is no longer known exactly.
+__device__ __forceinline__ void summ_invalidate(const TableDev& t, uint64_t b, int slot) {
+  atomicAnd(t.svalid + b, ~(1u << (slot >> 4)));
+}
+
 template <int G>
 __device__ __forceinline__ int tile_sum(const Tile8& tile, int v) {
   return (int)tile.sum((unsigned)v);  // REDUX over the tile's 8 lanes
