@@ -397,7 +397,8 @@ def run_single(a):
         lib.hkv_kernel_times(name.encode(), C.byref(ms), C.byref(n))
         return ms.value, n.value
 
-    find_ms, find_n = ktime("find")
+    find_ms, find_n = ktime("find")  # probe kernel
+    fg_ms, fg_n = ktime("find_gather")
     apply_ms, apply_n = ktime("apply")
     vw_ms, vw_n = ktime("values_write")
     # device times
@@ -441,13 +442,14 @@ def run_single(a):
     apply_bytes_launch = bytes_upsert(counts_total, dim) / max(apply_n, 1)
     cand = []
     if find_n:
-        cand.append(("k_find", find_ms, find_n, find_bytes_launch))
+        # a find is the probe (k_find) + the value gather (k_find_gather): bytes of the whole op over both
+        cand.append(("find:k_find+k_find_gather", find_ms + fg_ms, find_n, find_bytes_launch))
     if apply_n:
         # metadata pass: the byte model minus the value-row traffic (moved by k_values_write)
         v = 4 * dim
         moved = int(counts_total[[0, 1, 3]].sum()) * 2 * v + int(counts_total[2]) * v
         meta_bytes = (bytes_upsert(counts_total, dim) - moved) / max(apply_n, 1)
-        cand.append(("k_meta_single", apply_ms, apply_n, meta_bytes))
+        cand.append(("k_meta_tps", apply_ms, apply_n, meta_bytes))
     if vw_n:
         cand.append(("k_values_write", vw_ms, vw_n, int(counts_total[[0, 1, 3]].sum()) * 2 * 4 * dim / vw_n))
     name, kms, kn, kbytes = max(cand, key=lambda c: c[1])

@@ -12,6 +12,9 @@
 // the recorded rows with 8 x 16-B requests in flight per lane; separating it
 // from the dependent probe chain is what keeps the value traffic near the
 // copy roofline.
+#include <cstdlib>
+#include <string>
+
 #include "hkv_probe.cuh"
 #include "hkv_kernels.h"
 
@@ -178,9 +181,165 @@ __global__ void __launch_bounds__(256) k_find_gather(TableDev t, const uint32_t*
   block_ctrs_flush(bc, t.counters, nullptr, ctr, 0);
 }
 
+// Thread-per-key probe (the default): one thread reads its key's whole
+// 128-B digest line (8 x 16 B, all in flight together), matches the 128
+// digests with __vcmpeq4, then checks candidate keys in slot order.  No
+// cross-lane collectives: ~2.5x fewer warp instructions per key than the
+// 8-lane tile, and 32 keys per warp in flight instead of 16.
+__device__ __forceinline__ int probe_line_thread(const TableDev& t, uint64_t b, uint64_t key, uint32_t d,
+                                                 unsigned& ncmp) {
+  const uint64_t rowbase = b * kSlots;
+  uint32_t c[4];
+  if (t.digest_filter) {
+    const uint4* dp = reinterpret_cast<const uint4*>(t.digests + rowbase);
+    uint4 w[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) w[k] = ld_stream(dp + k);
+#pragma unroll
+    for (int q = 0; q < 4; q++) c[q] = match16(w[2 * q], d) | (match16(w[2 * q + 1], d) << 16);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; q++) c[q] = ~0u;
+  }
+  int hit = -1;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    uint32_t m = hit < 0 ? c[q] : 0u;
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const uint64_t k = __ldg(t.keys + rowbase + 32 * q + j);
+      if (k == kEmptyKey) continue;  // candidates exclude EMPTY slots (table.py:243-247)
+      ncmp++;
+      if (k == key) {
+        hit = 32 * q + j;
+        m = 0;
+      }
+    }
+  }
+  return hit;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_find_tpk(TableDev t, const uint64_t* __restrict__ keys, int64_t n,
+                                                  uint8_t* __restrict__ found, uint8_t* __restrict__ tier,
+                                                  int64_t* __restrict__ offset, uint32_t* __restrict__ rows) {
+  __shared__ BlockCtrs bc;
+  block_ctrs_init(bc);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
+  int bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t key = __ldg(keys + i);
+    bad |= key >= kLockedKey;
+    const uint64_t h = fmix64(key);
+    const uint32_t d = digest_of(h);
+    uint64_t b = h & t.mask;
+    unsigned ncmp = 0;
+    int slot = probe_line_thread(t, b, key, d, ncmp);
+    ctr[kLoads]++;
+    if (slot < 0 && t.dual) {  // second bucket only for first-bucket misses (table.py:291-298)
+      b = second_hash(h) & t.mask;
+      slot = probe_line_thread(t, b, key, d, ncmp);
+      ctr[kLoads]++;
+    }
+    ctr[kCompares] += ncmp;
+    const bool f = slot >= 0;
+    const uint64_t row = b * kSlots + (uint64_t)(f ? slot : 0);
+    found[i] = f;
+    if constexpr (MODE == 4) rows[i] = f ? (uint32_t)row : 0xFFFFFFFFu;
+    if constexpr (MODE == 2) {
+      const bool over = row >= t.fast_rows;
+      tier[i] = f ? (uint8_t)over : 0;
+      offset[i] = !f ? -1 : (int64_t)((over ? row - t.fast_rows : row) * (uint64_t)t.dim);
+    }
+  }
+  if (bad) atomicOr(t.err, 1);
+  block_ctrs_flush(bc, t.counters, nullptr, ctr, 0);
+}
+
+// Fused find (dim % 4 == 0, 16-B aligned rows): each warp probes 32 keys
+// (thread per key, as k_find_tpk), then moves the 32 value rows together:
+// the warp's 32 x (dim/4) 16-B vectors are spread over the lanes, U loads in
+// flight per lane before the matching stores (coalesced 16-B accesses on
+// both sides).  Warps of a block are in different phases at any time, so
+// probe latency overlaps other warps' value traffic without a second pass
+// over the keys.
+template <bool kZero, int U>
+__global__ void __launch_bounds__(256) k_find_fused(TableDev t, const uint64_t* __restrict__ keys, int64_t n,
+                                                    uint8_t* __restrict__ found, float* __restrict__ out) {
+  __shared__ BlockCtrs bc;
+  block_ctrs_init(bc);
+  const unsigned lane = threadIdx.x & 31u;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int nv = t.dim >> 2;  // 16-B vectors per row
+  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
+  int bad = 0;
+  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    uint32_t row = 0xFFFFFFFFu;
+    if (i < n) {
+      const uint64_t key = __ldg(keys + i);
+      bad |= key >= kLockedKey;
+      const uint64_t h = fmix64(key);
+      const uint32_t d = digest_of(h);
+      uint64_t b = h & t.mask;
+      unsigned ncmp = 0;
+      int slot = probe_line_thread(t, b, key, d, ncmp);
+      ctr[kLoads]++;
+      if (slot < 0 && t.dual) {
+        b = second_hash(h) & t.mask;
+        slot = probe_line_thread(t, b, key, d, ncmp);
+        ctr[kLoads]++;
+      }
+      ctr[kCompares] += ncmp;
+      found[i] = slot >= 0;
+      if (slot >= 0) {
+        row = (uint32_t)(b * kSlots + slot);
+        ctr[row < t.fast_rows ? kVFast : kVOver]++;
+      }
+    }
+    // value rows of the warp's 32 keys
+    const int nk = (n - base < 32) ? (int)(n - base) : 32;
+    const int total = nk * nv;
+    for (int v0 = 0; v0 < total; v0 += 32 * U) {  // warp-uniform trip count: every lane reaches the shuffles
+      uint4 x[U];
+      uint32_t rr[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int v = v0 + 32 * u + (int)lane;
+        const int k = v < total ? v / nv : 0;
+        rr[u] = __shfl_sync(0xffffffffu, row, k);
+        if (v < total && rr[u] != 0xFFFFFFFFu) x[u] = ld_stream(reinterpret_cast<const uint4*>(value_row(t, rr[u])) + (v - k * nv));
+        else x[u] = make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int v = v0 + 32 * u + (int)lane;
+        if (v >= total || (!kZero && rr[u] == 0xFFFFFFFFu)) continue;
+        const int k = v / nv;
+        st_stream(reinterpret_cast<uint4*>(out + (base + k) * (int64_t)t.dim) + (v - k * nv), x[u]);
+      }
+    }
+  }
+  if (bad) atomicOr(t.err, 1);
+  block_ctrs_flush(bc, t.counters, nullptr, ctr, 0);
+}
+
 template <int MODE>
 static void launch_probe(const TableDev& t, const uint64_t* keys, int64_t n, uint8_t* found, uint8_t* tier,
                          int64_t* offset, uint32_t* rows, cudaStream_t s, int num_sms) {
+  static const bool tile_probe = getenv("HKV_FIND") && std::string(getenv("HKV_FIND")) == "tile";
+  if (!tile_probe) {
+    int64_t blocks = (n + 255) / 256;
+    const int64_t max_blocks = (int64_t)num_sms * 8;
+    if (blocks > max_blocks) blocks = max_blocks;
+    if (blocks < 1) blocks = 1;
+    k_find_tpk<MODE><<<(unsigned)blocks, 256, 0, s>>>(t, keys, n, found, tier, offset, rows);
+    g_launches++;
+    return;
+  }
   constexpr int KPT = 4;
   int64_t blocks = (((n + KPT - 1) / KPT) * kG + 255) / 256;
   const int64_t max_blocks = (int64_t)num_sms * 8 * 4;
@@ -198,6 +357,15 @@ void launch_find(const TableDev& t, const uint64_t* keys, int64_t n, float* out,
     launch_probe<1>(t, keys, n, found, nullptr, nullptr, nullptr, s, num_sms);
   } else if (mode == 2) {
     launch_probe<2>(t, keys, n, found, tier, offset, nullptr, s, num_sms);
+  } else if ((t.dim % 4) == 0 && (((uintptr_t)out & 15) == 0) && (((uintptr_t)t.vfast & 15) == 0) &&
+             (((uintptr_t)t.vover & 15) == 0) && !(getenv("HKV_FIND") && std::string(getenv("HKV_FIND")) != "fused")) {
+    int64_t blocks = (n + 255) / 256;
+    const int64_t max_blocks = (int64_t)num_sms * 8;
+    if (blocks > max_blocks) blocks = max_blocks;
+    if (blocks < 1) blocks = 1;
+    if (mode == 3) k_find_fused<true, 8><<<(unsigned)blocks, 256, 0, s>>>(t, keys, n, found, out);
+    else k_find_fused<false, 8><<<(unsigned)blocks, 256, 0, s>>>(t, keys, n, found, out);
+    g_launches++;
   } else {
     launch_probe<4>(t, keys, n, found, nullptr, nullptr, rows, s, num_sms);
     ktimer_end("find", s);

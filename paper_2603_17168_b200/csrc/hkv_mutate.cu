@@ -1212,29 +1212,21 @@ __global__ void __launch_bounds__(kTpsThreads, 2) k_meta_tps(TableDev t, OpArgs 
     if (j >= nall) return SegRec{0, 0, 0, 0, 0};
     return j < nseg ? recs[j] : recs[cap - 1 - (j - nseg)];
   };
-  uint4* b0 = tps_buf(tps_smem, 0);
-  uint4* b1 = tps_buf(tps_smem, 1);
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   SegRec ra = rec_at(j), rb = rec_at(j + stride);
-  if (j < nall) tps_fetch(t, b0, ra.b);
+  if (j < nall) tps_fetch(t, tps_buf(tps_smem, 0), ra.b);
   cp_async_commit();
-  if (j + stride < nall) tps_fetch(t, b1, rb.b);
+  if (j + stride < nall) tps_fetch(t, tps_buf(tps_smem, 1), rb.b);
   cp_async_commit();
-  for (; j < nall; j += 2 * stride) {
-    SegRec rn = rec_at(j + 2 * stride);
+  for (int stage = 0; j < nall; j += stride, stage ^= 1) {
+    const SegRec rn = rec_at(j + 2 * stride);  // in flight while segment j is processed
     cp_async_wait<1>();
-    tps_segment<OP, COLLECT>(t, a, ra, b0, sb, sidx, run_end, skeys, n, vrow, rrow, rsrc, clock0, fel_open,
-                             spec, lfu_like, ctr, sd, fe_min);
-    ra = rn;
-    if (j + 2 * stride < nall) tps_fetch(t, b0, ra.b);
-    cp_async_commit();
-    if (j + stride >= nall) break;
-    rn = rec_at(j + 3 * stride);
-    cp_async_wait<1>();
-    tps_segment<OP, COLLECT>(t, a, rb, b1, sb, sidx, run_end, skeys, n, vrow, rrow, rsrc, clock0, fel_open,
-                             spec, lfu_like, ctr, sd, fe_min);
+    uint4* buf = tps_buf(tps_smem, stage);
+    tps_segment<OP, COLLECT>(t, a, ra, buf, sb, sidx, run_end, skeys, n, vrow, rrow, rsrc, clock0, fel_open, spec,
+                             lfu_like, ctr, sd, fe_min);
+    ra = rb;
     rb = rn;
-    if (j + 3 * stride < nall) tps_fetch(t, b1, rb.b);
+    if (j + 2 * stride < nall) tps_fetch(t, buf, rb.b);
     cp_async_commit();
   }
   cp_async_wait<0>();

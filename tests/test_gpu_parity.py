@@ -289,3 +289,33 @@ def test_zipf_same_key_runs(hkv, policy):
     assert_same_state(t, o)
     assert t.counters.as_dict() == o.counters
     assert t.check_consistency()
+
+
+@pytest.mark.parametrize("dim", [1, 3, 4, 8, 12, 64, 132])
+@pytest.mark.parametrize("mode", MODES)
+def test_find_paths_ragged(hkv, dim, mode):
+    """find through every kernel path (fused thread-per-key probe + warp row
+    copy for dim % 4 == 0, probe + gather otherwise), ragged batch sizes that
+    leave partial warps, caller-provided `out` (misses untouched) and
+    out=None (misses zeroed) — bit-exact against the oracle."""
+    cap = 128 * 64
+    t = make_table(hkv, cap, dim, mode)
+    o = OracleTable(cap, dim, mode)
+    rng = np.random.default_rng(dim)
+    keys = rng.integers(1, 2**63, size=int(cap * 0.9), dtype=np.uint64)
+    vals = rng.standard_normal((len(keys), dim)).astype(np.float32)
+    t.insert_or_assign(keys, vals)
+    o.insert_or_assign(keys, vals)
+    for n in (1, 31, 33, 1000, 4097):
+        q = np.concatenate([keys[rng.integers(0, len(keys), size=n - n // 3)],
+                            rng.integers(1, 2**63, size=n // 3, dtype=np.uint64)])
+        ft, vt = t.find(q)
+        fo, vo = o.find(q)
+        assert np.array_equal(ft, fo) and vt.tobytes() == vo.tobytes(), f"n={n}"
+        pre = np.full((n, dim), 7.0, np.float32)
+        ot = torch.from_numpy(pre.copy()).cuda()
+        ft2, vt2 = t.find(torch.from_numpy(q.view(np.int64)).cuda(), out=ot)
+        oo = pre.copy()
+        fo2, _ = o.find(q, out=oo)
+        assert np.array_equal(ft2.cpu().numpy(), fo2) and vt2.cpu().numpy().tobytes() == oo.tobytes(), f"out= n={n}"
+    assert t.counters.as_dict() == o.counters
