@@ -135,6 +135,17 @@ __device__ __forceinline__ uint32_t match16(uint4 w, uint32_t d) {
   return match4(w.x, dd) | (match4(w.y, dd) << 4) | (match4(w.z, dd) << 8) | (match4(w.w, dd) << 12);
 }
 
+// Does any of the 16 digest bytes equal d?  (x - 0x01..) & ~x & 0x80.. is
+// non-zero iff x has a zero byte (the per-byte bits may over-report above a
+// zero byte, the word-level answer is exact): 3 ALU ops per word against ~8
+// for the exact mask, so the common no-candidate case (78 % of fresh keys at
+// lambda 0.5) skips the mask entirely.
+__device__ __forceinline__ uint32_t any16(uint4 w, uint32_t dd) {
+  const uint32_t a = w.x ^ dd, b = w.y ^ dd, c = w.z ^ dd, e = w.w ^ dd;
+  return ((a - 0x01010101u) & ~a) | ((b - 0x01010101u) & ~b) | ((c - 0x01010101u) & ~c) |
+         ((e - 0x01010101u) & ~e);
+}
+
 // Streaming loads/stores for data touched once.
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 r;

@@ -195,6 +195,11 @@ __device__ __forceinline__ int probe_line_thread(const TableDev& t, uint64_t b, 
     uint4 w[8];
 #pragma unroll
     for (int k = 0; k < 8; k++) w[k] = ld_stream(dp + k);
+    const uint32_t dd = d * 0x01010101u;
+    uint32_t any = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) any |= any16(w[k], dd);
+    if ((any & 0x80808080u) == 0) return -1;  // no digest match: a miss without touching keys
 #pragma unroll
     for (int q = 0; q < 4; q++) c[q] = match16(w[2 * q], d) | (match16(w[2 * q + 1], d) << 16);
   } else {

@@ -835,10 +835,24 @@ __device__ __forceinline__ void put8(uint64_t (&a)[8], int g, uint64_t v) {
 
 // candidates of digest d: digest-equal and occupied (table.py:243-247)
 __device__ __forceinline__ void tps_cand(const TableDev& t, const TpsState& S, uint32_t d, uint32_t (&c)[4]) {
+  if (t.digest_filter) {
+    uint4 w[8];
 #pragma unroll
-  for (int w = 0; w < 4; w++) {
-    const uint32_t m = t.digest_filter ? (match16(S.L[2 * w], d) | (match16(S.L[2 * w + 1], d) << 16)) : ~0u;
-    c[w] = m & S.O[w];
+    for (int k = 0; k < 8; k++) w[k] = S.L[k];
+    const uint32_t dd = d * 0x01010101u;
+    uint32_t any = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) any |= any16(w[k], dd);
+    if ((any & 0x80808080u) == 0) {
+#pragma unroll
+      for (int q = 0; q < 4; q++) c[q] = 0;
+      return;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) c[q] = (match16(w[2 * q], d) | (match16(w[2 * q + 1], d) << 16)) & S.O[q];
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; q++) c[q] = S.O[q];
   }
 }
 
