@@ -20,6 +20,11 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompil
          "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
 
 
+# per-file extra flags: the dual-mode dataflow hands buckets between SMs
+# through acquire/release turn counters, so its global loads bypass L1
+EXTRA = {"hkv_dual.cu": ["-Xptxas", "-dlcm=cg"]}
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -44,7 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *EXTRA.get(os.path.basename(src), []), "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

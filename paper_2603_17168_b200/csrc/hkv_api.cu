@@ -108,6 +108,7 @@ struct hkv_table {
   int num_sms = 148;
   uint64_t fast_rows = 0;
   uint64_t epoch = 0;
+  unsigned long long dual_epoch = 0;  // dual-mode turn-counter tag (hkv_dual.cu)
   TableDev dev{};
   uint64_t* keys = nullptr;
   uint8_t* digests = nullptr;
@@ -388,7 +389,7 @@ int hkv_upsert(hkv_table* t, int32_t op, const uint64_t* keys, float* values, co
   a.op = op == HKV_OP_FIND_OR_INSERT ? kOpFindOrInsert : kOpUpsert;
   a.collect = collect;
   a.epoch = t->epoch;
-  cudaError_t e = run_mutation(t->dev, a, n, t->log2b, t->workspace(s), &t->sc->round, t->lead, n_evicted_dev,
+  cudaError_t e = run_mutation(t->dev, a, n, t->log2b, t->workspace(s), (++t->dual_epoch) << 32, t->lead, n_evicted_dev,
                                evicted_keys, evicted_values, evicted_scores, ticks ? clock_advance : (uint64_t)n,
                                s, t->num_sms);
   return e ? cuda_fail(e, "hkv_upsert") : HKV_OK;
@@ -404,7 +405,7 @@ int hkv_erase(hkv_table* t, const uint64_t* keys, int64_t n, uint8_t* outcomes, 
   a.op = kOpErase;
   a.epoch = t->epoch;
   a.values = nullptr;
-  cudaError_t e = run_mutation(t->dev, a, n, t->log2b, t->workspace(s), &t->sc->round, t->lead, nullptr, nullptr,
+  cudaError_t e = run_mutation(t->dev, a, n, t->log2b, t->workspace(s), (++t->dual_epoch) << 32, t->lead, nullptr, nullptr,
                                nullptr, nullptr, 0, s, t->num_sms);
   return e ? cuda_fail(e, "hkv_erase") : HKV_OK;
 }

@@ -44,6 +44,15 @@ struct Workspace {
   uint64_t* ek = nullptr;
   uint64_t* es = nullptr;
   float* ev = nullptr;
+  // dual mode: 2n (bucket, op) pairs and per-op ranks (hkv_dual.cu)
+  int64_t dcap = 0;
+  uint32_t* dpk = nullptr;
+  uint32_t* dpv = nullptr;
+  uint32_t* dsk = nullptr;
+  uint32_t* dsv = nullptr;
+  uint32_t* drank = nullptr;
+  void* dcub = nullptr;
+  size_t dcub_bytes = 0;
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
   int64_t cub_for_n = -1;
@@ -74,7 +83,7 @@ void launch_find(const TableDev& t, const uint64_t* keys, int64_t n, float* out,
 
 // Returns cudaSuccess or the first error.
 cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, Workspace& ws,
-                         unsigned long long* round_ctr, unsigned long long* lead, int64_t* n_evicted,
+                         unsigned long long dual_tag, unsigned long long* lead, int64_t* n_evicted,
                          uint64_t* ek_out, float* ev_out, uint64_t* es_out, uint64_t clock_advance,
                          cudaStream_t s, int num_sms);
 
@@ -97,6 +106,10 @@ void ktimer_begin(const char* name, cudaStream_t s);
 void ktimer_end(const char* name, cudaStream_t s);
 
 cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual);
+cudaError_t ws_reserve_dual(Workspace& ws, int64_t n, int log2_buckets);
+void ws_free_dual(Workspace& ws);
+cudaError_t run_dual(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, Workspace& ws,
+                     unsigned long long* turn, unsigned long long tag, int vec, cudaStream_t s, int num_sms);
 void ws_free(Workspace& ws);
 
 }  // namespace hkv

@@ -35,174 +35,6 @@
 namespace hkv {
 
 // ---------------------------------------------------------------------------
-// per-op processor (one 8-lane tile, exclusive ownership of the op's buckets)
-// ---------------------------------------------------------------------------
-template <int VEC>
-__device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
-                                           const Tile8& tile, uint32_t i,
-                                           uint64_t clock0, bool fel_open, ctr_t* ctr,
-                                           int& size_delta) {
-  const int r = tile.thread_rank();
-  const int dim = t.dim;
-  const uint64_t key = a.keys[i];
-  const uint64_t h = fmix64(key);
-  const uint32_t d = digest_of(h);
-  const uint64_t b1 = h & t.mask;
-  uint64_t hb = b1;
-  const uint32_t occ1 = load_occ(t, b1, r);
-  int slot = probe_bucket<true, false>(t, tile, b1, key, d, occ1, ctr[kCompares]);
-  ctr[kLoads]++;
-  uint64_t b2 = b1;
-  uint32_t occ2 = occ1;
-  if (t.dual) {
-    b2 = second_hash(h) & t.mask;
-    if (slot < 0) {
-      occ2 = load_occ(t, b2, r);
-      slot = probe_bucket<true, false>(t, tile, b2, key, d, occ2, ctr[kCompares]);
-      ctr[kLoads]++;
-      hb = b2;
-    }
-  }
-  uint8_t outcome;
-  if (a.op == kOpErase) {
-    // _round_erase, table.py:1017-1023: key -> EMPTY; digest/score/value stay stale
-    if (slot >= 0) {
-      if (slot / kSPL == r) {
-        const uint64_t row = hb * kSlots + slot;
-        t.keys[row] = kEmptyKey;
-        const uint32_t o = (hb == b1) ? occ1 : occ2;
-        store_occ(t, hb, r, o & ~(1u << (slot % kSPL)));
-      }
-      size_delta--;
-      outcome = kErased;
-    } else {
-      outcome = kNotFound;
-    }
-    if (r == 0) a.outcomes[i] = outcome;
-    return;
-  }
-  const uint64_t tick = a.ticks ? a.ticks[i] : clock0 + (uint64_t)i + 1;
-  const uint64_t cs = a.scores ? a.scores[i] : 0;
-  float* vin = a.values + (uint64_t)i * dim;
-  if (slot >= 0) {
-    // hit: table.py:1045-1062
-    const uint64_t row = hb * kSlots + slot;
-    if (slot / kSPL == r) {
-      const uint64_t old = hit_needs_old(t.policy) ? t.scores[row] : 0;
-      t.scores[row] = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
-      summ_invalidate(t, hb, slot);
-    }
-    float* vr = value_row(t, row);
-    if (a.op == kOpFindOrInsert) {
-      copy_row<kG, VEC>(vin, vr, dim, r);
-      outcome = kFound;
-    } else {
-      copy_row<kG, VEC>(vr, vin, dim, r);
-      outcome = kUpdated;
-    }
-    ctr[row < t.fast_rows ? kVFast : kVOver]++;
-    if (r == 0) a.outcomes[i] = outcome;
-    return;
-  }
-  // miss: insert_scores, scoring.py:105-127
-  const uint64_t s_in = insert_score(t.policy, a.epoch, tick, cs);
-  uint64_t tb = b1;
-  int m = 0;
-  uint64_t minv = 0;
-  bool admit = false;
-  bool free_insert = false;
-  if (!t.dual) {
-    const int occ_total = tile_sum<kG>(tile, __popc(occ1));
-    if (occ_total < kSlots) {
-      free_insert = true;  // _bulk_insert_free, table.py:1072-1076
-    } else {
-      bucket_min(t, tile, b1, minv, m);  // table.py:1079-1083
-      ctr[kScans]++;
-      admit = s_in >= minv;  // single-bucket path admits ties
-    }
-  } else {
-    const int o1 = tile_sum<kG>(tile, __popc(occ1));
-    const int o2 = tile_sum<kG>(tile, __popc(occ2));
-    if (o1 < kSlots || o2 < kSlots) {
-      tb = o1 <= o2 ? b1 : b2;  // D1, table.py:1089-1095
-      free_insert = true;
-    } else {
-      uint64_t min1, min2;  // D2, table.py:1096-1119
-      int m1, m2;
-      bucket_min(t, tile, b1, min1, m1);
-      bucket_min(t, tile, b2, min2, m2);
-      ctr[kScans] += 2;
-      const bool use2 = min2 < min1;
-      tb = use2 ? b2 : b1;
-      m = use2 ? m2 : m1;
-      minv = use2 ? min2 : min1;
-      admit = t.admit_unified ? s_in >= minv : s_in > minv;
-    }
-  }
-  if (free_insert) {
-    // lowest EMPTY slot (table.py:1171) = lowest clear occupancy bit
-    const uint32_t occ = (tb == b1) ? occ1 : occ2;
-    const uint32_t hasfree = tile.ballot(occ != 0xFFFFu);
-    const int fl = __ffs(hasfree) - 1;
-    int s = 0;
-    if (r == fl) {
-      const int j = __ffs(~occ & 0xFFFFu) - 1;
-      s = r * kSPL + j;
-      const uint64_t row = tb * kSlots + s;
-      t.keys[row] = key;
-      t.digests[row] = (uint8_t)d;
-      t.scores[row] = s_in;
-      summ_invalidate(t, tb, s);
-      store_occ(t, tb, r, occ | (1u << j));
-    }
-    s = tile.shfl(s, fl);
-    const uint64_t row = tb * kSlots + s;
-    copy_row<kG, VEC>(value_row(t, row), vin, dim, r);
-    ctr[row < t.fast_rows ? kVFast : kVOver]++;
-    size_delta++;
-    outcome = kInserted;
-  } else if (!admit) {
-    outcome = kRejected;
-  } else {
-    const uint64_t row = tb * kSlots + m;
-    const int ol = m / kSPL;
-    float* vr = value_row(t, row);
-    if (a.collect) {
-      if (r == ol) {
-        a.ek[i] = t.keys[row];
-        a.es[i] = minv;
-      }
-      copy_row<kG, VEC>(a.ev + (uint64_t)i * dim, vr, dim, r);
-      ctr[row < t.fast_rows ? kVFast : kVOver]++;
-    }
-    if (r == ol) {
-      t.keys[row] = key;
-      t.digests[row] = (uint8_t)d;
-      t.scores[row] = s_in;
-      summ_invalidate(t, tb, m);
-    }
-    copy_row<kG, VEC>(vr, vin, dim, r);
-    ctr[row < t.fast_rows ? kVFast : kVOver]++;
-    outcome = kEvicted;
-    if (fel_open && r == 0) atomicMin(&a.sc->first_ev, i);
-  }
-  if (r == 0) a.outcomes[i] = outcome;
-}
-
-__device__ __forceinline__ void flush_tile_counters(const Tile8& tile, const TableDev& t,
-                                                    ctr_t* ctr, int size_delta) {
-  if (tile.thread_rank() != 0) {
-#pragma unroll
-    for (int k = 0; k < 6; k++) ctr[k] = 0;
-    size_delta = 0;
-  }
-  flush_counters<256>(t.counters, ctr, 6);
-  long long v = size_delta;
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);  // 64-bit warp sum
-  if ((threadIdx.x & 31) == 0 && v) atomicAdd(t.size, (unsigned long long)v);
-}
-
-// ---------------------------------------------------------------------------
 // pipeline kernels
 // ---------------------------------------------------------------------------
 __global__ void k_prep(TableDev t, const uint64_t* __restrict__ keys, int64_t n, uint32_t* __restrict__ bkt,
@@ -1335,62 +1167,6 @@ __global__ void __launch_bounds__(256) k_values_read(TableDev t, float* __restri
   }
 }
 
-// Dual mode: device-side leader rounds (table.py:945-962).
-template <int VEC>
-__global__ void __launch_bounds__(256) k_dual_rounds(TableDev t, OpArgs a, const uint32_t* __restrict__ b1s,
-                                                     const uint32_t* __restrict__ b2s, uint32_t* pend0,
-                                                     uint32_t* pend1, unsigned long long* lead,
-                                                     unsigned long long* round_ctr, int64_t n) {
-  cg::grid_group grid = cg::this_grid();
-  if (a.sc->err) return;
-  const Tile8 tile;
-  const int r = tile.thread_rank();
-  const int64_t tid = grid.thread_rank();
-  const int64_t nthreads = grid.size();
-  const int64_t gid = tid / kG;
-  const int64_t ngroups = nthreads / kG;
-  const uint64_t clock0 = *t.clock;
-  const bool fel_open = !*t.fel_set;
-  const unsigned long long round_base = *round_ctr;
-  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
-  int sd = 0;
-  unsigned m = (unsigned)n;
-  uint32_t* cur = pend0;
-  uint32_t* nxt = pend1;
-  for (unsigned long long rd = 1;; rd++) {
-    const unsigned long long R = (round_base + rd) << 32;
-    if (tid == 0) a.sc->npend[rd & 1] = 0;
-    for (int64_t j = tid; j < m; j += nthreads) {
-      const uint32_t i = cur[j];
-      const unsigned long long tag = R | (0xFFFFFFFFull - i);
-      atomicMax(&lead[b1s[i]], tag);
-      atomicMax(&lead[b2s[i]], tag);
-    }
-    grid.sync();
-    for (int64_t j = gid; j < m; j += ngroups) {
-      const uint32_t i = cur[j];
-      const unsigned long long tag = R | (0xFFFFFFFFull - i);
-      const bool leader = lead[b1s[i]] == tag && lead[b2s[i]] == tag;
-      if (leader) {
-        process_op<VEC>(t, a, tile, i, clock0, fel_open, ctr, sd);
-      } else if (r == 0) {
-        const unsigned pos = atomicAdd(&a.sc->npend[rd & 1], 1u);
-        nxt[pos] = i;
-      }
-    }
-    grid.sync();
-    m = *((volatile unsigned*)&a.sc->npend[rd & 1]);
-    if (m == 0) {
-      if (tid == 0) *round_ctr = round_base + rd;
-      break;
-    }
-    uint32_t* tmp = cur;
-    cur = nxt;
-    nxt = tmp;
-  }
-  flush_tile_counters(tile, t, ctr, sd);
-}
-
 // Clock advance + first_eviction_lambda (table.py:986-991) + error latch.
 __global__ void k_finalize(TableDev t, Scalars* sc, const uint8_t* __restrict__ outcomes, int64_t n,
                            unsigned long long clock_advance, int add_found) {
@@ -1614,6 +1390,7 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual
 }
 
 void ws_free(Workspace& ws) {
+  ws_free_dual(ws);
   void* ptrs[] = {ws.bkt, ws.idx, ws.sbkt, ws.sidx, ws.seg, ws.aux, ws.aux2, ws.skey, ws.skeys, ws.vrow, ws.rrow,
                   ws.rsrc,
                   ws.b2, ws.pend,
@@ -1660,12 +1437,13 @@ static cudaError_t run_ends(Workspace& ws, int64_t n, cudaStream_t s) {
 }
 
 cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, Workspace& ws,
-                         unsigned long long* round_ctr, unsigned long long* lead, int64_t* n_evicted,
+                         unsigned long long dual_tag, unsigned long long* lead, int64_t* n_evicted,
                          uint64_t* ek_out, float* ev_out, uint64_t* es_out, uint64_t clock_advance,
                          cudaStream_t s, int num_sms) {
   cudaError_t e;
   const bool collect = a.collect != 0;
   if ((e = ws_reserve(ws, n, t.dim, collect ? (t.dual ? 2 : 1) : 0, t.dual != 0))) return e;
+  if (t.dual && (e = ws_reserve_dual(ws, n, log2_buckets))) return e;
   a.sc = ws.sc;
   a.ek = ws.ek;
   a.es = ws.es;
@@ -1715,25 +1493,9 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       ktimer_end("apply", s);
       g_launches++;
     } else {
-      // cooperative grid: all blocks co-resident
-      void* fn = vec == 4 ? (void*)k_dual_rounds<4> : vec == 2 ? (void*)k_dual_rounds<2> : (void*)k_dual_rounds<1>;
-      int per_sm = 0;
-      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0))) return e;
-      if (per_sm < 1) per_sm = 1;
-      int64_t blocks = (int64_t)per_sm * num_sms;
-      const int64_t want = (n * kG + 255) / 256;
-      if (blocks > want) blocks = want < 1 ? 1 : want;
-      TableDev tt = t;
-      const uint32_t* b1s = ws.bkt;
-      const uint32_t* b2s = ws.b2;
-      uint32_t* p0 = ws.idx;
-      uint32_t* p1 = ws.pend;
-      int64_t nn = n;
-      void* args[] = {&tt, &a, &b1s, &b2s, &p0, &p1, &lead, &round_ctr, &nn};
-      ktimer_begin("dual_rounds", s);
-      if ((e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)blocks), dim3(256), args, 0, s))) return e;
-      ktimer_end("dual_rounds", s);
-      g_launches++;
+      ktimer_begin("dual_flow", s);
+      if ((e = run_dual(t, a, n, log2_buckets, ws, lead, dual_tag, vec, s, num_sms))) return e;
+      ktimer_end("dual_flow", s);
     }
   }
   k_finalize<<<1, 1024, 0, s>>>(t, ws.sc, a.op == kOpErase ? nullptr : a.outcomes, n, clock_advance, 0);
