@@ -5,13 +5,13 @@
 // key compares on digest matches only -> value-row gather (store.py:115-123).
 // Dual mode probes the second bucket only for first-bucket misses.
 //
-// Two passes.  Probe: one tile of 8 lanes per key, the digest line read as
-// 8 x 16 B (one coalesced 128-B transaction); each tile keeps 4 keys in
-// flight (all digest lines requested before any is consumed, then all first
-// candidate keys) and records the hit row.  Gather: value rows streamed from
-// the recorded rows with 8 x 16-B requests in flight per lane; separating it
-// from the dependent probe chain is what keeps the value traffic near the
-// copy roofline.
+// find (dim % 4 == 0, 16-B aligned rows): k_find_fused — a thread per key
+// reads the key's 128-B digest line (8 x 16 B in flight), tests it with an
+// any-zero-byte check, builds the exact 128-bit candidate mask only when
+// needed, checks candidate keys in slot order; then the warp moves its 32
+// value rows with coalesced 16-B loads/stores, 8 in flight per lane.
+// Otherwise (and for contains / find_ptr): k_find_tpk (the same probe,
+// recording rows) + k_find_gather.
 #include <cstdlib>
 #include <string>
 
@@ -19,114 +19,6 @@
 #include "hkv_kernels.h"
 
 namespace hkv {
-
-// Probe pass.  MODE 1: contains (found only), 2: find_ptr (found, tier,
-// offset), 4: find (found + the hit row per key for the gather pass).
-template <int MODE, int KPT>
-__global__ void __launch_bounds__(256) k_find(TableDev t, const uint64_t* __restrict__ keys, int64_t n,
-                                              uint8_t* __restrict__ found, uint8_t* __restrict__ tier,
-                                              int64_t* __restrict__ offset, uint32_t* __restrict__ rows) {
-  __shared__ BlockCtrs bc;
-  block_ctrs_init(bc);
-  const Tile8 tile;
-  const int r = tile.thread_rank();
-  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
-  const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / kG;
-  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
-  const int dim = t.dim;
-  int bad = 0;
-
-  for (int64_t base = gid * KPT; base < n; base += ngroups * KPT) {
-    uint64_t key[KPT], h[KPT], b[KPT];
-    uint4 dl[KPT];
-    bool live[KPT];
-#pragma unroll
-    for (int u = 0; u < KPT; u++) {
-      const int64_t i = base + u;
-      live[u] = i < n;
-      key[u] = live[u] ? __ldg(keys + i) : 0;
-      if (key[u] >= kLockedKey) { bad = 1; }
-      h[u] = fmix64(key[u]);
-      b[u] = h[u] & t.mask;
-    }
-    // stage 1: all digest lines in flight
-#pragma unroll
-    for (int u = 0; u < KPT; u++) {
-      if (live[u] && t.digest_filter)
-        dl[u] = ld_stream(reinterpret_cast<const uint4*>(t.digests + b[u] * kSlots) + r);
-      else
-        dl[u] = make_uint4(0, 0, 0, 0);
-    }
-    // stage 2: candidate keys (usually 0-1 per key), first candidate of every key issued together
-    int slot[KPT];
-    uint32_t cand[KPT];
-    uint64_t k0[KPT];
-#pragma unroll
-    for (int u = 0; u < KPT; u++) {
-      cand[u] = !live[u] ? 0u : (t.digest_filter ? match16(dl[u], digest_of(h[u])) : 0xFFFFu);
-      k0[u] = cand[u] ? __ldg(t.keys + b[u] * kSlots + r * kSPL + (__ffs(cand[u]) - 1)) : kEmptyKey;
-    }
-#pragma unroll
-    for (int u = 0; u < KPT; u++) {
-      const uint64_t* kp = t.keys + b[u] * kSlots + r * kSPL;
-      int hit = -1, ncmp = 0, ncmp_all = 0;
-      uint32_t c = cand[u];
-      uint64_t k = k0[u];
-      while (c) {
-        const int j = __ffs(c) - 1;
-        c &= c - 1;
-        if (k != kEmptyKey) {
-          ncmp_all++;
-          if (k == key[u]) { hit = r * kSPL + j; ncmp = ncmp_all; break; }
-        }
-        if (c) k = __ldg(kp + (__ffs(c) - 1));
-      }
-      const uint32_t hm = tile.ballot(hit >= 0);
-      int contrib = ncmp_all;
-      slot[u] = -1;
-      if (hm) {
-        const int hl = __ffs(hm) - 1;
-        slot[u] = tile.shfl(hit, hl);
-        contrib = r < hl ? ncmp_all : (r == hl ? ncmp : 0);
-      }
-      ctr[kCompares] += tile_sum<kG>(tile, contrib);
-      ctr[kLoads] += live[u];
-    }
-    if (t.dual) {
-      // second bucket for first-bucket misses (table.py:291-298)
-#pragma unroll
-      for (int u = 0; u < KPT; u++) {
-        if (!live[u] || slot[u] >= 0) continue;
-        b[u] = second_hash(h[u]) & t.mask;
-        slot[u] = probe_bucket<false, true>(t, tile, b[u], key[u], digest_of(h[u]), 0xFFFFu, ctr[kCompares]);
-        ctr[kLoads]++;
-      }
-    }
-    // stage 3: outputs
-    if (r == 0) {
-#pragma unroll
-      for (int u = 0; u < KPT; u++) {
-        if (!live[u]) continue;
-        const int64_t i = base + u;
-        const bool f = slot[u] >= 0;
-        const uint64_t row = b[u] * kSlots + (uint64_t)(f ? slot[u] : 0);
-        found[i] = f;
-        if constexpr (MODE == 4) rows[i] = f ? (uint32_t)row : 0xFFFFFFFFu;
-        if constexpr (MODE == 2) {
-          const bool over = row >= t.fast_rows;
-          tier[i] = f ? (uint8_t)over : 0;
-          offset[i] = !f ? -1 : (int64_t)((over ? row - t.fast_rows : row) * (uint64_t)dim);
-        }
-      }
-    }
-  }
-  if (bad) atomicOr(t.err, 1);
-  if (r != 0) {
-#pragma unroll
-    for (int k = 0; k < 6; k++) ctr[k] = 0;
-  }
-  block_ctrs_flush(bc, t.counters, nullptr, ctr, 0);
-}
 
 // Gather pass: out[i] = value row of the hit (rows at random, output
 // sequential), zero rows for misses when requested; KPT keys per tile and
@@ -335,22 +227,11 @@ __global__ void __launch_bounds__(256) k_find_fused(TableDev t, const uint64_t* 
 template <int MODE>
 static void launch_probe(const TableDev& t, const uint64_t* keys, int64_t n, uint8_t* found, uint8_t* tier,
                          int64_t* offset, uint32_t* rows, cudaStream_t s, int num_sms) {
-  static const bool tile_probe = getenv("HKV_FIND") && std::string(getenv("HKV_FIND")) == "tile";
-  if (!tile_probe) {
-    int64_t blocks = (n + 255) / 256;
-    const int64_t max_blocks = (int64_t)num_sms * 8;
-    if (blocks > max_blocks) blocks = max_blocks;
-    if (blocks < 1) blocks = 1;
-    k_find_tpk<MODE><<<(unsigned)blocks, 256, 0, s>>>(t, keys, n, found, tier, offset, rows);
-    g_launches++;
-    return;
-  }
-  constexpr int KPT = 4;
-  int64_t blocks = (((n + KPT - 1) / KPT) * kG + 255) / 256;
-  const int64_t max_blocks = (int64_t)num_sms * 8 * 4;
+  int64_t blocks = (n + 255) / 256;
+  const int64_t max_blocks = (int64_t)num_sms * 8;
   if (blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
-  k_find<MODE, KPT><<<(unsigned)blocks, 256, 0, s>>>(t, keys, n, found, tier, offset, rows);
+  k_find_tpk<MODE><<<(unsigned)blocks, 256, 0, s>>>(t, keys, n, found, tier, offset, rows);
   g_launches++;
 }
 

@@ -7,23 +7,20 @@
 //
 //  single mode  -- a key's whole candidate space is one bucket, so ops on
 //    different buckets commute.  k_prep hashes the batch, a stable radix sort
-//    groups ops by bucket (ascending batch index inside a bucket), and
-//    k_meta_single gives each bucket segment to one 8-lane tile (the tile
-//    owning the segment's first sorted position) that applies its ops' metadata
-//    in order with exclusive ownership of the bucket: no CAS, no retries,
-//    bit-exact at any contention.  Value rows then move in streaming kernels
-//    (k_values_read / k_values_write) driven by the recorded row plan.
-//  dual mode    -- an op touches two buckets; k_dual_rounds runs the
-//    reference's leader rounds on the device (table.py:945-962): per round
-//    every pending op bids its batch index on both buckets (atomicMax on a
-//    round-tagged word), ops that win both buckets apply in parallel, the
-//    rest wait.  One cooperative kernel, grid-wide barrier between phases.
+//    groups ops by bucket (ascending batch index inside a bucket), k_segments
+//    emits one record per bucket segment (and marks same-key runs), and
+//    k_meta_tps gives each segment to one thread that applies its ops'
+//    metadata in order with exclusive ownership of the bucket: no CAS, no
+//    retries, bit-exact at any contention.  Value rows then move in streaming
+//    kernels (k_values_read / k_values_write) driven by the recorded row plan.
+//  dual mode    -- an op touches two buckets: hkv_dual.cu runs a device
+//    dataflow over per-bucket turn counters (process_op per op).
 //
-// Per op (process_op) the tile restates _round_upsert (table.py:1025-1119):
-// digest probe (one 128-B line) -> hit: score refresh + value write/read ->
+// Per op (tps_op) the thread restates _round_upsert (table.py:1025-1119):
+// digest probe (one 128-B line) -> hit: score refresh + value plan ->
 // miss: insert at the lowest free slot (occupancy bitmap, __ffs) or, on a full
-// bucket, tile-wide argmin over the score row, admission test and eviction
-// (_finish_admission, table.py:1121-1163).
+// bucket, argmin over the score row through the group summary, admission
+// test and eviction (_finish_admission, table.py:1121-1163).
 #include <cub/cub.cuh>
 #include <cstdlib>
 #include <string>
@@ -96,7 +93,7 @@ struct SegRec {
 // position p inside a multi-op segment, brk[p] = p unless the op at p+1 has the
 // same key (then ~0), so a reverse min-scan gives run_end[p] = the last
 // position of p's run.  Followers (p-1 has the same key) get the collapsed
-// outcome `fcode` and no value row up front; apply_run writes the exceptions.
+// outcome `fcode` and no value row up front; tps_run writes the exceptions.
 __global__ void __launch_bounds__(1024) k_segments(const uint32_t* __restrict__ sb, const uint32_t* __restrict__ sidx,
                                                    const uint64_t* __restrict__ keys, int64_t n,
                                                    SegRec* __restrict__ recs, int64_t cap, Scalars* sc,
@@ -166,207 +163,6 @@ __global__ void __launch_bounds__(1024) k_segments(const uint32_t* __restrict__ 
   }
 }
 
-__device__ __forceinline__ unsigned ws_ballot(bool p, unsigned tb) { return (__ballot_sync(kFull, p) >> tb) & 0xFFu; }
-__device__ __forceinline__ unsigned ws_sum8(unsigned v) {
-  v += __shfl_xor_sync(kFull, v, 1);
-  v += __shfl_xor_sync(kFull, v, 2);
-  v += __shfl_xor_sync(kFull, v, 4);
-  return v;
-}
-
-struct LastWriter {  // per-tile shared-memory view
-  int* op;           // [128] op index of the slot's last writer
-  uint16_t* gen;     // [128] segment generation that wrote it
-  uint16_t cur;      // current segment generation
-  __device__ __forceinline__ int get(int s) const { return gen[s] == cur ? op[s] : -1; }
-  __device__ __forceinline__ void set(int s, int i) {
-    op[s] = i;
-    gen[s] = cur;
-  }
-};
-
-// Byte j (0..15) of a lane's 16-B digest slice.
-__device__ __forceinline__ void set_digest_byte(uint4& w, int j, uint32_t d) {
-  const uint32_t sh = (uint32_t)(j & 3) * 8u;
-  const uint32_t m = ~(0xFFu << sh);
-  const uint32_t v = (d & 0xFFu) << sh;
-  switch (j >> 2) {
-    case 0: w.x = (w.x & m) | v; break;
-    case 1: w.y = (w.y & m) | v; break;
-    case 2: w.z = (w.z & m) | v; break;
-    default: w.w = (w.w & m) | v; break;
-  }
-}
-
-// One op of every active tile of the warp (must be called by all 32 lanes).
-// dw/occ: this lane's digest / occupancy slice of bucket b, already loaded.
-// Returns (tile-uniform) the slot holding `key` after the op, -1 if absent.
-template <int OP, bool COLLECT>
-__device__ __forceinline__ int meta_op_ws(const TableDev& t, const OpArgs& a, unsigned lane, bool active,
-                                           uint32_t i, uint64_t key, uint32_t d, uint64_t b, uint4& dw, uint32_t& occ,
-                                           uint64_t clock0, bool fel_open, bool spec, LastWriter& lw,
-                                           uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
-                                           int32_t* __restrict__ rsrc, ctr_t* ctr, int& size_delta) {
-  const int r = (int)(lane & 7u);
-  const unsigned tb = lane & ~7u;
-  const uint64_t rowbase = b * kSlots;
-  uint64_t lmin = kMaxScore;
-  int lm = r * kSPL;
-  auto scan_scores = [&]() {
-    const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(t.scores + rowbase + r * kSPL);
-    ulonglong2 sv[kSPL / 2];
-#pragma unroll
-    for (int k = 0; k < kSPL / 2; k++) sv[k] = sp[k];
-    lmin = sv[0].x;
-    lm = r * kSPL;
-#pragma unroll
-    for (int k = 0; k < kSPL / 2; k++) {
-      if (k > 0 && sv[k].x < lmin) { lmin = sv[k].x; lm = r * kSPL + 2 * k; }
-      if (sv[k].y < lmin) { lmin = sv[k].y; lm = r * kSPL + 2 * k + 1; }
-    }
-  };
-  // candidate keys (first one issued before the score row so both are in flight)
-  uint32_t cand = active ? ((t.digest_filter ? match16(dw, d) : 0xFFFFu) & occ) : 0u;
-  const uint64_t* kp = t.keys + rowbase + r * kSPL;
-  uint64_t kc = cand ? kp[__ffs(cand) - 1] : 0;
-  if (OP != kOpErase && spec && active) scan_scores();
-  int hit = -1;
-  unsigned ncmp = 0, ncmp_all = 0;
-  while (cand) {
-    const int j = __ffs(cand) - 1;
-    cand &= cand - 1;
-    ncmp_all++;
-    if (kc == key) { hit = r * kSPL + j; ncmp = ncmp_all; break; }
-    if (cand) kc = kp[__ffs(cand) - 1];
-  }
-  const unsigned hm = ws_ballot(hit >= 0, tb);
-  const int hl = hm ? __ffs(hm) - 1 : 0;
-  int slot = __shfl_sync(kFull, hit, (int)tb + hl);
-  if (!hm) slot = -1;
-  unsigned contrib = ncmp_all;
-  if (hm) contrib = r < hl ? ncmp_all : (r == hl ? ncmp : 0u);
-  contrib = ws_sum8(contrib);
-  if (active && r == 0) {
-    ctr[kCompares] += contrib;
-    ctr[kLoads]++;
-  }
-  if constexpr (OP == kOpErase) {  // _round_erase, table.py:1017-1023
-    if (active && slot >= 0) {
-      if (slot / kSPL == r) {
-        t.keys[rowbase + slot] = kEmptyKey;
-        occ &= ~(1u << (slot % kSPL));
-        store_occ(t, b, r, occ);
-      }
-      if (r == 0) size_delta--;
-    }
-    if (active && r == 0) a.outcomes[i] = slot >= 0 ? kErased : kNotFound;
-    return -1;
-  }
-  const bool is_hit = active && slot >= 0;
-  const bool miss = active && slot < 0;
-  uint64_t tick = 0, cs = 0;
-  if (active) {
-    tick = a.ticks ? a.ticks[i] : clock0 + (uint64_t)i + 1;
-    cs = a.scores ? a.scores[i] : 0;
-  }
-  const uint64_t s_in = insert_score(t.policy, a.epoch, tick, cs);
-  uint8_t outcome = kRejected;
-  int wslot = -1;  // slot this op's value goes to
-  int rslot = -1;  // slot whose value this op reads
-  if (is_hit && slot / kSPL == r) {  // table.py:1045-1062
-    const uint64_t row = rowbase + slot;
-    const uint64_t old = hit_needs_old(t.policy) ? t.scores[row] : 0;
-    t.scores[row] = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
-    summ_invalidate(t, b, slot);
-  }
-  if (is_hit) {
-    if constexpr (OP == kOpFindOrInsert) {
-      outcome = kFound;
-      rslot = slot;
-    } else {
-      outcome = kUpdated;
-      wslot = slot;
-    }
-  }
-  const unsigned occ_total = ws_sum8(__popc(occ));
-  const bool free_ins = miss && occ_total < kSlots;
-  const bool full = miss && occ_total >= kSlots;
-  // _bulk_insert_free, table.py:1165-1181: lowest EMPTY slot = lowest clear bit
-  const unsigned hasfree = ws_ballot(occ != 0xFFFFu, tb);
-  const int fl = hasfree ? __ffs(hasfree) - 1 : 0;
-  int sl = 0;
-  if (free_ins && r == fl) {
-    const int j = __ffs(~occ & 0xFFFFu) - 1;
-    sl = r * kSPL + j;
-    t.keys[rowbase + sl] = key;
-    t.digests[rowbase + sl] = (uint8_t)d;
-    t.scores[rowbase + sl] = s_in;
-    summ_invalidate(t, b, sl);
-    occ |= 1u << j;
-    store_occ(t, b, r, occ);
-    set_digest_byte(dw, j, d);
-  }
-  sl = __shfl_sync(kFull, sl, (int)tb + fl);
-  if (free_ins) {
-    wslot = sl;
-    outcome = kInserted;
-    if (r == 0) size_delta++;
-  }
-  // full bucket: tile argmin over the score row, admission, eviction (table.py:1079-1083, 1121-1163)
-  if (__any_sync(kFull, full)) {
-    if (!spec && full) scan_scores();
-#pragma unroll
-    for (int o = kG / 2; o > 0; o >>= 1) {
-      const uint64_t ov = __shfl_xor_sync(kFull, lmin, o);
-      const int om = __shfl_xor_sync(kFull, lm, o);
-      if (ov < lmin || (ov == lmin && om < lm)) { lmin = ov; lm = om; }
-    }
-    if (full) {
-      if (r == 0) ctr[kScans]++;
-      if (s_in >= lmin) {  // the single-bucket path admits ties (table.py:1083)
-        const uint64_t row = rowbase + lm;
-        if (lm / kSPL == r) {
-          if constexpr (COLLECT) {
-            a.ek[i] = t.keys[row];
-            a.es[i] = lmin;
-          }
-          t.keys[row] = key;
-          t.digests[row] = (uint8_t)d;
-          t.scores[row] = s_in;
-          summ_invalidate(t, b, lm);
-          set_digest_byte(dw, lm % kSPL, d);
-        }
-        wslot = lm;
-        if constexpr (COLLECT) rslot = lm;
-        outcome = kEvicted;
-        if (fel_open && r == 0) atomicMin(&a.sc->first_ev, i);
-      }
-    }
-  }
-  if (!active) return -1;
-  // value plan (provenance read BEFORE this op's own write is recorded)
-  if (rslot >= 0) {
-    if (r == 0) ctr[rowbase + rslot < t.fast_rows ? kVFast : kVOver]++;
-    if (rslot / kSPL == r) {
-      rrow[i] = (uint32_t)(rowbase + rslot);
-      rsrc[i] = lw.get(rslot);
-    }
-  }
-  if (wslot >= 0) {
-    if (r == 0) ctr[rowbase + wslot < t.fast_rows ? kVFast : kVOver]++;
-    if (wslot / kSPL == r) {
-      const int prev = lw.get(wslot);
-      if (prev >= 0) vrow[prev] = kNoRow;  // retired: a later op of this segment rewrites the slot
-      lw.set(wslot, (int)i);
-      vrow[i] = (uint32_t)(rowbase + wslot);
-    }
-  } else if (r == 0) {
-    vrow[i] = kNoRow;
-  }
-  if (r == 0) a.outcomes[i] = outcome;
-  return rslot >= 0 ? rslot : wslot;
-}
-
 // Score after `cnt` consecutive hits of one key, the last one with tick tl /
 // custom score cs (scoring.py:79-102 applied cnt times; Lfu / EpochLfu
 // saturate exactly like the one-at-a-time loop).
@@ -389,214 +185,13 @@ __device__ __forceinline__ uint64_t run_hit_score(int policy, uint64_t old, uint
   }
 }
 
-// A run of consecutive ops on one key inside a bucket segment (sorted
-// positions q+1 .. qe, all after the op at q).  Under serial semantics
-// (SURVEY.md 3.3, App. A.8) every one of them sees the bucket exactly as the
-// op at q left it, so the run applies in O(1):
-//   key resident at slot `res`  -> cnt hits: Updated / Found, one aggregated
-//                                  score refresh, the last op's value wins
-//   erase                       -> key absent: NotFound
-//   absent, Lfu / EpochLfu      -> same admission score, same bucket: Rejected
-// Followers' outcome / vrow were pre-set by k_segments (Updated / Found /
-// NotFound, no value row); only the exceptions are written here.  TxnCounters
-// are exactly those of cnt individual probes.  Per-tile code, no collectives.
-template <int OP>
-__device__ __forceinline__ void apply_run(const TableDev& t, const OpArgs& a, int r, int64_t q, int64_t qe, int res,
-                                          uint64_t b, uint32_t d, uint4 dw, uint32_t occ, uint64_t clock0,
-                                          const uint32_t* __restrict__ sidx, LastWriter& lw,
-                                          uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
-                                          int32_t* __restrict__ rsrc, ctr_t* ctr) {
-  const uint32_t cnt = (uint32_t)(qe - q);
-  const uint64_t rowbase = b * kSlots;
-  uint32_t cand = (t.digest_filter ? match16(dw, d) : 0xFFFFu) & occ;
-  if (res >= 0) {  // compares stop at the match (table.py:243-268)
-    const int ol = res / kSPL;
-    if (r > ol) cand = 0;
-    else if (r == ol) cand &= (2u << (res % kSPL)) - 1u;
-  }
-  ctr[kCompares] += cnt * (uint32_t)__popc(cand);
-  if (r == 0) ctr[kLoads] += cnt;
-  if constexpr (OP == kOpErase) return;
-  if (res < 0) {  // rejected run
-    if (r == 0) ctr[kScans] += cnt;
-    for (int64_t p = q + 1 + r; p <= qe; p += kG) a.outcomes[sidx[p]] = kRejected;
-    return;
-  }
-  const uint64_t row = rowbase + res;
-  if (r == 0) ctr[row < t.fast_rows ? kVFast : kVOver] += cnt;
-  const uint32_t il = sidx[qe];
-  if (res / kSPL == r) {
-    const uint64_t tl = a.ticks ? a.ticks[il] : clock0 + (uint64_t)il + 1;
-    const uint64_t cs = a.scores ? a.scores[il] : 0;
-    t.scores[row] = run_hit_score(t.policy, t.scores[row], a.epoch, tl, a.scores != nullptr, cs, cnt);
-    summ_invalidate(t, b, res);
-    if constexpr (OP == kOpUpsert) {
-      const int prev = lw.get(res);
-      if (prev >= 0) vrow[prev] = kNoRow;
-      lw.set(res, (int)il);
-      vrow[il] = (uint32_t)row;
-    }
-  }
-  if constexpr (OP == kOpFindOrInsert) {  // every follower reads what the run head left in the row
-    const int src = lw.get(res);
-    for (int64_t p = q + 1 + r; p <= qe; p += kG) {
-      const uint32_t i = sidx[p];
-      rrow[i] = (uint32_t)row;
-      rsrc[i] = src;
-    }
-  }
-}
-
-__device__ __forceinline__ void load_slices(const TableDev& t, bool active, uint64_t b, int r, uint4& dw,
-                                            uint32_t& occ) {
-  if (active) {
-    dw = reinterpret_cast<const uint4*>(t.digests + b * kSlots)[r];
-    occ = load_occ(t, b, r);
-  } else {
-    dw = make_uint4(0, 0, 0, 0);
-    occ = 0;
-  }
-}
-
-// Metadata pass over one record list (singletons, or multi-op segments).
-// The next group's record and digest/occupancy slices are requested one
-// iteration ahead: segments own distinct buckets, so a prefetched slice can
-// never be stale.
-template <int OP, bool COLLECT>
-__device__ __forceinline__ void meta_pass(const TableDev& t, const OpArgs& a, const uint32_t* __restrict__ sb,
-                                          const uint32_t* __restrict__ sidx, const uint32_t* __restrict__ run_end,
-                                          const uint64_t* __restrict__ skeys, const SegRec* __restrict__ recs,
-                                          int64_t nrec, int64_t dir, int64_t n,
-                                          uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
-                                          int32_t* __restrict__ rsrc, LastWriter& lw, uint64_t clock0, bool fel_open,
-                                          bool spec, ctr_t* ctr, int& sd) {
-  const unsigned lane = threadIdx.x & 31u;
-  const int r = (int)(lane & 7u);
-  const int tile_in_warp = (int)(lane >> 3);
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t stride = nwarps * 4;
-  const bool lfu_like = t.policy == kLfu || t.policy == kEpochLfu;
-  auto rec_at = [&](int64_t sg) -> SegRec {
-    if (sg < nrec) return recs[dir > 0 ? sg : -sg];
-    return SegRec{0, 0, 0, 0, 0};
-  };
-  int64_t sg = warp * 4 + tile_in_warp;
-  SegRec rec = rec_at(sg);
-  uint4 dw;
-  uint32_t occ;
-  load_slices(t, sg < nrec, rec.b, r, dw, occ);
-  SegRec rec_n = rec_at(sg + stride);
-  for (int64_t sg0 = warp * 4; sg0 < nrec; sg0 += stride, sg += stride) {
-    bool active = sg < nrec;
-    // prefetch: next group's slices (its record arrived last iteration), the record after
-    uint4 dw_n;
-    uint32_t occ_n;
-    load_slices(t, sg + stride < nrec, rec_n.b, r, dw_n, occ_n);
-    const SegRec rec_nn = rec_at(sg + 2 * stride);
-    const uint64_t b = rec.b;
-    const bool multi = (rec.flags & 1u) != 0;
-    uint32_t i = rec.i, d = rec.flags >> 8;
-    uint64_t key = rec.key;
-    int64_t q = rec.p;
-    if (lw.cur == 0xFFFEu) {  // generation wrap: forget all
-#pragma unroll
-      for (int j = 0; j < kSPL; j++) lw.gen[r * kSPL + j] = 0xFFFFu;
-      lw.cur = 0;
-    }
-    lw.cur++;
-    __syncwarp();
-    while (true) {
-      // the next sorted position's inputs do not depend on this op: in flight while it runs
-      uint32_t nb_ = kNoRow, ni = 0;
-      uint64_t nk = 0;
-      int64_t qe = q;
-      if (active && multi && q + 1 < n) {
-        nb_ = sb[q + 1];
-        ni = sidx[q + 1];
-        nk = skeys[q + 1];
-        qe = (int64_t)run_end[q];
-      }
-      const int res = meta_op_ws<OP, COLLECT>(t, a, lane, active, i, key, d, b, dw, occ, clock0, fel_open, spec, lw,
-                                              vrow, rrow, rsrc, ctr, sd);
-      // a same-key run after this op collapses (apply_run)
-      int64_t run_to = -1;
-      if (active) {
-        if (nb_ == (uint32_t)b) {
-          if (qe > q && (OP == kOpErase || res >= 0 || lfu_like)) run_to = qe;
-        } else {
-          active = false;
-        }
-      }
-      if (!__any_sync(kFull, active)) break;
-      __syncwarp();  // LastWriter (shared memory) written by one lane, read by the tile
-      if (active) {
-        // dw / occ already reflect this tile's own writes (meta_op_ws keeps them in sync)
-        if (run_to >= 0) {
-          apply_run<OP>(t, a, r, q, run_to, res, b, d, dw, occ, clock0, sidx, lw, vrow, rrow, rsrc, ctr);
-          q = run_to;  // a run changes one score only
-          if (q + 1 < n && sb[q + 1] == (uint32_t)b) {
-            ++q;
-            i = sidx[q];
-            key = skeys[q];
-          } else {
-            active = false;
-          }
-        } else {
-          ++q;
-          i = ni;
-          key = nk;
-        }
-        if (active) d = digest_of(fmix64(key));
-      }
-      if (!__any_sync(kFull, active)) break;
-    }
-    rec = rec_n;
-    rec_n = rec_nn;
-    dw = dw_n;
-    occ = occ_n;
-  }
-}
-
-template <int OP, bool COLLECT>
-__global__ void __launch_bounds__(256, 3) k_meta_single(TableDev t, OpArgs a, const uint32_t* __restrict__ sb,
-                                                        const uint32_t* __restrict__ sidx,
-                                                        const uint32_t* __restrict__ run_end,
-                                                        const uint64_t* __restrict__ skeys,
-                                                        const SegRec* __restrict__ recs, int64_t cap, int64_t n,
-                                                        uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
-                                                        int32_t* __restrict__ rsrc) {
-  __shared__ int lw_op[256 / kG][kSlots];
-  __shared__ uint16_t lw_gen[256 / kG][kSlots];
-  __shared__ BlockCtrs bc;
-  if (a.sc->err) return;
-  const unsigned lane = threadIdx.x & 31u;
-  const int r = (int)(lane & 7u);
-  LastWriter lw{lw_op[threadIdx.x / kG], lw_gen[threadIdx.x / kG], 0};
-#pragma unroll
-  for (int j = 0; j < kSPL; j++) lw.gen[r * kSPL + j] = 0xFFFFu;
-  block_ctrs_init(bc);
-  const uint64_t clock0 = *t.clock;
-  const bool fel_open = !*t.fel_set;
-  // speculative score-row read with the digest line when buckets are almost surely full
-  const unsigned long long sz = *t.size;
-  const bool spec = sz * 100ull > t.capacity * 97ull;
-  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
-  int sd = 0;
-  meta_pass<OP, COLLECT>(t, a, sb, sidx, run_end, skeys, recs, (int64_t)a.sc->nseg, 1, n, vrow, rrow, rsrc, lw, clock0,
-                         fel_open, spec, ctr, sd);
-  meta_pass<OP, COLLECT>(t, a, sb, sidx, run_end, skeys, recs + (cap - 1), (int64_t)a.sc->nmulti, -1, n, vrow, rrow, rsrc,
-                         lw, clock0, fel_open, spec, ctr, sd);
-  block_ctrs_flush(bc, t.counters, t.size, ctr, sd);
-}
-
 // ---------------------------------------------------------------------------
 // Single mode, metadata pass, one THREAD per bucket segment (the default).
 //
 // A thread owns its segment's bucket for the whole batch, keeps the bucket's
-// digest line (128 B) and occupancy bitmap (16 B) in registers, updates them
-// in place after its own writes, and applies the segment's ops in batch order
-// (same per-op restatement of _round_upsert as meta_op_ws, table.py:1025-1163).
+// digest line (128 B) and occupancy bitmap (16 B) in shared memory (staged by
+// cp.async one segment ahead), updates them in place after its own writes,
+// and applies the segment's ops in batch order (table.py:1025-1163).
 // Full-bucket decisions use the per-group eviction summary (smin / svalid):
 // argmin over 8 group minima (64 B), then the chosen group's 16 scores
 // (128 B) to find the slot — np.argmin's first-index tie rule holds because
@@ -898,7 +493,17 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
   return rslot >= 0 ? rslot : wslot;
 }
 
-// same-key run q+1 .. qe after the op at q (see apply_run): thread version
+// A run of consecutive ops on one key inside a bucket segment (sorted
+// positions q+1 .. qe, all after the op at q).  Under serial semantics
+// (SURVEY.md 3.3, App. A.8) every one of them sees the bucket exactly as the
+// op at q left it, so the run applies in O(1):
+//   key resident at slot `res`  -> cnt hits: Updated / Found, one aggregated
+//                                  score refresh, the last op's value wins
+//   erase                       -> key absent: NotFound
+//   absent, Lfu / EpochLfu      -> same admission score, same bucket: Rejected
+// Followers' outcome / vrow were pre-set by k_segments (Updated / Found /
+// NotFound, no value row); only the exceptions are written here.  TxnCounters
+// are exactly those of cnt individual probes.
 template <int OP>
 __device__ __forceinline__ void tps_run(const TableDev& t, const OpArgs& a, TpsState& S, int64_t q, int64_t qe,
                                         int res, uint64_t b, uint32_t d, uint64_t clock0,
@@ -1462,34 +1067,23 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
                                                                  a.outcomes, ws.vrow, fcode, ws.skeys);
       g_launches++;
       if ((e = run_ends(ws, n, s))) return e;
-      int64_t blocks = (((n + kG - 1) / kG) * kG + 255) / 256;
-      if (blocks > (int64_t)num_sms * 3) blocks = (int64_t)num_sms * 3;  // one resident wave (3 blocks/SM)
       ktimer_begin("apply", s);
-      static const bool tile_meta = getenv("HKV_META") && std::string(getenv("HKV_META")) == "tile";
-      if (tile_meta) {
-        auto* fn = a.op == kOpErase ? k_meta_single<kOpErase, false>
-                   : a.op == kOpFindOrInsert ? k_meta_single<kOpFindOrInsert, false>
-                   : a.collect ? k_meta_single<kOpUpsert, true> : k_meta_single<kOpUpsert, false>;
-        fn<<<(unsigned)blocks, 256, 0, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, recs, n, n, ws.vrow, ws.rrow,
-                                            ws.rsrc);
-      } else {
-        auto* fn = a.op == kOpErase ? k_meta_tps<kOpErase, false>
-                   : a.op == kOpFindOrInsert ? k_meta_tps<kOpFindOrInsert, false>
-                   : a.collect ? k_meta_tps<kOpUpsert, true> : k_meta_tps<kOpUpsert, false>;
-        const size_t smem = 2 * kTpsThreads * kTpsStageU4 * sizeof(uint4);
-        static bool attr_set = false;
-        if (!attr_set) {
-          for (auto* f : {k_meta_tps<kOpErase, false>, k_meta_tps<kOpFindOrInsert, false>, k_meta_tps<kOpUpsert, true>,
-                          k_meta_tps<kOpUpsert, false>})
-            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          attr_set = true;
-        }
-        int64_t tb = (n + kTpsThreads - 1) / kTpsThreads;
-        const int64_t tcap = (int64_t)num_sms * 2;  // one resident wave
-        if (tb > tcap) tb = tcap;
-        fn<<<(unsigned)(tb < 1 ? 1 : tb), kTpsThreads, smem, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, recs, n, n,
-                                                                 ws.vrow, ws.rrow, ws.rsrc);
+      auto* fn = a.op == kOpErase ? k_meta_tps<kOpErase, false>
+                 : a.op == kOpFindOrInsert ? k_meta_tps<kOpFindOrInsert, false>
+                 : a.collect ? k_meta_tps<kOpUpsert, true> : k_meta_tps<kOpUpsert, false>;
+      const size_t smem = 2 * kTpsThreads * kTpsStageU4 * sizeof(uint4);
+      static bool attr_set = false;
+      if (!attr_set) {
+        for (auto* f : {k_meta_tps<kOpErase, false>, k_meta_tps<kOpFindOrInsert, false>, k_meta_tps<kOpUpsert, true>,
+                        k_meta_tps<kOpUpsert, false>})
+          cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
       }
+      int64_t tb = (n + kTpsThreads - 1) / kTpsThreads;
+      const int64_t tcap = (int64_t)num_sms * 2;  // one resident wave
+      if (tb > tcap) tb = tcap;
+      fn<<<(unsigned)(tb < 1 ? 1 : tb), kTpsThreads, smem, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, recs, n, n,
+                                                               ws.vrow, ws.rrow, ws.rsrc);
       ktimer_end("apply", s);
       g_launches++;
     } else {
