@@ -1,0 +1,108 @@
+"""GPU side of the sharded table on the one GPU this run has:
+
+* hkv_route (hash + stable grouping by owner rank) against a numpy router for
+  world sizes 2 / 4 / 8;
+* ShardedCacheTable over a 1-rank NCCL process group: real CUDA local table,
+  real all_to_all_single, explicit global LRU ticks and clock_advance through
+  the kernels — bit-exact against one global oracle table.
+
+The multi-rank exchange logic itself is covered on CPU by
+tests/test_sharded_gloo.py (world size 2, gloo).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+
+from oracle.oracle import OracleTable  # noqa: E402
+from test_sharded_gloo import numpy_router  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_route_kernel_matches_numpy(world):
+    from paper_2603_17168_b200.sharded import cuda_router
+
+    rng = np.random.default_rng(world)
+    keys = rng.integers(1, 2**63, size=100_003, dtype=np.uint64)
+    kd = torch.from_numpy(keys.view(np.int64)).cuda()
+    gb = 1 << 16
+    perm_d, counts_d = cuda_router(kd, gb, world)
+    perm_h, counts_h = numpy_router(torch.from_numpy(keys.view(np.int64)), gb, world)
+    assert np.array_equal(counts_d.cpu().numpy(), counts_h.numpy())
+    assert np.array_equal(perm_d.cpu().numpy(), perm_h.numpy())
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("policy", ["kLru", "kLfu", "kCustomized"])
+def test_sharded_one_rank_nccl_equals_oracle(policy):
+    import paper_2603_17168_b200 as hkv
+    from paper_2603_17168_b200.sharded import ShardedCacheTable
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        cap, dim = 128 * 64, 8
+        st = ShardedCacheTable(hkv.TableConfig(capacity=cap, value_dim=dim, score_policy=policy))
+        g = OracleTable(cap, dim, "single", policy)
+        rng = np.random.default_rng(7)
+        ops = ["insert_or_assign", "insert_and_evict", "find", "find_or_insert", "erase", "assign", "assign_scores",
+               "contains", "insert_and_evict"] * 3
+        for step, op in enumerate(ops):
+            n = int(rng.integers(500, 3000))
+            k = rng.integers(1, 3 * cap, size=n).astype(np.uint64)
+            v = rng.standard_normal((n, dim)).astype(np.float32)
+            s = rng.integers(0, 40, size=n).astype(np.uint64) if policy == "kCustomized" else None
+            kt = torch.from_numpy(k.view(np.int64)).cuda()
+            vt = torch.from_numpy(v.copy()).cuda()
+            stt = None if s is None else torch.from_numpy(s.view(np.int64)).cuda()
+            if op == "insert_or_assign":
+                assert np.array_equal(st.insert_or_assign(kt, vt, stt).cpu().numpy(), g.insert_or_assign(k, v, s))
+            elif op == "insert_and_evict":
+                o, ek, ev, es = st.insert_and_evict(kt, vt, stt)
+                go, gek, gev, ges = g.insert_and_evict(k, v, s)
+                assert np.array_equal(o.cpu().numpy(), go)
+                assert np.array_equal(ek.view(torch.int64).cpu().numpy().view(np.uint64), gek)
+                assert ev.cpu().numpy().tobytes() == gev.tobytes()
+                assert np.array_equal(es.view(torch.int64).cpu().numpy().view(np.uint64), ges)
+            elif op == "find":
+                f, vv = st.find(kt)
+                gf, gvv = g.find(k)
+                assert np.array_equal(f.cpu().numpy(), gf) and vv.cpu().numpy().tobytes() == gvv.tobytes()
+            elif op == "contains":
+                assert np.array_equal(st.contains(kt).cpu().numpy(), g.contains(k))
+            elif op == "find_or_insert":
+                o = st.find_or_insert(kt, vt, stt)
+                gv = v.copy()
+                go = g.find_or_insert(k, gv, s)
+                assert np.array_equal(o.cpu().numpy(), go) and vt.cpu().numpy().tobytes() == gv.tobytes()
+            elif op == "erase":
+                assert np.array_equal(st.erase(kt).cpu().numpy(), g.erase(k))
+            elif op == "assign":
+                assert np.array_equal(st.assign(kt, vt).cpu().numpy(), g.assign(k, v))
+            elif op == "assign_scores":
+                a = st.assign_scores(kt, stt) if policy == "kCustomized" else st.assign_scores(kt)
+                b = g.assign_scores(k, s) if policy == "kCustomized" else g.assign_scores(k)
+                assert np.array_equal(a.cpu().numpy(), b), op
+        assert st.size() == g.size()
+        state = st.local.export_state()
+        assert state["keys"].tobytes() == g.keys.tobytes()
+        assert state["scores"].tobytes() == g.scores.tobytes()
+        assert state["values"].tobytes() == g.values.tobytes()
+        assert state["clock"] == g.clock and st.clock == g.clock
+    finally:
+        dist.destroy_process_group()
