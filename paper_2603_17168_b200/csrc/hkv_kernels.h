@@ -15,7 +15,7 @@ struct Scalars {
   unsigned nmulti;               // multi-op bucket segments
   unsigned first_ev;             // lowest batch index with an Evicted outcome
   unsigned npend[2];             // dual-mode pending list sizes (per round parity)
-  unsigned pad;
+  unsigned has_runs;             // single mode: some op is followed by the same key in its bucket segment
   long long size_before;         // table size when the batch started
   unsigned long long nfound;     // assign: found ops (clock advance for refresh)
   long long n_sel;               // DeviceSelect count
@@ -38,7 +38,8 @@ struct Workspace {
   uint64_t* skeys = nullptr; // single mode: keys in sorted (bucket, batch index) order
   uint32_t* vrow = nullptr;  // single mode: destination row of final value writers
   uint32_t* rrow = nullptr;  // single mode: row of a value read
-  int32_t* rsrc = nullptr;   // single mode: provenance of a value read (-1 = pre-batch row)
+  int32_t* rsrc = nullptr;
+  int* lwtab = nullptr;       // single mode: per-thread last-writer tables of the metadata pass   // single mode: provenance of a value read (-1 = pre-batch row)
   uint32_t* b2 = nullptr;    // dual: second bucket
   uint32_t* pend = nullptr;  // dual: second pending list
   uint64_t* ek = nullptr;

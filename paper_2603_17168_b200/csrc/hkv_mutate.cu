@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(1024) k_segments(const uint32_t* __restrict__ 
   if (p < n) {
     const bool same_next = multi && k_next == k;
     brk[p] = same_next ? 0xFFFFFFFFu : (uint32_t)p;
+    if (same_next) sc->has_runs = 1;
     if (in_multi) skeys[p] = k;
     if (prev_same_b && k_prev == k) {
       outcomes[i] = fcode;
@@ -201,7 +202,16 @@ __device__ __forceinline__ uint64_t run_hit_score(int policy, uint64_t old, uint
 // cross-lane collectives, which is what the metadata pass is bound by
 // (dependent random loads, profiles/r01).
 // ---------------------------------------------------------------------------
+constexpr int kTpsThreads = 256;  // block size of k_meta_tps (stride of its per-thread shared arrays)
+
 struct TpsState {
+  int* lw;           // last-writer table: lw[slot * lws] = op that last wrote the slot (global scratch,
+  int64_t lws;       //   one 128-entry table per thread; used once a segment passes kLwScan ops)
+  const uint32_t* sidx;
+  const uint32_t* vrow;
+  int64_t p0;        // the segment's first sorted position
+  uint64_t rowbase;
+  bool tab;          // the table holds this segment's writers
   uint4* L;          // digest line (shared memory, 8 x 16 B)
   uint32_t* O;       // occupancy bitmap words (shared memory, slots 32w .. 32w+31)
   uint32_t wm[4];    // slots already written by an earlier op of this segment
@@ -330,23 +340,53 @@ __device__ __forceinline__ void tps_score_written(const TableDev& t, uint64_t b,
   }
 }
 
-// The op of this segment that last wrote `row` at or before sorted position
-// `from` (the segment starts at p0).  Only called when the slot's bit in
-// S.wm says some earlier op of the segment wrote it, which is rare: retired
-// writers hold kNoRow, so the latest writer is the one whose vrow == row.
-__device__ __forceinline__ int tps_last_writer(const uint32_t* __restrict__ sidx, const uint32_t* vrow, uint32_t row,
-                                               int64_t p0, int64_t from) {
-  for (int64_t p = from; p >= p0; p--) {
-    const uint32_t j = sidx[p];
-    if (vrow[j] == row) return (int)j;
+// Last writer of a slot within the current segment (asked only when S.wm
+// says an earlier op of the segment wrote it).  Short segments scan back
+// through their few positions (retired writers hold kNoRow, so the latest
+// writer is the one whose vrow is the row); once a segment passes kLwScan ops
+// (configs[0]: ~128 ops per bucket, zipf hot buckets) the thread's table in
+// global scratch is filled from those positions and kept current, so long
+// segments stay linear.  Nothing is written for the short segments that make
+// up uniform batches.
+constexpr int kLwScan = 16;
+__device__ __forceinline__ int lw_get(const TpsState& S, int slot, int64_t from) {
+  if (S.tab) return S.lw[slot * S.lws];
+  const uint32_t row = (uint32_t)(S.rowbase + slot);
+  for (int64_t p = from; p >= S.p0; p--) {
+    const uint32_t j = S.sidx[p];
+    if (S.vrow[j] == row) return (int)j;
   }
   return -1;
+}
+__device__ __forceinline__ void lw_set(const TpsState& S, int slot, uint32_t op) {
+  if (S.tab) S.lw[slot * S.lws] = (int)op;
+}
+// Collapsed stretches of same-key runs hold no writer but their last op, and
+// tps_run leaves a jump mark (run_end[q+1] = qe | kJump) at their start, so the
+// fill costs the segment's individually applied ops, not its positions (a
+// zipf hot bucket holds tens of thousands of positions but ~60 runs).
+constexpr uint32_t kJump = 0x80000000u;
+__device__ __forceinline__ void lw_fill(TpsState& S, int64_t q, const uint32_t* run_end, bool runs) {
+  // (run_end is read through the coherent path: tps_run writes it in this kernel)
+  for (int64_t p = S.p0; p < q;) {
+    if (runs) {
+      const uint32_t m = run_end[p];
+      if (m & kJump) {
+        p = (int64_t)(m & ~kJump);  // the stretch's last op (its only possible writer)
+        continue;
+      }
+    }
+    const uint32_t j = S.sidx[p];
+    const uint32_t w = S.vrow[j];
+    if (w != kNoRow) S.lw[(int64_t)(w - S.rowbase) * S.lws] = (int)j;
+    p++;
+  }
+  S.tab = true;
 }
 
 template <int OP, bool COLLECT>
 __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsState& S, uint64_t b, uint32_t i,
-                                      uint64_t key, uint32_t d, uint64_t clock0, bool fel_open, int64_t p0,
-                                      int64_t q, const uint32_t* __restrict__ sidx,
+                                      uint64_t key, uint32_t d, uint64_t clock0, bool fel_open, int64_t q,
                                       uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
                                       int32_t* __restrict__ rsrc, ctr_t* ctr, int& sd, uint32_t& fe_min) {
   const uint64_t rowbase = b * kSlots;
@@ -476,15 +516,16 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
   if (rslot >= 0) {
     ctr[rowbase + rslot < t.fast_rows ? kVFast : kVOver]++;
     rrow[i] = (uint32_t)(rowbase + rslot);
-    rsrc[i] = bit128(S.wm, rslot) ? tps_last_writer(sidx, vrow, (uint32_t)(rowbase + rslot), p0, q - 1) : -1;
+    rsrc[i] = bit128(S.wm, rslot) ? lw_get(S, rslot, q - 1) : -1;
   }
   if (wslot >= 0) {
     ctr[rowbase + wslot < t.fast_rows ? kVFast : kVOver]++;
     if (bit128(S.wm, wslot)) {  // retired: this op rewrites the slot
-      const int prev = tps_last_writer(sidx, vrow, (uint32_t)(rowbase + wslot), p0, q - 1);
+      const int prev = lw_get(S, wslot, q - 1);
       if (prev >= 0) vrow[prev] = kNoRow;
     }
     setbit128(S.wm, wslot);
+    lw_set(S, wslot, i);
     vrow[i] = (uint32_t)(rowbase + wslot);
   } else {
     vrow[i] = kNoRow;
@@ -507,7 +548,7 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
 template <int OP>
 __device__ __forceinline__ void tps_run(const TableDev& t, const OpArgs& a, TpsState& S, int64_t q, int64_t qe,
                                         int res, uint64_t b, uint32_t d, uint64_t clock0,
-                                        const uint32_t* __restrict__ sidx, int64_t p0, uint32_t* __restrict__ vrow,
+                                        const uint32_t* __restrict__ sidx, uint32_t* __restrict__ vrow,
                                         uint32_t* __restrict__ rrow, int32_t* __restrict__ rsrc, ctr_t* ctr) {
   const uint32_t cnt = (uint32_t)(qe - q);
   const uint64_t rowbase = b * kSlots;
@@ -538,14 +579,15 @@ __device__ __forceinline__ void tps_run(const TableDev& t, const OpArgs& a, TpsS
   tps_score_written(t, b, S, res, ns);
   if constexpr (OP == kOpUpsert) {
     if (bit128(S.wm, res)) {
-      const int prev = tps_last_writer(sidx, vrow, (uint32_t)row, p0, q);
+      const int prev = lw_get(S, res, q);
       if (prev >= 0) vrow[prev] = kNoRow;
     }
     setbit128(S.wm, res);
+    lw_set(S, res, il);
     vrow[il] = (uint32_t)row;
   }
   if constexpr (OP == kOpFindOrInsert) {
-    const int src = bit128(S.wm, res) ? tps_last_writer(sidx, vrow, (uint32_t)row, p0, q) : -1;
+    const int src = bit128(S.wm, res) ? lw_get(S, res, q) : -1;
     for (int64_t p = q + 1; p <= qe; p++) {
       const uint32_t j = sidx[p];
       rrow[j] = (uint32_t)row;
@@ -562,7 +604,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-constexpr int kTpsThreads = 256;
 constexpr int kTpsStageU4 = 9;  // per thread and stage: 8 x 16 B digest line + 16 B occupancy (odd stride: no bank conflicts)
 
 // stage buffer of this thread: [stage][thread][9 x uint4]
@@ -579,12 +620,20 @@ __device__ __forceinline__ void tps_fetch(const TableDev& t, uint4* buf, uint64_
 template <int OP, bool COLLECT>
 __device__ __forceinline__ void tps_segment(const TableDev& t, const OpArgs& a, const SegRec& rec, uint4* buf,
                                             const uint32_t* __restrict__ sb, const uint32_t* __restrict__ sidx,
-                                            const uint32_t* __restrict__ run_end, const uint64_t* __restrict__ skeys,
+                                            uint32_t* run_end, const uint64_t* __restrict__ skeys,
                                             int64_t n, uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
                                             int32_t* __restrict__ rsrc, uint64_t clock0, bool fel_open,
-                                            bool spec, bool lfu_like, ctr_t* ctr, int& sd, uint32_t& fe_min) {
+                                            bool spec, bool lfu_like, bool runs, ctr_t* ctr, int& sd,
+                                            uint32_t& fe_min, int* lw, int64_t lws) {
   const uint64_t b = rec.b;
   TpsState S;
+  S.lw = lw;
+  S.lws = lws;
+  S.sidx = sidx;
+  S.vrow = vrow;
+  S.p0 = rec.p;
+  S.rowbase = b * kSlots;
+  S.tab = false;
   S.L = buf;
   S.O = reinterpret_cast<uint32_t*>(buf + 8);
 #pragma unroll
@@ -605,13 +654,15 @@ __device__ __forceinline__ void tps_segment(const TableDev& t, const OpArgs& a, 
       nb_ = sb[q + 1];
       ni = sidx[q + 1];
       nk = skeys[q + 1];
-      qe = (int64_t)run_end[q];
+      qe = runs ? (int64_t)run_end[q] : q;
     }
-    const int res = tps_op<OP, COLLECT>(t, a, S, b, i, key, d, clock0, fel_open, rec.p, q, sidx, vrow, rrow, rsrc,
+    if (!S.tab && q - S.p0 >= kLwScan) lw_fill(S, q, run_end, runs);
+    const int res = tps_op<OP, COLLECT>(t, a, S, b, i, key, d, clock0, fel_open, q, vrow, rrow, rsrc,
                                         ctr, sd, fe_min);
     if (nb_ != (uint32_t)b) break;
     if (qe > q && (OP == kOpErase || res >= 0 || lfu_like)) {
-      tps_run<OP>(t, a, S, q, qe, res, b, d, clock0, sidx, rec.p, vrow, rrow, rsrc, ctr);
+      tps_run<OP>(t, a, S, q, qe, res, b, d, clock0, sidx, vrow, rrow, rsrc, ctr);
+      if (qe > q + 1) run_end[q + 1] = (uint32_t)qe | kJump;  // for lw_fill
       q = qe;
       if (!(q + 1 < n && sb[q + 1] == (uint32_t)b)) break;
       ++q;
@@ -639,11 +690,11 @@ __device__ __forceinline__ void tps_segment(const TableDev& t, const OpArgs& a, 
 template <int OP, bool COLLECT>
 __global__ void __launch_bounds__(kTpsThreads, 2) k_meta_tps(TableDev t, OpArgs a, const uint32_t* __restrict__ sb,
                                                             const uint32_t* __restrict__ sidx,
-                                                            const uint32_t* __restrict__ run_end,
+                                                            uint32_t* run_end,  // written: lw_fill jump marks
                                                             const uint64_t* __restrict__ skeys,
                                                             const SegRec* __restrict__ recs, int64_t cap, int64_t n,
                                                             uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
-                                                            int32_t* __restrict__ rsrc) {
+                                                            int32_t* __restrict__ rsrc, int* __restrict__ lwtab) {
   extern __shared__ uint4 tps_smem[];
   __shared__ BlockCtrs bc;
   if (a.sc->err) return;
@@ -653,6 +704,7 @@ __global__ void __launch_bounds__(kTpsThreads, 2) k_meta_tps(TableDev t, OpArgs 
   // at lambda > 0.97 a full bucket is the rule: fetch the summary with the first op
   const bool spec = *t.size * 100ull > t.capacity * 97ull;
   const bool lfu_like = t.policy == kLfu || t.policy == kEpochLfu;
+  const bool runs = a.sc->has_runs != 0;
   ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
   int sd = 0;
   uint32_t fe_min = 0xFFFFFFFFu;
@@ -663,7 +715,8 @@ __global__ void __launch_bounds__(kTpsThreads, 2) k_meta_tps(TableDev t, OpArgs 
     if (j >= nall) return SegRec{0, 0, 0, 0, 0};
     return j < nseg ? recs[j] : recs[cap - 1 - (j - nseg)];
   };
-  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t j = gtid;
   SegRec ra = rec_at(j), rb = rec_at(j + stride);
   if (j < nall) tps_fetch(t, tps_buf(tps_smem, 0), ra.b);
   cp_async_commit();
@@ -674,7 +727,7 @@ __global__ void __launch_bounds__(kTpsThreads, 2) k_meta_tps(TableDev t, OpArgs 
     cp_async_wait<1>();
     uint4* buf = tps_buf(tps_smem, stage);
     tps_segment<OP, COLLECT>(t, a, ra, buf, sb, sidx, run_end, skeys, n, vrow, rrow, rsrc, clock0, fel_open, spec,
-                             lfu_like, ctr, sd, fe_min);
+                             lfu_like, runs, ctr, sd, fe_min, lwtab + gtid, stride);
     ra = rb;
     rb = rn;
     if (j + 2 * stride < nall) tps_fetch(t, buf, rb.b);
@@ -997,6 +1050,7 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual
 void ws_free(Workspace& ws) {
   ws_free_dual(ws);
   void* ptrs[] = {ws.bkt, ws.idx, ws.sbkt, ws.sidx, ws.seg, ws.aux, ws.aux2, ws.skey, ws.skeys, ws.vrow, ws.rrow,
+                  ws.lwtab,
                   ws.rsrc,
                   ws.b2, ws.pend,
                   ws.ek, ws.es, ws.ev, ws.cub_tmp, ws.sc};
@@ -1030,15 +1084,58 @@ static cudaError_t sort_segments(Workspace& ws, int64_t n, int log2_buckets, cud
   return cudaGetLastError();
 }
 
-// run_end[p] = min{p' >= p : brk[p'] != ~0} — a reverse inclusive min-scan
-// over brk (k_segments) giving the last position of p's same-key run.
+// run_end[p] = min{p' >= p : brk[p'] != ~0}: the last position of p's
+// same-key run.  Two passes over tiles of kRunTile positions, both skipped
+// when the batch has no same-key run (uniform batches): an in-tile reverse
+// min-scan (thread 0 takes the tile's last chunk, so a forward block scan
+// over threads is a reverse scan over positions) that also records each
+// tile's first break, then a fix-up for positions whose run crosses the
+// tile end (walks the following tiles' first breaks).
+constexpr int kRunThreads = 1024, kRunPer = 4, kRunTile = kRunThreads * kRunPer;
+
+__global__ void __launch_bounds__(kRunThreads) k_run_ends_tile(const uint32_t* __restrict__ brk, int64_t n,
+                                                               uint32_t* __restrict__ run_end,
+                                                               uint32_t* __restrict__ tile_first, const Scalars* sc) {
+  if (!sc->has_runs || sc->err) return;
+  typedef cub::BlockScan<uint32_t, kRunThreads> BS;
+  __shared__ typename BS::TempStorage tmp;
+  const int64_t base = (int64_t)blockIdx.x * kRunTile + (int64_t)(kRunThreads - 1 - threadIdx.x) * kRunPer;
+  uint32_t v[kRunPer];
+  uint32_t agg = 0xFFFFFFFFu;
+#pragma unroll
+  for (int k = kRunPer - 1; k >= 0; k--) {
+    const int64_t p = base + k;
+    const uint32_t x = p < n ? brk[p] : 0xFFFFFFFFu;
+    agg = x < agg ? x : agg;
+    v[k] = agg;  // first break at or after p inside this chunk
+  }
+  uint32_t after;  // first break in the chunks after this one (inside the tile)
+  BS(tmp).ExclusiveScan(agg, after, 0xFFFFFFFFu, cub::Min());
+  if (threadIdx.x == kRunThreads - 1) tile_first[blockIdx.x] = agg < after ? agg : after;
+#pragma unroll
+  for (int k = 0; k < kRunPer; k++) {
+    const int64_t p = base + k;
+    if (p < n) run_end[p] = v[k] < after ? v[k] : after;
+  }
+}
+
+__global__ void k_run_ends_fix(int64_t n, uint32_t* __restrict__ run_end, const uint32_t* __restrict__ tile_first,
+                               int64_t ntiles, const Scalars* sc) {
+  if (!sc->has_runs || sc->err) return;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n || run_end[p] != 0xFFFFFFFFu) return;
+  uint32_t r = 0xFFFFFFFFu;
+  for (int64_t tl = p / kRunTile + 1; tl < ntiles && r == 0xFFFFFFFFu; tl++) r = tile_first[tl];
+  run_end[p] = r == 0xFFFFFFFFu ? (uint32_t)(n - 1) : r;
+}
+
 static cudaError_t run_ends(Workspace& ws, int64_t n, cudaStream_t s) {
-  size_t bytes = ws.cub_bytes;
-  thrust::reverse_iterator<const uint32_t*> in(ws.aux2 + n);
-  thrust::reverse_iterator<uint32_t*> out(ws.seg + n);
-  cudaError_t e = cub::DeviceScan::InclusiveScan(ws.cub_tmp, bytes, in, out, cub::Min(), (int)n, s);
+  // tile_first lives in ws.rrow: the metadata pass that fills rrow runs after both kernels
+  const int64_t ntiles = (n + kRunTile - 1) / kRunTile;
+  k_run_ends_tile<<<(unsigned)ntiles, kRunThreads, 0, s>>>(ws.aux2, n, ws.seg, ws.rrow, ws.sc);
+  k_run_ends_fix<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, ws.seg, ws.rrow, ntiles, ws.sc);
   g_launches += 2;
-  return e ? e : cudaGetLastError();
+  return cudaGetLastError();
 }
 
 cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, Workspace& ws,
@@ -1081,9 +1178,11 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       }
       int64_t tb = (n + kTpsThreads - 1) / kTpsThreads;
       const int64_t tcap = (int64_t)num_sms * 2;  // one resident wave
+      if (!ws.lwtab && (e = grow(ws.lwtab, tcap * kTpsThreads * kSlots))) return e;  // 128 entries per thread
       if (tb > tcap) tb = tcap;
       fn<<<(unsigned)(tb < 1 ? 1 : tb), kTpsThreads, smem, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, recs, n, n,
-                                                               ws.vrow, ws.rrow, ws.rsrc);
+                                                               ws.vrow, ws.rrow, ws.rsrc,
+                                                               ws.lwtab);
       ktimer_end("apply", s);
       g_launches++;
     } else {
