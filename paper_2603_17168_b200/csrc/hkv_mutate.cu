@@ -656,7 +656,7 @@ __device__ __forceinline__ void tps_segment(const TableDev& t, const OpArgs& a, 
       nk = skeys[q + 1];
       qe = runs ? (int64_t)run_end[q] : q;
     }
-    if (!S.tab && q - S.p0 >= kLwScan) lw_fill(S, q, run_end, runs);
+    if (OP != kOpErase && !S.tab && q - S.p0 >= kLwScan) lw_fill(S, q, run_end, runs);  // erase writes no rows
     const int res = tps_op<OP, COLLECT>(t, a, S, b, i, key, d, clock0, fel_open, q, vrow, rrow, rsrc,
                                         ctr, sd, fe_min);
     if (nb_ != (uint32_t)b) break;
