@@ -65,6 +65,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--quick", action="store_true", help="2^24 slots, for profiling runs")
+    p.add_argument("--force-sharded", action="store_true",
+                   help="run the sharded (multi-GPU) path even at world size 1 (launch under torchrun)")
     a = p.parse_args()
     if a.quick:
         a.capacity = 2**24
@@ -568,12 +570,22 @@ def run_sharded(a, rank, world):
 
     queries = [present_keys(q) for q in qidx]
     ins = [W.uniform_distinct_keys_torch(B, 0, stream_offset=2**44 + (s * world + rank) * B) for s in range(n_steps)]
-    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    ev_pool = [torch.cuda.Event(enable_timing=True) for _ in range(3 * n_steps)]
+    for e in ev_pool:
+        e.record()
+    torch.cuda.synchronize()
+    clocks = Clocks(local_rank) if rank == 0 else None
+    if clocks is not None:
+        clocks.start()
+        clocks.wait_first_sample()
     times = []
+    launches0 = 0
     for s in range(n_steps):
+        if s == a.warmup:
+            launches0 = lib.hkv_launch_count()
         dist.barrier()
         torch.cuda.synchronize()
-        e0, e1, e2 = ev(), ev(), ev()
+        e0, e1, e2 = ev_pool.pop(), ev_pool.pop(), ev_pool.pop()
         e0.record()
         f, v = t.find(queries[s])
         e1.record()
@@ -584,21 +596,57 @@ def run_sharded(a, rank, world):
         if s >= a.warmup:
             times.append((e0.elapsed_time(e1), e1.elapsed_time(e2)))
             assert bool(f.all())
+    launches = lib.hkv_launch_count() - launches0
+    clk = clocks.stop() if clocks is not None else None
+    # device time of the step (the routing's split exchange synchronises the host, so the
+    # pairs include it): mean over steps, max over ranks
     step_ms = torch.tensor([sum(x[0] + x[1] for x in times) / len(times)], device="cuda")
     find_ms = torch.tensor([sum(x[0] for x in times) / len(times)], device="cuda")
     dist.all_reduce(step_ms, op=dist.ReduceOp.MAX)
     dist.all_reduce(find_ms, op=dist.ReduceOp.MAX)
+    # e2e through the public API: pinned host keys/values in, host results out
+    e2e = None
+    if not a.no_e2e:
+        hq = [q.cpu().pin_memory() for q in queries[: a.steps]]
+        hk = [k.cpu().pin_memory() for k in ins[: a.steps]]
+        hv = vals.cpu().pin_memory()
+        fh = torch.empty(B, dtype=torch.bool, pin_memory=True)
+        vh = torch.empty((B, dim), dtype=torch.float32, pin_memory=True)
+        oh = torch.empty(B, dtype=torch.uint8, pin_memory=True)
+        wall = 0.0
+        for s in range(a.steps + 1):
+            dist.barrier()
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
+            f, v = t.find(hq[s % a.steps].cuda(non_blocking=True))
+            fh.copy_(f, non_blocking=True)
+            vh.copy_(v, non_blocking=True)
+            o = t.insert_or_assign(hk[s % a.steps].cuda(non_blocking=True), hv.cuda(non_blocking=True))
+            oh.copy_(o, non_blocking=True)
+            torch.cuda.synchronize()
+            w1 = time.perf_counter()
+            t.local.restore()
+            if s > 0:
+                wall += w1 - w0
+        wt = torch.tensor([wall / a.steps], device="cuda")
+        dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * 2 * B / wt.item() / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 2 * B * 8 + B * dim * 4, "d2h_bytes_per_step": B + B * dim * 4 + B}
     if rank == 0:
         value = world * 2 * B / (step_ms.item() / 1e3) / 1e9
         line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": round(step_ms.item(), 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u64 keys, f32 values",
-                "data": "synthetic", "config": {"workload": f"hash-sharded table {cap} slots over {world} GPUs "
-                                                            "(contiguous bucket ranges), dim 64, lambda 0.5; "
-                                                            "per rank find 1M + insert_or_assign 1M",
-                                                "capacity_per_gpu": cap_local, "batch_per_gpu": B},
+                "data": "synthetic (uniform_distinct_keys fill; resident-key queries; fresh-key inserts)",
+                "config": {"workload": f"hash-sharded table {cap} slots over {world} GPUs "
+                                       "(contiguous bucket ranges, NCCL all-to-all routing), dim 64, lambda 0.5; "
+                                       "per rank and step: find 1M resident keys + insert_or_assign 1M fresh keys",
+                           "capacity_per_gpu": cap_local, "batch_per_gpu": B,
+                           "l2": "inputs larger than L2 (34 GB per GPU); metadata restore between steps",
+                           "timing": "CUDA events per op on each rank (host-synchronising split exchange "
+                                     "included), mean over steps, max over ranks"},
                 "find_bkvs_aggregate": round(world * B / (find_ms.item() / 1e3) / 1e9, 4),
-                "gpu_launches": int(lib.hkv_launch_count())}
+                "clocks": clk, "gpu_launches": int(launches), "e2e": e2e}
         print(json.dumps(line), flush=True)
 
 
@@ -606,7 +654,8 @@ def main():
     a = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if world > 1:
+    sharded = world > 1 or a.force_sharded
+    if sharded:
         import torch.distributed as dist
 
         backend = "gloo" if a.impl == "reference" else "nccl"
@@ -617,11 +666,11 @@ def main():
         dist.init_process_group(backend)
     if a.impl == "reference":
         run_reference_arm(a, rank, world)
-    elif world > 1:
+    elif sharded:
         run_sharded(a, rank, world)
     else:
         run_single(a)
-    if world > 1:
+    if sharded:
         import torch.distributed as dist
 
         dist.barrier()
