@@ -523,6 +523,53 @@ class CacheTable:
     def reset_counters(self) -> None:
         _lib.check(self._lib.hkv_reset_counters(self._h, self._sp()))
 
+    # ----- checkpoint (the reference streams export_batch_if
+    # "for checkpointing", but has no restore) --
+    CHECKPOINT_VERSION = 1
+
+    def save_checkpoint(self, path) -> None:
+        """Write the table's exact state (slot positions, stale erased
+        entries, scores, values, size, logical clock, epoch, first-eviction
+        lambda) to one uncompressed .npz file; load_checkpoint restores it
+        bit-for-bit, so every later op behaves as on the original table.
+        TxnCounters are not part of the state."""
+        st = self.export_state()
+        c = self.config
+        header = {"version": self.CHECKPOINT_VERSION, "capacity": c.capacity, "value_dim": c.value_dim,
+                  "mode": c.mode.value, "score_policy": c.score_policy.value,
+                  "fast_tier_budget": c.fast_tier_budget, "digest_filter": bool(c.digest_filter),
+                  "admit_ties_unified": bool(c.admit_ties_unified), "epoch": int(self.epoch.current_epoch),
+                  "clock": int(st["clock"]), "size": int(st["size"]),
+                  "first_eviction_lambda": st["fel"]}
+        import json
+
+        with open(path, "wb") as f:
+            np.savez(f, header=np.frombuffer(json.dumps(header).encode(), dtype=np.uint8), keys=st["keys"],
+                     digests=st["digests"], scores=st["scores"], values=st["values"])
+
+    @classmethod
+    def load_checkpoint(cls, path, device: Optional[int] = None, overflow_in_hbm: bool = False) -> "CacheTable":
+        """Create a table from save_checkpoint's file (same configuration,
+        same bytes)."""
+        import json
+
+        with np.load(path) as z:
+            h = json.loads(bytes(z["header"]).decode())
+            if h.get("version") != cls.CHECKPOINT_VERSION:
+                raise ValueError("unsupported checkpoint version")
+            cfg = TableConfig(capacity=h["capacity"], value_dim=h["value_dim"], mode=h["mode"],
+                              score_policy=h["score_policy"], fast_tier_budget=h["fast_tier_budget"],
+                              digest_filter=h["digest_filter"], admit_ties_unified=h["admit_ties_unified"],
+                              device=device, overflow_in_hbm=overflow_in_hbm)
+            t = cls(cfg)
+            t.import_state(z["keys"], z["digests"], z["scores"], z["values"], clock=h["clock"],
+                           first_eviction_lambda=h["first_eviction_lambda"])
+        if h["epoch"]:
+            t.set_epoch(h["epoch"])
+        if t.size() != h["size"]:
+            raise ValueError("checkpoint size does not match its keys")
+        return t
+
     # ----- raw state (test / checkpoint support) -----------------------------
     def export_state(self) -> dict:
         """Host copy of the raw arrays in the reference layout (table.py:143-146)."""
