@@ -1,6 +1,8 @@
 // hkv_misc.cu — export_batch_if, state import support, consistency scan and
 // the sharding router.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "hkv_kernels.h"
 #include "hkv_probe.cuh"
@@ -61,9 +63,9 @@ cudaError_t run_export(const TableDev& t, int64_t cursor, int64_t max_count, int
   long long* nsel = &ws.sc->n_sel;
   while (pos < end && taken < max_count) {
     const int64_t len = (end - pos) < kChunk ? (end - pos) : kChunk;
-    cub::CountingInputIterator<int64_t> cnt(0);
+    thrust::counting_iterator<int64_t> cnt(0);
     ExportFlag f{t.keys, t.scores, mask, pos, cursor, has_min, min_score};
-    cub::TransformInputIterator<bool, ExportFlag, cub::CountingInputIterator<int64_t>> fl(cnt, f);
+    thrust::transform_iterator<ExportFlag, thrust::counting_iterator<int64_t>, bool> fl(cnt, f);
     size_t bytes = ws.cub_bytes;
     if ((e = cub::DeviceSelect::Flagged(ws.cub_tmp, bytes, cnt, fl, ws.aux, nsel, (int)len, s))) return e;
     g_launches += 2;

@@ -22,6 +22,8 @@
 // bucket, argmin over the score row through the group summary, admission
 // test and eviction (_finish_admission, table.py:1121-1163).
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 #include <cstdlib>
 #include <string>
 #include <thrust/iterator/reverse_iterator.h>
@@ -234,26 +236,6 @@ __device__ __forceinline__ void setbit128(uint32_t (&m)[4], int s) {
   const uint32_t bit = 1u << (s & 31);
 #pragma unroll
   for (int w = 0; w < 4; w++) m[w] |= bit & eqmask(w, s >> 5);
-}
-__device__ __forceinline__ void clrbit128(uint32_t (&m)[4], int s) {
-  const uint32_t bit = 1u << (s & 31);
-#pragma unroll
-  for (int w = 0; w < 4; w++) m[w] &= ~(bit & eqmask(w, s >> 5));
-}
-__device__ __forceinline__ void set_line_byte(uint4 (&dg)[8], int s, uint32_t d) {
-  const int j = s & 15;
-  const uint32_t sh = (uint32_t)(j & 3) * 8u;
-  const uint32_t bm = 0xFFu << sh, bv = (d & 0xFFu) << sh;
-#pragma unroll
-  for (int k = 0; k < 8; k++) {
-    const uint32_t on = eqmask(k, s >> 4);
-    const uint32_t mx = bm & on & eqmask(j >> 2, 0), my = bm & on & eqmask(j >> 2, 1);
-    const uint32_t mz = bm & on & eqmask(j >> 2, 2), mw = bm & on & eqmask(j >> 2, 3);
-    dg[k].x = (dg[k].x & ~mx) | (bv & mx);
-    dg[k].y = (dg[k].y & ~my) | (bv & my);
-    dg[k].z = (dg[k].z & ~mz) | (bv & mz);
-    dg[k].w = (dg[k].w & ~mw) | (bv & mw);
-  }
 }
 __device__ __forceinline__ uint64_t eqmask64(int a, int b) { return 0ull - (uint64_t)(a == b); }
 __device__ __forceinline__ uint64_t sel8(const uint64_t (&a)[8], int g) {
@@ -1023,10 +1005,10 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual
     size_t b_sort = 0, b_sel = 0, b_scan = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b_sort, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                     (uint32_t*)nullptr, (int)ws.cap_n, 0, 32);
-    cub::CountingInputIterator<int64_t> cnt(0);
-    cub::TransformInputIterator<bool, IsEvicted, cub::CountingInputIterator<int64_t>> fl(cnt, IsEvicted{nullptr});
+    thrust::counting_iterator<int64_t> cnt(0);
+    thrust::transform_iterator<IsEvicted, thrust::counting_iterator<int64_t>, bool> fl(cnt, IsEvicted{nullptr});
     cub::DeviceSelect::Flagged(nullptr, b_sel, cnt, fl, (uint32_t*)nullptr, (long long*)nullptr, (int)ws.cap_n);
-    cub::TransformInputIterator<uint32_t, IsUpdated, cub::CountingInputIterator<int64_t>> up(cnt,
+    thrust::transform_iterator<IsUpdated, thrust::counting_iterator<int64_t>, uint32_t> up(cnt,
                                                                                             IsUpdated{nullptr});
     cub::DeviceScan::ExclusiveSum(nullptr, b_scan, up, (uint32_t*)nullptr, (int)ws.cap_n);
     size_t b_min = 0;
@@ -1196,8 +1178,8 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
   long long* nev = reinterpret_cast<long long*>(n_evicted);
   if (collect && n > 0) {
     size_t bytes = ws.cub_bytes;
-    cub::CountingInputIterator<int64_t> cnt(0);
-    cub::TransformInputIterator<bool, IsEvicted, cub::CountingInputIterator<int64_t>> fl(cnt, IsEvicted{a.outcomes});
+    thrust::counting_iterator<int64_t> cnt(0);
+    thrust::transform_iterator<IsEvicted, thrust::counting_iterator<int64_t>, bool> fl(cnt, IsEvicted{a.outcomes});
     if ((e = cub::DeviceSelect::Flagged(ws.cub_tmp, bytes, cnt, fl, ws.aux, nev, (int)n, s))) return e;
     g_launches += 2;
   }
@@ -1267,8 +1249,8 @@ cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* val
     g_launches++;
     if (need_ticks) {
       size_t bytes = ws.cub_bytes;
-      cub::CountingInputIterator<int64_t> cnt(0);
-      cub::TransformInputIterator<uint32_t, IsUpdated, cub::CountingInputIterator<int64_t>> up(cnt,
+      thrust::counting_iterator<int64_t> cnt(0);
+      thrust::transform_iterator<IsUpdated, thrust::counting_iterator<int64_t>, uint32_t> up(cnt,
                                                                                               IsUpdated{outcomes});
       if ((e = cub::DeviceScan::ExclusiveSum(ws.cub_tmp, bytes, up, ws.aux2, (int)n, s))) return e;
       g_launches += 2;
