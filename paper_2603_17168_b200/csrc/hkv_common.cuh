@@ -11,7 +11,8 @@
 //   scores  [B][128] u64  8 lines per bucket (read only on full-bucket decisions)
 //   smin    [B][8]   u64  eviction summary: min score of each 16-slot group, so
 //   svalid  [B]      u32  a full-bucket argmin reads 64 B + one group's 128 B
-//                         instead of the 1-KB score row (bit g: group g exact)
+//                         instead of the 1-KB score row (bit g: group g exact;
+//                         only meaningful while the bucket is full)
 //   values  rows [capacity][dim] f32: rows < fast_rows in HBM, the rest in the
 //           overflow arena (mapped pinned host memory, or HBM)
 #pragma once

@@ -438,7 +438,20 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
       S.O[s >> 5] = o;
       t.bits[b * 4 + (s >> 5)] = o;
       reinterpret_cast<uint8_t*>(S.L)[s] = (uint8_t)d;
-      tps_score_written(t, b, S, s, s_in);
+      // The summary is only consulted while the bucket is full, so a free
+      // insert leaves it alone unless it fills the bucket: then every group
+      // is marked unknown at once (the next full decision rescans).  This
+      // keeps a scattered atomic off ~all inserts below lambda = 1.
+      if (occ_total + 1 == kSlots) {
+        if (S.sloaded) {
+          if (S.sv) {
+            S.sv = 0;
+            S.svdirty = true;
+          }
+        } else {
+          atomicAnd(t.svalid + b, 0u);
+        }
+      }
       wslot = s;
       outcome = kInserted;
       sd++;
