@@ -53,23 +53,18 @@ __global__ void k_prep(TableDev t, const uint64_t* __restrict__ keys, int64_t n,
 }
 
 // ---------------------------------------------------------------------------
-// Single mode, metadata pass.  One 8-lane tile per bucket segment, ops in
-// batch order.  Only metadata is touched here (digest line, occupancy bits,
-// candidate keys, score row); value rows move in separate streaming kernels
-// (k_values_read / k_values_write) that have far more memory-level
-// parallelism than a tile walking its serial chain.  To stay bit-exact the
-// pass records, per op:
+// Single mode value plan.  The metadata pass (k_meta_tps) touches only digest
+// lines, occupancy bits, candidate keys and scores; value rows move in
+// separate streaming kernels (k_values_read / k_values_write) that have far
+// more memory-level parallelism than a thread walking its serial chain.  To
+// stay bit-exact the pass records, per op:
 //   vrow[i]  destination row when op i is the LAST writer of that row in its
 //            segment (a later writer of the same slot retires the earlier one)
 //   rrow[i], rsrc[i]  for value reads (find_or_insert hits, insert_and_evict
 //            victims): the row, and the op whose input currently sits in that
 //            row (-1 = the row's content before the batch)
-// "Last writer of a slot in the current segment" lives in shared memory,
-// tagged with a per-segment generation so no per-segment reset is needed.
-//
-// Warp-synchronous: a warp's four tiles advance in lockstep (a tile whose
-// segment is exhausted idles), every collective uses the full warp mask and
-// outcome branches are predicates, so no divergent-collective emulation.
+// The last writer of a slot comes from a short scan back through the
+// segment, or from a per-thread table once a segment is long (lw_get).
 // ---------------------------------------------------------------------------
 constexpr uint32_t kNoRow = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xFFFFFFFFu;
