@@ -779,7 +779,9 @@ __global__ void __launch_bounds__(256) k_values_write(TableDev t, const float* _
 // content (rsrc < 0) or the input of the op that wrote it earlier in the batch.
 //   list == nullptr: find_or_insert hits -> values[i] for outcome Found
 //   list != nullptr: insert_and_evict victims, j-th evicted op -> ev[j], ek/es
-template <int VEC>
+// KPT reads per tile, two 16-B vectors per read and lane in flight (as in
+// k_values_write).
+template <int VEC, int KPT>
 __global__ void __launch_bounds__(256) k_values_read(TableDev t, float* __restrict__ values,
                                                      const uint8_t* __restrict__ outcomes,
                                                      const uint32_t* __restrict__ rrow,
@@ -788,30 +790,58 @@ __global__ void __launch_bounds__(256) k_values_read(TableDev t, float* __restri
                                                      const uint64_t* __restrict__ es_tmp, uint64_t* ek, uint64_t* es,
                                                      float* ev, int64_t n, const Scalars* sc) {
   if (sc->err) return;
+  using V = typename std::conditional<VEC == 4, uint4, typename std::conditional<VEC == 2, float2, float>::type>::type;
   const Tile8 tile;
   const int r = tile.thread_rank();
   const int64_t tid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
   const int64_t ntiles = (int64_t)gridDim.x * blockDim.x / kG;
   const int dim = t.dim;
+  const int nv = dim / VEC;
   const int64_t m = list ? (int64_t)*n_list : n;
-  for (int64_t j = tid; j < m; j += ntiles) {
-    uint32_t i;
-    float* dst;
-    if (list) {
-      i = list[j];
-      dst = ev + j * (int64_t)dim;
-      if (r == 0) {
-        ek[j] = ek_tmp[i];
-        es[j] = es_tmp[i];
+  for (int64_t base = tid * KPT; base < m; base += ntiles * KPT) {
+    const V* from[KPT];
+    V* dst[KPT];
+#pragma unroll
+    for (int u = 0; u < KPT; u++) {
+      const int64_t j = base + u;
+      from[u] = nullptr;
+      dst[u] = nullptr;
+      if (j >= m) continue;
+      uint32_t i;
+      if (list) {
+        i = list[j];
+        dst[u] = reinterpret_cast<V*>(ev + j * (int64_t)dim);
+        if (r == 0) {
+          ek[j] = ek_tmp[i];
+          es[j] = es_tmp[i];
+        }
+      } else {
+        i = (uint32_t)j;
+        if (outcomes[i] != kFound) continue;
+        dst[u] = reinterpret_cast<V*>(values + (uint64_t)i * dim);
       }
-    } else {
-      i = (uint32_t)j;
-      if (outcomes[i] != kFound) continue;
-      dst = values + (uint64_t)i * dim;
+      const int32_t src = rsrc[i];
+      from[u] = reinterpret_cast<const V*>(src < 0 ? value_row(t, rrow[i]) : values + (uint64_t)src * dim);
     }
-    const int32_t src = rsrc[i];
-    const float* from = src < 0 ? value_row(t, rrow[i]) : values + (uint64_t)src * dim;
-    copy_row<kG, VEC>(dst, from, dim, r);
+    for (int e0 = r; e0 < nv; e0 += kG * 2) {
+      V x[KPT][2];
+#pragma unroll
+      for (int u = 0; u < KPT; u++) {
+#pragma unroll
+        for (int w = 0; w < 2; w++) {
+          const int e = e0 + w * kG;
+          if (from[u] && e < nv) x[u][w] = ld_vec(from[u] + e);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < KPT; u++) {
+#pragma unroll
+        for (int w = 0; w < 2; w++) {
+          const int e = e0 + w * kG;
+          if (from[u] && e < nv) st_vec(dst[u] + e, x[u][w]);
+        }
+      }
+    }
   }
 }
 
@@ -1197,14 +1227,18 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
     const int vr = vec_of(t.dim, a.values, t.vfast, t.vover, collect ? ev_out : nullptr);
     if (collect || a.op == kOpFindOrInsert) {
       const uint32_t* list = collect ? ws.aux : nullptr;
+      int64_t rblocks = (((n + 3) / 4) * kG + 255) / 256;
+      const int64_t rcap = (int64_t)num_sms * 8 * 4;
+      if (rblocks > rcap) rblocks = rcap;
+      if (rblocks < 1) rblocks = 1;
       if (vr == 4)
-        k_values_read<4><<<(unsigned)vblocks, 256, 0, s>>>(t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
+        k_values_read<4, 4><<<(unsigned)rblocks, 256, 0, s>>>(t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
                                                            ws.ek, ws.es, ek_out, es_out, ev_out, n, ws.sc);
       else if (vr == 2)
-        k_values_read<2><<<(unsigned)vblocks, 256, 0, s>>>(t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
+        k_values_read<2, 4><<<(unsigned)rblocks, 256, 0, s>>>(t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
                                                            ws.ek, ws.es, ek_out, es_out, ev_out, n, ws.sc);
       else
-        k_values_read<1><<<(unsigned)vblocks, 256, 0, s>>>(t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
+        k_values_read<1, 4><<<(unsigned)rblocks, 256, 0, s>>>(t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
                                                            ws.ek, ws.es, ek_out, es_out, ev_out, n, ws.sc);
       g_launches++;
     }
