@@ -29,31 +29,97 @@ namespace hkv {
 // ---------------------------------------------------------------------------
 // per-op processor (one 8-lane tile, exclusive ownership of the op's buckets)
 // ---------------------------------------------------------------------------
+// The op's input row, loaded before the op waits for its buckets (it does not
+// depend on the table): up to kPreVec 16-B vectors per lane, i.e. dim <= 64.
+constexpr int kPreVec = 2;
+struct InRow {
+  uint4 v[kPreVec];
+  bool ok;  // the row fits (VEC == 4, dim / 4 <= kPreVec * kG)
+};
+template <int VEC>
+__device__ __forceinline__ InRow prefetch_row(const float* vin, int dim, int r) {
+  InRow p;
+  p.ok = VEC == 4 && dim / 4 <= kPreVec * kG;
+  if (p.ok) {
+    const uint4* s = reinterpret_cast<const uint4*>(vin);
+#pragma unroll
+    for (int u = 0; u < kPreVec; u++) {
+      const int e = r + u * kG;
+      if (e < dim / 4) p.v[u] = s[e];
+    }
+  }
+  return p;
+}
+template <int VEC>
+__device__ __forceinline__ void write_row(float* dst, const float* vin, const InRow& p, int dim, int r) {
+  if (p.ok) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int u = 0; u < kPreVec; u++) {
+      const int e = r + u * kG;
+      if (e < dim / 4) d[e] = p.v[u];
+    }
+  } else {
+    copy_row<kG, VEC>(dst, vin, dim, r);
+  }
+}
+
+// probe_bucket with the lane's digest slice already loaded
+__device__ __forceinline__ int probe_loaded(const TableDev& t, const Tile8& tile, uint64_t b, uint64_t key,
+                                            uint32_t d, uint4 dw, uint32_t occ, ctr_t& n_compares) {
+  const int r = tile.thread_rank();
+  uint32_t cand = (t.digest_filter ? match16(dw, d) : 0xFFFFu) & occ;
+  const uint64_t* kp = t.keys + b * kSlots + r * kSPL;
+  int hit = -1, ncmp = 0, ncmp_all = 0;
+  while (cand) {
+    const int j = __ffs(cand) - 1;
+    cand &= cand - 1;
+    ncmp_all++;
+    if (kp[j] == key) {
+      hit = r * kSPL + j;
+      ncmp = ncmp_all;
+      break;
+    }
+  }
+  const uint32_t hm = tile.ballot(hit >= 0);
+  int slot = -1, contrib = ncmp_all;
+  if (hm) {
+    const int hl = __ffs(hm) - 1;
+    slot = tile.shfl(hit, hl);
+    contrib = r < hl ? ncmp_all : (r == hl ? ncmp : 0);
+  }
+  n_compares += tile.sum((unsigned)contrib);
+  return slot;
+}
+
 template <int VEC>
 __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
                                            const Tile8& tile, uint32_t i,
                                            uint64_t clock0, bool fel_open, ctr_t* ctr,
-                                           int& size_delta) {
+                                           int& size_delta, const InRow& pre) {
   const int r = tile.thread_rank();
   const int dim = t.dim;
   const uint64_t key = a.keys[i];
   const uint64_t h = fmix64(key);
   const uint32_t d = digest_of(h);
   const uint64_t b1 = h & t.mask;
+  const uint64_t b2 = t.dual ? second_hash(h) & t.mask : b1;
   uint64_t hb = b1;
+  // both buckets' digest slices and occupancy in one round trip
+  const uint4 dw1 = reinterpret_cast<const uint4*>(t.digests + b1 * kSlots)[r];
   const uint32_t occ1 = load_occ(t, b1, r);
-  int slot = probe_bucket<true, false>(t, tile, b1, key, d, occ1, ctr[kCompares]);
-  ctr[kLoads]++;
-  uint64_t b2 = b1;
+  uint4 dw2 = dw1;
   uint32_t occ2 = occ1;
   if (t.dual) {
-    b2 = second_hash(h) & t.mask;
-    if (slot < 0) {
-      occ2 = load_occ(t, b2, r);
-      slot = probe_bucket<true, false>(t, tile, b2, key, d, occ2, ctr[kCompares]);
-      ctr[kLoads]++;
-      hb = b2;
-    }
+    dw2 = reinterpret_cast<const uint4*>(t.digests + b2 * kSlots)[r];
+    occ2 = load_occ(t, b2, r);
+  }
+  int slot = probe_loaded(t, tile, b1, key, d, dw1, occ1, ctr[kCompares]);
+  ctr[kLoads]++;
+  if (t.dual && slot < 0) {
+    slot = probe_loaded(t, tile, b2, key, d, dw2, occ2, ctr[kCompares]);
+    ctr[kLoads]++;
+    hb = b2;
   }
   uint8_t outcome;
   if (a.op == kOpErase) {
@@ -89,7 +155,7 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
       copy_row<kG, VEC>(vin, vr, dim, r);
       outcome = kFound;
     } else {
-      copy_row<kG, VEC>(vr, vin, dim, r);
+      write_row<VEC>(vr, vin, pre, dim, r);
       outcome = kUpdated;
     }
     ctr[row < t.fast_rows ? kVFast : kVOver]++;
@@ -149,7 +215,7 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
     }
     s = tile.shfl(s, fl);
     const uint64_t row = tb * kSlots + s;
-    copy_row<kG, VEC>(value_row(t, row), vin, dim, r);
+    write_row<VEC>(value_row(t, row), vin, pre, dim, r);
     ctr[row < t.fast_rows ? kVFast : kVOver]++;
     size_delta++;
     outcome = kInserted;
@@ -173,7 +239,7 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
       t.scores[row] = s_in;
       summ_invalidate(t, tb, m);
     }
-    copy_row<kG, VEC>(vr, vin, dim, r);
+    write_row<VEC>(vr, vin, pre, dim, r);
     ctr[row < t.fast_rows ? kVFast : kVOver]++;
     outcome = kEvicted;
     if (fel_open && r == 0) atomicMin(&a.sc->first_ev, i);
@@ -250,13 +316,16 @@ __global__ void __launch_bounds__(256) k_dual_flow(TableDev t, OpArgs a, const u
     if (r == 0) i = atomicAdd(next, 1u);
     i = tile.shfl(i, 0);
     if ((int64_t)i >= n) break;
+    InRow pre;  // the input row does not depend on the table: load it before waiting
+    pre.ok = false;
+    if (a.values) pre = prefetch_row<VEC>(a.values + (uint64_t)i * t.dim, t.dim, r);
     const uint32_t b1 = b1s[i], b2 = b2s[i];
     const uint32_t r1 = rank[2 * i];
     const uint32_t r2 = b2 == b1 ? 0u : rank[2 * i + 1];
     // every lane acquires: the bucket data it reads next was published with a release
     if (r1) while (ld_acquire_u64(turn + b1) < (tag | r1)) __nanosleep(32);
     if (b2 != b1 && r2) while (ld_acquire_u64(turn + b2) < (tag | r2)) __nanosleep(32);
-    process_op<VEC>(t, a, tile, i, clock0, fel_open, ctr, sd);
+    process_op<VEC>(t, a, tile, i, clock0, fel_open, ctr, sd, pre);
     __threadfence();
     tile.sync();
     if (r == 0) {
