@@ -255,8 +255,9 @@ def test_full_size_properties_dim64(hkv):
     assert res.numel() == t.size()
 
 
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("policy", POLICIES)
-def test_zipf_same_key_runs(hkv, policy):
+def test_zipf_same_key_runs(hkv, policy, mode):
     """Zipf batches (alpha 0.99, small universe): one key fills thousands of
     consecutive sorted positions of its bucket, so the collapsed same-key
     runs (hits, rejections under Lfu, erase misses, find_or_insert reads) are
@@ -264,8 +265,8 @@ def test_zipf_same_key_runs(hkv, policy):
     from paper_2603_17168_b200.workloads import zipf_keys
 
     cap, dim = 128 * 32, 4
-    t = make_table(hkv, cap, dim, policy=policy)
-    o = OracleTable(cap, dim, "single", policy)
+    t = make_table(hkv, cap, dim, mode, policy=policy)
+    o = OracleTable(cap, dim, mode, policy)
     rng = np.random.default_rng(11)
     custom = policy == "kCustomized"
     for j in range(14):
