@@ -104,6 +104,24 @@ int hkv_upsert(hkv_table *t, int32_t op, const uint64_t *keys, float *values,
                float *evicted_values, uint64_t *evicted_scores, int64_t *n_evicted_dev,
                const uint64_t *ticks, uint64_t clock_advance, hkv_stream stream);
 
+/* Host-buffer entry points: the same operations on HOST arrays (the
+ * reference's numpy-in / numpy-out contract, table.py:304-323 and 515-551).
+ * Pinned (page-locked) buffers get full PCIe bandwidth; pageable ones work
+ * but stage through the driver.  The call is SYNCHRONOUS: it returns once
+ * every output is in host memory.  Internally the batch is pipelined:
+ *   hkv_find_host    probes chunk c+1 while chunk c's rows stream back (D2H);
+ *   hkv_upsert_host  copies the value rows H2D on a second stream while the
+ *                    metadata pass (which needs only the keys) runs; the value
+ *                    scatter waits for that copy.
+ * op: HKV_OP_INSERT_OR_ASSIGN, or HKV_OP_FIND_OR_INSERT (values in/out: the
+ * rows of found keys are copied back).  ticks as in hkv_upsert (host array
+ * or NULL). */
+int hkv_find_host(hkv_table *t, const uint64_t *keys, int64_t n, float *out, uint8_t *found,
+                  int32_t zero_misses, hkv_stream stream);
+int hkv_upsert_host(hkv_table *t, int32_t op, const uint64_t *keys, float *values,
+                    const uint64_t *scores, int64_t n, uint8_t *outcomes, const uint64_t *ticks,
+                    uint64_t clock_advance, hkv_stream stream);
+
 /* assign (table.py:438-442) when values != NULL; assign_scores (444-449) with
  * explicit scores (kCustomized) or refresh != 0.  Last duplicate wins.
  * Refresh ticks: NULL -> clock + (found keys before i) + 1 and clock += found
@@ -176,7 +194,9 @@ int64_t hkv_launch_count(void);
  * kernel of each op (probe / apply / assign-apply) is bracketed by CUDA
  * events on its launch stream.  hkv_kernel_times() synchronises, returns the
  * accumulated milliseconds and launch count of the kernel named `name`
- * ("find", "apply", "dual_rounds", "assign_apply") and resets it. */
+ * ("find", "find_gather", "apply", "values_write", "dual_flow", "assign_apply")
+ * and resets it.  enable = 2 also brackets the mutation pipeline's stages
+ * ("prep", "sort", "segments", "finalize"; more events, so not for bench). */
 int hkv_set_kernel_timing(int32_t enable);
 int hkv_kernel_times(const char *name, double *ms, int64_t *launches);
 

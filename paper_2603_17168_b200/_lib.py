@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhkv_b200.so")
+LIB_PATH = os.environ.get("HKV_LIB") or os.path.join(_HERE, "libhkv_b200.so")  # HKV_LIB: experiment builds
 
 HKV_OK, HKV_EINVAL, HKV_ECUDA, HKV_ENOMEM = 0, 1, 2, 3
 
@@ -45,6 +45,8 @@ SIGNATURES = {
     "hkv_contains": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "hkv_find_ptr": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "hkv_upsert": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _u64, _vp]),
+    "hkv_find_host": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _i32, _vp]),
+    "hkv_upsert_host": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _u64, _vp]),
     "hkv_assign": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _u64, _vp]),
     "hkv_erase": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "hkv_export": (C.c_int, [_vp, _i64, _i64, _i32, _u64, _vp, _i64, _vp, _vp, _vp,

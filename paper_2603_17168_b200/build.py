@@ -6,6 +6,7 @@
 from __future__ import annotations
 
 import glob
+import concurrent.futures
 import os
 import subprocess
 import sys
@@ -23,6 +24,8 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompil
 # per-file extra flags: the dual-mode dataflow hands buckets between SMs
 # through acquire/release turn counters, so its global loads bypass L1
 EXTRA = {"hkv_dual.cu": ["-Xptxas", "-dlcm=cg"]}
+# experiments: extra nvcc flags for every file (e.g. HKV_NVCC_EXTRA="-DHKV_TPS_MINB=3")
+FLAGS += os.environ.get("HKV_NVCC_EXTRA", "").split()
 
 
 def sources():
@@ -46,19 +49,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(HERE, "_obj")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for src in sources():
+    def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, *EXTRA.get(os.path.basename(src), []), "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed for {src}")
-        if verbose:
-            sys.stderr.write(r.stderr)
-        with open(obj + ".ptxas.txt", "w") as f:
-            f.write(r.stderr)
-        objs.append(obj)
+        return src, obj, r
+
+    objs = []
+    # one nvcc per translation unit, in parallel
+    with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1))) as ex:
+        for src, obj, r in ex.map(compile_one, sources()):
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed for {src}")
+            if verbose:
+                sys.stderr.write(r.stderr)
+            with open(obj + ".ptxas.txt", "w") as f:
+                f.write(r.stderr)
+            objs.append(obj)
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)

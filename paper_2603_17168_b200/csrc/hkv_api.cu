@@ -20,6 +20,7 @@ namespace {
 struct KTimer {
   std::mutex mu;
   bool enabled = false;
+  int level = 0;  // 1: the per-kernel regions bench.py reads; 2: also pipeline stages (tools/stage_times.py)
   struct Pending {
     std::string name;
     cudaEvent_t a, b;
@@ -47,10 +48,10 @@ KTimer& ktimer() {
 }
 }  // namespace
 
-void ktimer_begin(const char* name, cudaStream_t s) {
+void ktimer_begin(const char* name, cudaStream_t s, int level) {
   KTimer& k = ktimer();
   std::lock_guard<std::mutex> g(k.mu);
-  if (!k.enabled) return;
+  if (!k.enabled || level > k.level) return;
   KTimer::Pending p;
   p.name = name;
   p.a = k.take();
@@ -59,10 +60,10 @@ void ktimer_begin(const char* name, cudaStream_t s) {
   k.open[s].push_back(p);
 }
 
-void ktimer_end(const char* name, cudaStream_t s) {
+void ktimer_end(const char* name, cudaStream_t s, int level) {
   KTimer& k = ktimer();
   std::lock_guard<std::mutex> g(k.mu);
-  if (!k.enabled) return;
+  if (!k.enabled || level > k.level) return;
   auto& v = k.open[s];
   if (v.empty()) return;
   KTimer::Pending p = v.back();
@@ -101,6 +102,56 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 }  // namespace
 
+// Device staging for the host-buffer entry points (hkv_find_host /
+// hkv_upsert_host): a copy stream, a ring of chunk slots and their events.
+constexpr int kRing = 3;
+struct HostStage {
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ready[kRing] = {}, done[kRing] = {}, start = nullptr, vals = nullptr;
+  uint64_t* keys = nullptr;  // find: kRing chunk slots; upsert: the batch
+  size_t keys_cap = 0;
+  float* rows = nullptr;
+  size_t rows_cap = 0;
+  uint8_t* bytes = nullptr;  // found / outcomes
+  size_t bytes_cap = 0;
+  uint64_t* aux = nullptr;   // scores, ticks
+  size_t aux_cap = 0;
+  cudaError_t init() {
+    if (copy) return cudaSuccess;
+    cudaError_t e = cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking);
+    for (int k = 0; k < kRing && !e; k++) {
+      if ((e = cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming))) break;
+      e = cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
+    }
+    if (!e) e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+    if (!e) e = cudaEventCreateWithFlags(&vals, cudaEventDisableTiming);
+    return e;
+  }
+  void release() {
+    if (copy) cudaStreamSynchronize(copy);
+    for (void* p : {(void*)keys, (void*)rows, (void*)bytes, (void*)aux})
+      if (p) cudaFree(p);
+    for (int k = 0; k < kRing; k++) {
+      if (ready[k]) cudaEventDestroy(ready[k]);
+      if (done[k]) cudaEventDestroy(done[k]);
+    }
+    if (start) cudaEventDestroy(start);
+    if (vals) cudaEventDestroy(vals);
+    if (copy) cudaStreamDestroy(copy);
+  }
+};
+
+template <class T>
+cudaError_t grow_dev(T*& p, size_t& cap, size_t need) {
+  if (need <= cap) return cudaSuccess;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  cudaError_t e = cudaMalloc(&p, need * sizeof(T));
+  if (!e) cap = need;
+  return e;
+}
+
 struct hkv_table {
   hkv_config cfg;
   int64_t buckets = 0;
@@ -131,10 +182,15 @@ struct hkv_table {
   TableScalars* snap_sc = nullptr;
   std::mutex mu;
   std::map<cudaStream_t, Workspace> ws;
+  std::map<cudaStream_t, HostStage> hs;
 
   Workspace& workspace(cudaStream_t s) {
     std::lock_guard<std::mutex> g(mu);
     return ws[s];
+  }
+  HostStage& stage(cudaStream_t s) {
+    std::lock_guard<std::mutex> g(mu);
+    return hs[s];
   }
 };
 
@@ -167,6 +223,7 @@ void free_table(hkv_table* t) {
   if (t->vover_host) cudaFreeHost(t->vover_host);
   else if (t->vover) cudaFree(t->vover);
   for (auto& kv : t->ws) ws_free(kv.second);
+  for (auto& kv : t->hs) kv.second.release();
   delete t;
 }
 
@@ -182,6 +239,7 @@ int hkv_set_kernel_timing(int32_t enable) {
   KTimer& k = ktimer();
   std::lock_guard<std::mutex> g(k.mu);
   k.enabled = enable != 0;
+  k.level = enable;
   while (k.enabled && k.pool.size() < 8192) {
     cudaEvent_t e;
     if (cudaEventCreate(&e) != cudaSuccess) break;
@@ -234,6 +292,14 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
   if (c.value_dim > (1 << 20)) return fail(HKV_EINVAL, "value_dim too large");
 
   DeviceGuard g(c.device);
+  if (const char* l2 = getenv("HKV_L2_FETCH")) {  // experiment: L2 fetch granularity hint (bytes)
+    size_t before = 0;
+    cudaDeviceGetLimit(&before, cudaLimitMaxL2FetchGranularity);
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2));
+    size_t after = 0;
+    cudaDeviceGetLimit(&after, cudaLimitMaxL2FetchGranularity);
+    fprintf(stderr, "hkv: L2 fetch granularity %zu -> %zu\n", before, after);
+  }
   hkv_table* t = new hkv_table();
   t->cfg = c;
   t->cfg.fast_tier_budget = budget;
@@ -393,6 +459,113 @@ int hkv_upsert(hkv_table* t, int32_t op, const uint64_t* keys, float* values, co
                                evicted_keys, evicted_values, evicted_scores, ticks ? clock_advance : (uint64_t)n,
                                s, t->num_sms);
   return e ? cuda_fail(e, "hkv_upsert") : HKV_OK;
+}
+
+// Host-buffer find: chunks of keys go H2D, are probed into a ring slot, and
+// the slot's found bytes and rows come back D2H on the copy stream while the
+// next chunk is probed.  A caller `out` with zero_misses == 0 keeps its miss
+// rows: the chunk's rows go H2D first (the PCIe link is full duplex, so this
+// rides beside the previous chunk's D2H).
+int hkv_find_host(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uint8_t* found, int32_t zero_misses,
+                  hkv_stream stream) {
+  CHECK_T();
+  if (n && (!keys || !found)) return fail(HKV_EINVAL, "null keys/found");
+  if (n == 0) return HKV_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  HostStage& h = t->stage(s);
+  cudaError_t e = h.init();
+  if (e) return cuda_fail(e, "hkv_find_host init");
+  const int64_t dim = t->cfg.value_dim;
+  int64_t chunk = out ? ((int64_t)16 << 20) / (dim * 4) : n;  // ~16 MB of rows per slot
+  if (chunk < 4096) chunk = 4096;
+  if (chunk > n) chunk = n;
+  if ((e = grow_dev(h.keys, h.keys_cap, (size_t)(kRing * chunk)))) return cuda_fail(e, "hkv_find_host staging");
+  if ((e = grow_dev(h.bytes, h.bytes_cap, (size_t)(kRing * chunk)))) return cuda_fail(e, "hkv_find_host staging");
+  if (out && (e = grow_dev(h.rows, h.rows_cap, (size_t)(kRing * chunk * dim))))
+    return cuda_fail(e, "hkv_find_host staging");
+  Workspace& ws = t->workspace(s);
+  if (out && (e = ws_reserve(ws, chunk, (int)dim, 0, false))) return cuda_fail(e, "hkv_find_host workspace");
+  if ((e = cudaEventRecord(h.start, s)) || (e = cudaStreamWaitEvent(h.copy, h.start, 0)))
+    return cuda_fail(e, "hkv_find_host");
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  for (int64_t c = 0; c < nchunks; c++) {
+    const int slot = (int)(c % kRing);
+    const int64_t off = c * chunk, cnt = (n - off < chunk) ? n - off : chunk;
+    uint64_t* dk = h.keys + (size_t)slot * chunk;
+    uint8_t* df = h.bytes + (size_t)slot * chunk;
+    float* dr = out ? h.rows + (size_t)slot * chunk * dim : nullptr;
+    if (c >= kRing && (e = cudaStreamWaitEvent(s, h.done[slot], 0))) break;
+    if ((e = cudaMemcpyAsync(dk, keys + off, cnt * 8, cudaMemcpyHostToDevice, s))) break;
+    if (out && !zero_misses &&
+        (e = cudaMemcpyAsync(dr, out + off * dim, cnt * dim * 4, cudaMemcpyHostToDevice, s)))
+      break;
+    launch_find(t->dev, dk, cnt, dr, df, nullptr, nullptr, out ? (zero_misses ? 3 : 0) : 1, out ? ws.vrow : nullptr,
+                s, t->num_sms);
+    if ((e = cudaGetLastError())) break;
+    if ((e = cudaEventRecord(h.ready[slot], s)) || (e = cudaStreamWaitEvent(h.copy, h.ready[slot], 0))) break;
+    if ((e = cudaMemcpyAsync(found + off, df, cnt, cudaMemcpyDeviceToHost, h.copy))) break;
+    if (out && (e = cudaMemcpyAsync(out + off * dim, dr, cnt * dim * 4, cudaMemcpyDeviceToHost, h.copy))) break;
+    if ((e = cudaEventRecord(h.done[slot], h.copy))) break;
+  }
+  cudaError_t e2 = cudaEventRecord(h.vals, h.copy);
+  if (!e2) e2 = cudaStreamWaitEvent(s, h.vals, 0);
+  if (!e2) e2 = cudaStreamSynchronize(s);
+  if (e || e2) return cuda_fail(e ? e : e2, "hkv_find_host");
+  return HKV_OK;
+}
+
+// Host-buffer upsert: keys (and scores / ticks) go H2D on the caller's stream
+// and the metadata pass starts at once; the value rows go H2D on the copy
+// stream in parallel, and run_mutation holds the value phase until they land.
+int hkv_upsert_host(hkv_table* t, int32_t op, const uint64_t* keys, float* values, const uint64_t* scores, int64_t n,
+                    uint8_t* outcomes, const uint64_t* ticks, uint64_t clock_advance, hkv_stream stream) {
+  CHECK_T();
+  if (op != HKV_OP_INSERT_OR_ASSIGN && op != HKV_OP_FIND_OR_INSERT) return fail(HKV_EINVAL, "unknown upsert op");
+  const bool custom = t->cfg.score_policy == HKV_CUSTOMIZED;
+  if (custom && !scores) return fail(HKV_EINVAL, "kCustomized requires explicit scores");
+  if (!custom && scores) return fail(HKV_EINVAL, "explicit scores require the kCustomized policy");
+  if (n && (!keys || !values || !outcomes)) return fail(HKV_EINVAL, "null keys/values/outcomes");
+  if (n > 0xFFFFFFFEll) return fail(HKV_EINVAL, "batch too large");
+  cudaStream_t s = (cudaStream_t)stream;
+  HostStage& h = t->stage(s);
+  cudaError_t e = h.init();
+  if (e) return cuda_fail(e, "hkv_upsert_host init");
+  const int64_t dim = t->cfg.value_dim;
+  const size_t nn = n > 0 ? (size_t)n : 1;
+  if ((e = grow_dev(h.keys, h.keys_cap, nn)) || (e = grow_dev(h.bytes, h.bytes_cap, nn)) ||
+      (e = grow_dev(h.rows, h.rows_cap, nn * dim)) || (e = grow_dev(h.aux, h.aux_cap, 2 * nn)))
+    return cuda_fail(e, "hkv_upsert_host staging");
+  uint64_t* dscores = scores ? h.aux : nullptr;
+  uint64_t* dticks = ticks ? h.aux + nn : nullptr;
+  if (n > 0) {
+    if ((e = cudaEventRecord(h.start, s)) || (e = cudaStreamWaitEvent(h.copy, h.start, 0)) ||
+        (e = cudaMemcpyAsync(h.keys, keys, n * 8, cudaMemcpyHostToDevice, s)) ||
+        (scores && (e = cudaMemcpyAsync(dscores, scores, n * 8, cudaMemcpyHostToDevice, s))) ||
+        (ticks && (e = cudaMemcpyAsync(dticks, ticks, n * 8, cudaMemcpyHostToDevice, s))) ||
+        (e = cudaMemcpyAsync(h.rows, values, n * dim * 4, cudaMemcpyHostToDevice, h.copy)) ||
+        (e = cudaEventRecord(h.vals, h.copy)))
+      return cuda_fail(e, "hkv_upsert_host copy-in");
+  }
+  OpArgs a{};
+  a.keys = h.keys;
+  a.values = h.rows;
+  a.scores = dscores;
+  a.ticks = dticks;
+  a.outcomes = h.bytes;
+  a.op = op == HKV_OP_FIND_OR_INSERT ? kOpFindOrInsert : kOpUpsert;
+  a.collect = 0;
+  a.epoch = t->epoch;
+  e = run_mutation(t->dev, a, n, t->log2b, t->workspace(s), (++t->dual_epoch) << 32, t->lead, nullptr, nullptr,
+                   nullptr, nullptr, ticks ? clock_advance : (uint64_t)n, s, t->num_sms, n > 0 ? h.vals : nullptr);
+  if (e) return cuda_fail(e, "hkv_upsert_host");
+  if (n > 0) {
+    if ((e = cudaMemcpyAsync(outcomes, h.bytes, n, cudaMemcpyDeviceToHost, s))) return cuda_fail(e, "hkv_upsert_host");
+    if (op == HKV_OP_FIND_OR_INSERT &&
+        (e = cudaMemcpyAsync(values, h.rows, n * dim * 4, cudaMemcpyDeviceToHost, s)))
+      return cuda_fail(e, "hkv_upsert_host");
+  }
+  if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "hkv_upsert_host");
+  return HKV_OK;
 }
 
 int hkv_erase(hkv_table* t, const uint64_t* keys, int64_t n, uint8_t* outcomes, hkv_stream stream) {

@@ -86,7 +86,7 @@ void launch_find(const TableDev& t, const uint64_t* keys, int64_t n, float* out,
 cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, Workspace& ws,
                          unsigned long long dual_tag, unsigned long long* lead, int64_t* n_evicted,
                          uint64_t* ek_out, float* ev_out, uint64_t* es_out, uint64_t clock_advance,
-                         cudaStream_t s, int num_sms);
+                         cudaStream_t s, int num_sms, cudaEvent_t values_ready = nullptr);
 
 cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* values,
                        const uint64_t* scores, int refresh, uint64_t epoch, int64_t n, uint8_t* outcomes,
@@ -103,8 +103,8 @@ cudaError_t run_route(const uint64_t* keys, int64_t n, int64_t global_buckets, i
                       int64_t* counts, Workspace& ws, cudaStream_t s);
 
 // Live timing of dominant kernels (hkv_set_kernel_timing).
-void ktimer_begin(const char* name, cudaStream_t s);
-void ktimer_end(const char* name, cudaStream_t s);
+void ktimer_begin(const char* name, cudaStream_t s, int level = 1);
+void ktimer_end(const char* name, cudaStream_t s, int level = 1);
 
 cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual);
 cudaError_t ws_reserve_dual(Workspace& ws, int64_t n, int log2_buckets);

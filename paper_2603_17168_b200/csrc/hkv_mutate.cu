@@ -199,6 +199,9 @@ __device__ __forceinline__ uint64_t run_hit_score(int policy, uint64_t old, uint
 // cross-lane collectives, which is what the metadata pass is bound by
 // (dependent random loads, profiles/r01).
 // ---------------------------------------------------------------------------
+#ifndef HKV_TPS_MINB
+#define HKV_TPS_MINB 2  // resident blocks per SM the metadata pass is compiled for
+#endif
 constexpr int kTpsThreads = 256;  // block size of k_meta_tps (stride of its per-thread shared arrays)
 
 struct TpsState {
@@ -678,7 +681,7 @@ __device__ __forceinline__ void tps_segment(const TableDev& t, const OpArgs& a, 
 // digest line + occupancy of segment k+1 are in flight into shared memory
 // and the record of segment k+2 into registers.
 template <int OP, bool COLLECT>
-__global__ void __launch_bounds__(kTpsThreads, 2) k_meta_tps(TableDev t, OpArgs a, const uint32_t* __restrict__ sb,
+__global__ void __launch_bounds__(kTpsThreads, HKV_TPS_MINB) k_meta_tps(TableDev t, OpArgs a, const uint32_t* __restrict__ sb,
                                                             const uint32_t* __restrict__ sidx,
                                                             uint32_t* run_end,  // written: lw_fill jump marks
                                                             const uint64_t* __restrict__ skeys,
@@ -1161,7 +1164,10 @@ static cudaError_t run_ends(Workspace& ws, int64_t n, cudaStream_t s) {
 cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, Workspace& ws,
                          unsigned long long dual_tag, unsigned long long* lead, int64_t* n_evicted,
                          uint64_t* ek_out, float* ev_out, uint64_t* es_out, uint64_t clock_advance,
-                         cudaStream_t s, int num_sms) {
+                         cudaStream_t s, int num_sms, cudaEvent_t values_ready) {
+  // values_ready: the value rows may still be in flight (host-buffer entry
+  // points copy them H2D on another stream); nothing before the value phase
+  // (dual mode: the dataflow) reads them.
   cudaError_t e;
   const bool collect = a.collect != 0;
   if ((e = ws_reserve(ws, n, t.dim, collect ? (t.dual ? 2 : 1) : 0, t.dual != 0))) return e;
@@ -1172,18 +1178,24 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
   a.ev = ws.ev;
   if ((e = cudaMemsetAsync(ws.sc, 0, sizeof(Scalars), s))) return e;
   if (n > 0) {
+    ktimer_begin("prep", s, 2);
     k_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(t, a.keys, n, ws.bkt, ws.idx, t.dual ? ws.b2 : nullptr,
                                                         ws.sc);
+    ktimer_end("prep", s, 2);
     g_launches++;
     const int vec = vec_of(t.dim, a.values, t.vfast, t.vover, collect ? ws.ev : nullptr);
     if (!t.dual) {
+      ktimer_begin("sort", s, 2);
       if ((e = sort_segments(ws, n, log2_buckets, s))) return e;
+      ktimer_end("sort", s, 2);
       SegRec* recs = reinterpret_cast<SegRec*>(ws.skey);
       const uint8_t fcode = a.op == kOpErase ? kNotFound : a.op == kOpFindOrInsert ? kFound : kUpdated;
+      ktimer_begin("segments", s, 2);
       k_segments<<<(unsigned)((n + 1023) / 1024), 1024, 0, s>>>(ws.sbkt, ws.sidx, a.keys, n, recs, n, ws.sc, ws.aux2,
                                                                  a.outcomes, ws.vrow, fcode, ws.skeys);
       g_launches++;
       if ((e = run_ends(ws, n, s))) return e;
+      ktimer_end("segments", s, 2);
       ktimer_begin("apply", s);
       auto* fn = a.op == kOpErase ? k_meta_tps<kOpErase, false>
                  : a.op == kOpFindOrInsert ? k_meta_tps<kOpFindOrInsert, false>
@@ -1197,7 +1209,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
         attr_set = true;
       }
       int64_t tb = (n + kTpsThreads - 1) / kTpsThreads;
-      const int64_t tcap = (int64_t)num_sms * 2;  // one resident wave
+      const int64_t tcap = (int64_t)num_sms * HKV_TPS_MINB;  // one resident wave
       if (!ws.lwtab && (e = grow(ws.lwtab, tcap * kTpsThreads * kSlots))) return e;  // 128 entries per thread
       if (tb > tcap) tb = tcap;
       fn<<<(unsigned)(tb < 1 ? 1 : tb), kTpsThreads, smem, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, recs, n, n,
@@ -1206,12 +1218,16 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       ktimer_end("apply", s);
       g_launches++;
     } else {
+      if (values_ready && (e = cudaStreamWaitEvent(s, values_ready, 0))) return e;
+      values_ready = nullptr;
       ktimer_begin("dual_flow", s);
       if ((e = run_dual(t, a, n, log2_buckets, ws, lead, dual_tag, vec, s, num_sms))) return e;
       ktimer_end("dual_flow", s);
     }
   }
+  ktimer_begin("finalize", s, 2);
   k_finalize<<<1, 1024, 0, s>>>(t, ws.sc, a.op == kOpErase ? nullptr : a.outcomes, n, clock_advance, 0);
+  ktimer_end("finalize", s, 2);
   g_launches++;
   long long* nev = reinterpret_cast<long long*>(n_evicted);
   if (collect && n > 0) {
@@ -1223,6 +1239,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
   }
   const int64_t vblocks = tile_blocks(n, num_sms);
   if (!t.dual && n > 0 && a.op != kOpErase) {
+    if (values_ready && (e = cudaStreamWaitEvent(s, values_ready, 0))) return e;
     // value reads (provenance-resolved) strictly before value writes
     const int vr = vec_of(t.dim, a.values, t.vfast, t.vover, collect ? ev_out : nullptr);
     if (collect || a.op == kOpFindOrInsert) {

@@ -241,6 +241,8 @@ class CacheTable:
     def find(self, keys, out=None):
         """Batched lookup copying values; returns (found, values).  Misses leave
         the output row untouched (table.py:304-323)."""
+        if self._host_call(keys, out):
+            return self._find_host(keys, out)
         k, np_mode = self._keys_in(keys)
         n = k.numel()
         dim = self.config.value_dim
@@ -289,6 +291,66 @@ class CacheTable:
             host_out[...] = out_d.cpu().numpy()
             return f, host_out
         return f, out_d.cpu().numpy()
+
+    # ----- host buffers (pinned CPU tensors): hkv_find_host / hkv_upsert_host --
+    @staticmethod
+    def _host_call(keys, *others) -> bool:
+        """CPU torch tensors in and out: the library pipelines the PCIe copies
+        with the kernels (include/hkv_b200.h, host-buffer entry points)."""
+        if not (isinstance(keys, torch.Tensor) and keys.device.type == "cpu"):
+            return False
+        return all(o is None or (isinstance(o, torch.Tensor) and o.device.type == "cpu") for o in others)
+
+    def _host_keys(self, keys: torch.Tensor) -> torch.Tensor:
+        # table.py:164-170; the reserved-sentinel test runs on the device
+        # (error latch, no mutation) and surfaces through _check_device_error
+        if keys.dim() != 1:
+            raise ValueError("keys must be one-dimensional")
+        if keys.dtype not in (torch.int64, torch.uint64):
+            raise ValueError("keys must be uint64 (or bit-identical int64)")
+        return keys.contiguous().view(torch.int64)
+
+    def _find_host(self, keys, out):
+        k = self._host_keys(keys)
+        n = k.numel()
+        dim = self.config.value_dim
+        zero_misses = 0
+        if out is None:
+            out = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
+            zero_misses = 1
+        elif tuple(out.shape) != (n, dim) or out.dtype != torch.float32 or not out.is_contiguous():
+            raise ValueError("out must be float32 with shape (len(keys), value_dim)")
+        found = torch.empty(n, dtype=torch.bool, pin_memory=True)
+        with self.gate.acquire(Role.Reader, self._stream()):
+            _lib.check(self._lib.hkv_find_host(self._h, _ptr(k), n, _ptr(out), _ptr(found), zero_misses,
+                                               self._sp()))
+        self._check_device_error()
+        return found, out
+
+    def _upsert_host(self, op: int, keys, values, scores, clock_advance: int):
+        k = self._host_keys(keys)
+        n = k.numel()
+        dim = self.config.value_dim
+        if tuple(values.shape) != (n, dim) or values.dtype != torch.float32:
+            raise ValueError("values must have shape (len(keys), value_dim)")
+        if op == 1 and not values.is_contiguous():
+            raise ValueError("values_inout must be a C-contiguous float32 array of shape (n, value_dim)")
+        v = values.contiguous()
+        s = None  # table.py:178-188
+        if self.config.score_policy is PolicyId.kCustomized:
+            if scores is None:
+                raise ValueError("kCustomized requires explicit scores")
+            if tuple(scores.shape) != (n,):
+                raise ValueError("scores must have shape (len(keys),)")
+            s = scores.contiguous().view(torch.int64)
+        elif scores is not None:
+            raise ValueError("explicit scores require the kCustomized policy")
+        outcomes = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        with self.gate.acquire(Role.Inserter, self._stream()):
+            _lib.check(self._lib.hkv_upsert_host(self._h, op, _ptr(k), _ptr(v), _ptr(s), n, _ptr(outcomes), None,
+                                                 int(clock_advance), self._sp()))
+        self._check_device_error()
+        return outcomes
 
     def contains(self, keys):
         k, np_mode = self._keys_in(keys)
@@ -403,6 +465,8 @@ class CacheTable:
 
     # ----- inserter operations (table.py:515-558) ----------------------------
     def insert_or_assign(self, keys, values, scores=None, *, ticks=None, clock_advance: int = 0):
+        if ticks is None and self._host_call(keys, values, scores):
+            return self._upsert_host(0, keys, values, scores, clock_advance)
         k, np_mode = self._keys_in(keys)
         n = k.numel()
         v = self._values_in(values, n, np_mode)

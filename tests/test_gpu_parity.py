@@ -353,3 +353,54 @@ def test_checkpoint_round_trip(hkv, mode, tmp_path):
         ro = o.insert_and_evict(k, v)
         assert all(x.tobytes() == y.tobytes() for x, y in zip(r2, ro))
     assert_same_state(t2, o)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_buffer_entry_points(hkv, mode, pinned):
+    """hkv_find_host / hkv_upsert_host (CPU tensors in and out, PCIe copies
+    pipelined inside the library) give the oracle's results bit-exactly: a
+    batch spanning several ring cycles of find chunks, a caller `out` whose
+    miss rows stay untouched, and host scores under kCustomized."""
+    cap, dim = 2**18, 64
+    rng = np.random.default_rng(11)
+    for policy in ("kLru", "kCustomized"):
+        t = make_table(hkv, cap, dim, mode, policy)
+        o = OracleTable(cap, dim, mode=mode, score_policy=policy)
+        pin = (lambda x: x.pin_memory()) if pinned else (lambda x: x)
+        for step in range(3):
+            n = 300_001 if step == 0 else 123_457  # 300k rows = 5 find chunks of 64k (ring of 3)
+            keys = rng.integers(1, 2**40, size=n, dtype=np.uint64)
+            keys[: n // 10] = keys[n // 10: 2 * (n // 10)]  # in-batch duplicates
+            vals = rng.standard_normal((n, dim)).astype(np.float32)
+            sc = rng.integers(0, 2**20, size=n, dtype=np.uint64) if policy == "kCustomized" else None
+            kh = pin(torch.from_numpy(keys.view(np.int64)))
+            vh = pin(torch.from_numpy(vals))
+            sh = None if sc is None else pin(torch.from_numpy(sc.view(np.int64)))
+            out_t = t.insert_or_assign(kh, vh, sh)
+            assert out_t.device.type == "cpu"
+            assert np.array_equal(out_t.numpy(), o.insert_or_assign(keys, vals, sc)), (policy, step)
+            q = np.concatenate([keys[: n // 2], rng.integers(2**41, 2**42, size=n // 2, dtype=np.uint64)])
+            qh = pin(torch.from_numpy(q.view(np.int64)))
+            f, v = t.find(qh)
+            fo, vo = o.find(q)
+            assert f.device.type == "cpu" and np.array_equal(f.numpy(), fo)
+            assert v.numpy().tobytes() == vo.tobytes()
+            # caller-provided out: miss rows keep their contents
+            base = rng.standard_normal((len(q), dim)).astype(np.float32)
+            out = pin(torch.from_numpy(base.copy()))
+            f2, v2 = t.find(qh, out=out)
+            assert v2 is out and np.array_equal(f2.numpy(), fo)
+            exp = np.where(fo[:, None], vo, base)
+            assert v2.numpy().tobytes() == exp.tobytes()
+        assert_same_state(t, o)
+    # sentinel keys through the host path: ValueError, no mutation
+    t = make_table(hkv, 1024, 4, mode)
+    t.insert_or_assign(np.arange(1, 11, dtype=np.uint64), np.ones((10, 4), np.float32))
+    before = t.export_state()
+    with pytest.raises(ValueError):
+        t.insert_or_assign(torch.tensor([5, -2, 7], dtype=torch.int64), torch.zeros((3, 4)))
+    after = t.export_state()
+    for k in ("keys", "digests", "scores", "values"):
+        assert before[k].tobytes() == after[k].tobytes()
+    assert before["clock"] == after["clock"] and before["size"] == after["size"]
