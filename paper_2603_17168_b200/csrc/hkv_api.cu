@@ -292,14 +292,6 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
   if (c.value_dim > (1 << 20)) return fail(HKV_EINVAL, "value_dim too large");
 
   DeviceGuard g(c.device);
-  if (const char* l2 = getenv("HKV_L2_FETCH")) {  // experiment: L2 fetch granularity hint (bytes)
-    size_t before = 0;
-    cudaDeviceGetLimit(&before, cudaLimitMaxL2FetchGranularity);
-    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2));
-    size_t after = 0;
-    cudaDeviceGetLimit(&after, cudaLimitMaxL2FetchGranularity);
-    fprintf(stderr, "hkv: L2 fetch granularity %zu -> %zu\n", before, after);
-  }
   hkv_table* t = new hkv_table();
   t->cfg = c;
   t->cfg.fast_tier_budget = budget;
