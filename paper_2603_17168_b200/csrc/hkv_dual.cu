@@ -342,6 +342,7 @@ cudaError_t run_dual(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, W
   const int64_t m = 2 * n;
   const uint32_t none = (uint32_t)(1ull << log2_buckets);
   const unsigned blk = (unsigned)((n + 255) / 256), blk2 = (unsigned)((m + 255) / 256);
+  ktimer_begin("dual_ranks", s, 2);
   k_dual_pairs<<<blk, 256, 0, s>>>(ws.bkt, ws.b2, n, none, ws.dpk, ws.dpv, ws.sc);
   size_t bytes = ws.dcub_bytes;
   if ((e = cub::DeviceRadixSort::SortPairs(ws.dcub, bytes, ws.dpk, ws.dsk, ws.dpv, ws.dsv, (int)m, 0,
@@ -351,6 +352,7 @@ cudaError_t run_dual(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, W
   bytes = ws.dcub_bytes;
   if ((e = cub::DeviceScan::InclusiveScan(ws.dcub, bytes, ws.dpk, ws.dpv, cub::Max(), (int)m, s))) return e;
   k_dual_ranks<<<blk2, 256, 0, s>>>(ws.dsk, ws.dsv, ws.dpv, m, none, ws.drank);
+  ktimer_end("dual_ranks", s, 2);
   g_launches += 10;
   int per_sm = 0;
   void* fn = vec == 4 ? (void*)k_dual_flow<4> : vec == 2 ? (void*)k_dual_flow<2> : (void*)k_dual_flow<1>;

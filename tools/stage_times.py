@@ -1,6 +1,6 @@
 """Warm per-stage device times of the single-mode mutation pipeline on C2.
 
-    python tools/stage_times.py [log2_capacity]
+    python tools/stage_times.py [log2_capacity] [lambdas, e.g. 0.5,1.0] [single|dual]
 
 Fills a dim-64 table to lambda 0.5 and 1.0, then runs insert_or_assign of
 1M fresh keys (snapshot restored after each), assign of 1M resident keys and
@@ -19,7 +19,7 @@ from paper_2603_17168_b200 import _lib  # noqa: E402
 from paper_2603_17168_b200 import workloads as W  # noqa: E402
 
 STAGES = ["prep", "sort", "segments", "apply", "finalize", "values_write", "assign_apply", "find", "find_gather",
-          "dual_flow"]
+          "dual_ranks", "dual_flow"]
 lg = int(sys.argv[1]) if len(sys.argv) > 1 else 27
 cap, dim, B = 2**lg, 64, 2**20
 lib = _lib.load()
@@ -36,7 +36,8 @@ def stage_report(label, reps, total_ms):
     print(f"{label}: total {1e3 * total_ms / reps:.1f} us | " + " | ".join(parts), flush=True)
 
 
-t = hkv.CacheTable(hkv.TableConfig(capacity=cap, value_dim=dim))
+mode = sys.argv[3] if len(sys.argv) > 3 else "single"
+t = hkv.CacheTable(hkv.TableConfig(capacity=cap, value_dim=dim, mode=mode))
 t.validate_keys = False
 vals = torch.randn((B, dim), device="cuda")
 off = 0
