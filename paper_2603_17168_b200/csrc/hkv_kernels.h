@@ -16,6 +16,7 @@ struct Scalars {
   unsigned first_ev;             // lowest batch index with an Evicted outcome
   unsigned npend[2];             // dual-mode pending list sizes (per round parity)
   unsigned has_runs;             // single mode: some op is followed by the same key in its bucket segment
+  unsigned nlong;                // single mode: segments of >= kLongSeg ops (k_meta_long)
   long long size_before;         // table size when the batch started
   unsigned long long nfound;     // assign: found ops (clock advance for refresh)
   long long n_sel;               // DeviceSelect count
@@ -35,6 +36,7 @@ struct Workspace {
   uint32_t* aux = nullptr;   // assign: rows / evicted list
   uint32_t* aux2 = nullptr;  // assign: found ranks
   uint64_t* skey = nullptr;  // single mode: bucket-segment records (3 u64 per item)
+  uint64_t* lrec = nullptr;  // single mode: records of long segments (3 u64 each)
   uint64_t* skeys = nullptr; // single mode: keys in sorted (bucket, batch index) order
   uint32_t* vrow = nullptr;  // single mode: destination row of final value writers
   uint32_t* rrow = nullptr;  // single mode: row of a value read

@@ -91,9 +91,13 @@ struct SegRec {
 // same key (then ~0), so a reverse min-scan gives run_end[p] = the last
 // position of p's run.  Followers (p-1 has the same key) get the collapsed
 // outcome `fcode` and no value row up front; tps_run writes the exceptions.
+// Segments of at least kLongSeg ops go to a third list for k_meta_long.
+constexpr int kLongSeg = 32;
+
 __global__ void __launch_bounds__(1024) k_segments(const uint32_t* __restrict__ sb, const uint32_t* __restrict__ sidx,
                                                    const uint64_t* __restrict__ keys, int64_t n,
-                                                   SegRec* __restrict__ recs, int64_t cap, Scalars* sc,
+                                                   SegRec* __restrict__ recs, int64_t cap, SegRec* __restrict__ lrecs,
+                                                   Scalars* sc,
                                                    uint32_t* __restrict__ brk, uint8_t* __restrict__ outcomes,
                                                    uint32_t* __restrict__ vrow, uint8_t fcode,
                                                    uint64_t* __restrict__ skeys) {
@@ -129,8 +133,9 @@ __global__ void __launch_bounds__(1024) k_segments(const uint32_t* __restrict__ 
       vrow[i] = kNoRow;
     }
   }
+  const bool lng = head && multi && lrecs != nullptr && p + kLongSeg - 1 < n && sb[p + kLongSeg - 1] == b;
   const unsigned ms = __ballot_sync(kFull, head && !multi);
-  const unsigned mm = __ballot_sync(kFull, head && multi);
+  const unsigned mm = __ballot_sync(kFull, head && multi && !lng);
   if (lane == 0) {
     wcount[0][warp] = __popc(ms);
     wcount[1][warp] = __popc(mm);
@@ -154,6 +159,10 @@ __global__ void __launch_bounds__(1024) k_segments(const uint32_t* __restrict__ 
     rec.b = b;
     rec.i = i;
     rec.flags = (multi ? 1u : 0u) | (digest_of(fmix64(rec.key)) << 8);
+    if (lng) {
+      lrecs[atomicAdd(&sc->nlong, 1u)] = rec;
+      return;
+    }
     const int c = multi ? 1 : 0;
     const unsigned m = multi ? mm : ms;
     const int64_t slot = block_base[c] + wcount[c][warp] + __popc(m & ((1u << lane) - 1));
@@ -214,6 +223,9 @@ struct TpsState {
   bool tab;          // the table holds this segment's writers
   uint4* L;          // digest line (shared memory, 8 x 16 B)
   uint32_t* O;       // occupancy bitmap words (shared memory, slots 32w .. 32w+31)
+  uint64_t* K;       // long-segment engine: the bucket's keys / scores in shared memory
+  uint64_t* Sc;      //   (slot j at [j * cs]); nullptr in the global-memory engine
+  int cs;
   uint32_t wm[4];    // slots already written by an earlier op of this segment
   uint64_t sm[8];    // group minima (register copy, valid where sv says so)
   uint32_t sv;       // summary valid bits (register copy)
@@ -250,6 +262,35 @@ __device__ __forceinline__ void put8(uint64_t (&a)[8], int g, uint64_t v) {
   }
 }
 
+// Bucket rows: global memory (k_meta_tps), or the shared-memory copy of the
+// long-segment engine (k_meta_long: written back once when the segment ends,
+// so a long serial chain never waits on a global round trip for data it wrote
+// itself).
+template <bool C>
+__device__ __forceinline__ uint64_t bkey(const TableDev& t, const TpsState& S, int j) {
+  if constexpr (C) return S.K[j * S.cs]; else return t.keys[S.rowbase + j];
+}
+template <bool C>
+__device__ __forceinline__ void set_bkey(const TableDev& t, const TpsState& S, int j, uint64_t v) {
+  if constexpr (C) S.K[j * S.cs] = v; else t.keys[S.rowbase + j] = v;
+}
+template <bool C>
+__device__ __forceinline__ uint64_t bscore(const TableDev& t, const TpsState& S, int j) {
+  if constexpr (C) return S.Sc[j * S.cs]; else return t.scores[S.rowbase + j];
+}
+template <bool C>
+__device__ __forceinline__ void set_bscore(const TableDev& t, const TpsState& S, int j, uint64_t v) {
+  if constexpr (C) S.Sc[j * S.cs] = v; else t.scores[S.rowbase + j] = v;
+}
+template <bool C>
+__device__ __forceinline__ void set_bdigest(const TableDev& t, const TpsState& S, int j, uint32_t d) {
+  if constexpr (!C) t.digests[S.rowbase + j] = (uint8_t)d;  // cached: S.L holds it, flushed at the end
+}
+template <bool C>
+__device__ __forceinline__ void set_bocc(const TableDev& t, const TpsState& S, uint64_t b, int w, uint32_t o) {
+  if constexpr (!C) t.bits[b * 4 + w] = o;  // cached: S.O holds it, flushed at the end
+}
+
 // candidates of digest d: digest-equal and occupied (table.py:243-247)
 __device__ __forceinline__ void tps_cand(const TableDev& t, const TpsState& S, uint32_t d, uint32_t (&c)[4]) {
   if (t.digest_filter) {
@@ -274,14 +315,20 @@ __device__ __forceinline__ void tps_cand(const TableDev& t, const TpsState& S, u
 }
 
 // the 16 scores of group g: min and first slot holding it
-__device__ __forceinline__ void tps_group_scan(const TableDev& t, uint64_t rowbase, int g, uint64_t (&v)[16],
+template <bool C>
+__device__ __forceinline__ void tps_group_scan(const TableDev& t, const TpsState& S, int g, uint64_t (&v)[16],
                                                uint64_t& mn, int& ms) {
-  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(t.scores + rowbase + 16 * g);
+  if constexpr (C) {
 #pragma unroll
-  for (int k = 0; k < 8; k++) {
-    const ulonglong2 x = p[k];
-    v[2 * k] = x.x;
-    v[2 * k + 1] = x.y;
+    for (int k = 0; k < 16; k++) v[k] = S.Sc[(16 * g + k) * S.cs];
+  } else {
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(t.scores + S.rowbase + 16 * g);
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const ulonglong2 x = p[k];
+      v[2 * k] = x.x;
+      v[2 * k + 1] = x.y;
+    }
   }
   mn = v[0];
   ms = 0;
@@ -364,7 +411,7 @@ __device__ __forceinline__ void lw_fill(TpsState& S, int64_t q, const uint32_t* 
   S.tab = true;
 }
 
-template <int OP, bool COLLECT>
+template <int OP, bool COLLECT, bool C>
 __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsState& S, uint64_t b, uint32_t i,
                                       uint64_t key, uint32_t d, uint64_t clock0, bool fel_open, int64_t q,
                                       uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
@@ -381,7 +428,7 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
       const int j = __ffs(m) - 1;
       m &= m - 1;
       ncmp++;
-      if (t.keys[rowbase + 32 * w + j] == key) {
+      if (bkey<C>(t, S, 32 * w + j) == key) {
         hit = 32 * w + j;
         m = 0;
       }
@@ -391,10 +438,10 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
   ctr[kCompares] += ncmp;
   if constexpr (OP == kOpErase) {  // _round_erase, table.py:1017-1023
     if (hit >= 0) {
-      t.keys[rowbase + hit] = kEmptyKey;
+      set_bkey<C>(t, S, hit, kEmptyKey);
       const uint32_t o = S.O[hit >> 5] & ~(1u << (hit & 31));
       S.O[hit >> 5] = o;
-      t.bits[b * 4 + (hit >> 5)] = o;
+      set_bocc<C>(t, S, b, hit >> 5, o);
       sd--;
     }
     a.outcomes[i] = hit >= 0 ? kErased : kNotFound;
@@ -405,10 +452,9 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
   uint8_t outcome = kRejected;
   int wslot = -1, rslot = -1;
   if (hit >= 0) {  // table.py:1045-1062
-    const uint64_t row = rowbase + hit;
-    const uint64_t old = hit_needs_old(t.policy) ? t.scores[row] : 0;
+    const uint64_t old = hit_needs_old(t.policy) ? bscore<C>(t, S, hit) : 0;
     const uint64_t ns = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
-    t.scores[row] = ns;
+    set_bscore<C>(t, S, hit, ns);
     tps_score_written(t, b, S, hit, ns);
     if constexpr (OP == kOpFindOrInsert) {
       outcome = kFound;
@@ -428,13 +474,12 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
 #pragma unroll
       for (int w = 3; w >= 0; w--)
         if (oc[w] != 0xFFFFFFFFu) s = 32 * w + __ffs(~oc[w]) - 1;
-      const uint64_t row = rowbase + s;
-      t.keys[row] = key;
-      t.digests[row] = (uint8_t)d;
-      t.scores[row] = s_in;
+      set_bkey<C>(t, S, s, key);
+      set_bdigest<C>(t, S, s, d);
+      set_bscore<C>(t, S, s, s_in);
       const uint32_t o = S.O[s >> 5] | (1u << (s & 31));
       S.O[s >> 5] = o;
-      t.bits[b * 4 + (s >> 5)] = o;
+      set_bocc<C>(t, S, b, s >> 5, o);
       reinterpret_cast<uint8_t*>(S.L)[s] = (uint8_t)d;
       // The summary is only consulted while the bucket is full, so a free
       // insert leaves it alone unless it fills the bucket: then every group
@@ -464,7 +509,7 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
       while (inv) {
         const int g = __ffs(inv) - 1;
         inv &= inv - 1;
-        tps_group_scan(t, rowbase, g, v, mn, ms);
+        tps_group_scan<C>(t, S, g, v, mn, ms);
         put8(S.sm, g, mn);
         S.smdirty |= 1u << g;
       }
@@ -477,17 +522,16 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
 #pragma unroll
       for (int k = 1; k < 8; k++)
         if (S.sm[k] < gmin) { gmin = S.sm[k]; gi = k; }
-      tps_group_scan(t, rowbase, gi, v, mn, ms);  // mn == gmin; ms = first slot holding it
+      tps_group_scan<C>(t, S, gi, v, mn, ms);  // mn == gmin; ms = first slot holding it
       if (s_in >= gmin) {  // the single-bucket path admits ties (table.py:1083)
         const int m = 16 * gi + ms;
-        const uint64_t row = rowbase + m;
         if constexpr (COLLECT) {
-          a.ek[i] = t.keys[row];
+          a.ek[i] = bkey<C>(t, S, m);
           a.es[i] = gmin;
         }
-        t.keys[row] = key;
-        t.digests[row] = (uint8_t)d;
-        t.scores[row] = s_in;
+        set_bkey<C>(t, S, m, key);
+        set_bdigest<C>(t, S, m, d);
+        set_bscore<C>(t, S, m, s_in);
         reinterpret_cast<uint8_t*>(S.L)[m] = (uint8_t)d;
         // the group's new minimum, exactly (its 16 scores are in registers)
         uint64_t nm = kMaxScore;
@@ -538,7 +582,7 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
 // Followers' outcome / vrow were pre-set by k_segments (Updated / Found /
 // NotFound, no value row); only the exceptions are written here.  TxnCounters
 // are exactly those of cnt individual probes.
-template <int OP>
+template <int OP, bool C>
 __device__ __forceinline__ void tps_run(const TableDev& t, const OpArgs& a, TpsState& S, int64_t q, int64_t qe,
                                         int res, uint64_t b, uint32_t d, uint64_t clock0,
                                         const uint32_t* __restrict__ sidx, uint32_t* __restrict__ vrow,
@@ -567,8 +611,8 @@ __device__ __forceinline__ void tps_run(const TableDev& t, const OpArgs& a, TpsS
   const uint32_t il = sidx[qe];
   const uint64_t tl = a.ticks ? a.ticks[il] : clock0 + (uint64_t)il + 1;
   const uint64_t cs = a.scores ? a.scores[il] : 0;
-  const uint64_t ns = run_hit_score(t.policy, t.scores[row], a.epoch, tl, a.scores != nullptr, cs, cnt);
-  t.scores[row] = ns;
+  const uint64_t ns = run_hit_score(t.policy, bscore<C>(t, S, res), a.epoch, tl, a.scores != nullptr, cs, cnt);
+  set_bscore<C>(t, S, res, ns);
   tps_score_written(t, b, S, res, ns);
   if constexpr (OP == kOpUpsert) {
     if (bit128(S.wm, res)) {
@@ -610,14 +654,15 @@ __device__ __forceinline__ void tps_fetch(const TableDev& t, uint4* buf, uint64_
   cp_async16(buf + 8, reinterpret_cast<const uint4*>(t.bits) + b);
 }
 
-template <int OP, bool COLLECT>
+template <int OP, bool COLLECT, bool C>
 __device__ __forceinline__ void tps_segment(const TableDev& t, const OpArgs& a, const SegRec& rec, uint4* buf,
                                             const uint32_t* __restrict__ sb, const uint32_t* __restrict__ sidx,
                                             uint32_t* run_end, const uint64_t* __restrict__ skeys,
                                             int64_t n, uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
                                             int32_t* __restrict__ rsrc, uint64_t clock0, bool fel_open,
                                             bool spec, bool lfu_like, bool runs, ctr_t* ctr, int& sd,
-                                            uint32_t& fe_min, int* lw, int64_t lws) {
+                                            uint32_t& fe_min, int* lw, int64_t lws, uint64_t* K = nullptr,
+                                            uint64_t* Sc = nullptr, int cs = 0) {
   const uint64_t b = rec.b;
   TpsState S;
   S.lw = lw;
@@ -626,15 +671,18 @@ __device__ __forceinline__ void tps_segment(const TableDev& t, const OpArgs& a, 
   S.vrow = vrow;
   S.p0 = rec.p;
   S.rowbase = b * kSlots;
-  S.tab = false;
+  S.tab = C;  // the long-segment engine keeps its last-writer table in shared memory from the start
   S.L = buf;
   S.O = reinterpret_cast<uint32_t*>(buf + 8);
+  S.K = K;
+  S.Sc = Sc;
+  S.cs = cs;
 #pragma unroll
   for (int w = 0; w < 4; w++) S.wm[w] = 0;
   S.sloaded = false;
   S.svdirty = false;
   S.smdirty = 0;
-  if (OP != kOpErase && spec) tps_load_summary(t, b, S);
+  if (OP != kOpErase && (spec || C)) tps_load_summary(t, b, S);
   const bool multi = (rec.flags & 1u) != 0;
   uint32_t i = rec.i, d = rec.flags >> 8;
   uint64_t key = rec.key;
@@ -650,11 +698,11 @@ __device__ __forceinline__ void tps_segment(const TableDev& t, const OpArgs& a, 
       qe = runs ? (int64_t)run_end[q] : q;
     }
     if (OP != kOpErase && !S.tab && q - S.p0 >= kLwScan) lw_fill(S, q, run_end, runs);  // erase writes no rows
-    const int res = tps_op<OP, COLLECT>(t, a, S, b, i, key, d, clock0, fel_open, q, vrow, rrow, rsrc,
+    const int res = tps_op<OP, COLLECT, C>(t, a, S, b, i, key, d, clock0, fel_open, q, vrow, rrow, rsrc,
                                         ctr, sd, fe_min);
     if (nb_ != (uint32_t)b) break;
     if (qe > q && (OP == kOpErase || res >= 0 || lfu_like)) {
-      tps_run<OP>(t, a, S, q, qe, res, b, d, clock0, sidx, vrow, rrow, rsrc, ctr);
+      tps_run<OP, C>(t, a, S, q, qe, res, b, d, clock0, sidx, vrow, rrow, rsrc, ctr);
       if (qe > q + 1) run_end[q + 1] = (uint32_t)qe | kJump;  // for lw_fill
       q = qe;
       if (!(q + 1 < n && sb[q + 1] == (uint32_t)b)) break;
@@ -675,6 +723,19 @@ __device__ __forceinline__ void tps_segment(const TableDev& t, const OpArgs& a, 
       if ((S.smdirty >> k) & 1u) t.smin[b * 8 + k] = S.sm[k];
   }
   if (S.svdirty || S.smdirty) t.svalid[b] = S.sv;
+  if constexpr (C) {  // write the bucket back once
+    ulonglong2* kd = reinterpret_cast<ulonglong2*>(t.keys + S.rowbase);
+    ulonglong2* sd2 = reinterpret_cast<ulonglong2*>(t.scores + S.rowbase);
+#pragma unroll 8
+    for (int j = 0; j < kSlots / 2; j++) {
+      kd[j] = make_ulonglong2(S.K[(2 * j) * cs], S.K[(2 * j + 1) * cs]);
+      sd2[j] = make_ulonglong2(S.Sc[(2 * j) * cs], S.Sc[(2 * j + 1) * cs]);
+    }
+    uint4* dd = reinterpret_cast<uint4*>(t.digests + S.rowbase);
+#pragma unroll
+    for (int k = 0; k < 8; k++) dd[k] = S.L[k];
+    reinterpret_cast<uint4*>(t.bits)[b] = *reinterpret_cast<const uint4*>(S.O);
+  }
 }
 
 // Two-stage cp.async pipeline per thread: while segment k is processed, the
@@ -719,7 +780,7 @@ __global__ void __launch_bounds__(kTpsThreads, HKV_TPS_MINB) k_meta_tps(TableDev
     const SegRec rn = rec_at(j + 2 * stride);  // in flight while segment j is processed
     cp_async_wait<1>();
     uint4* buf = tps_buf(tps_smem, stage);
-    tps_segment<OP, COLLECT>(t, a, ra, buf, sb, sidx, run_end, skeys, n, vrow, rrow, rsrc, clock0, fel_open, spec,
+    tps_segment<OP, COLLECT, false>(t, a, ra, buf, sb, sidx, run_end, skeys, n, vrow, rrow, rsrc, clock0, fel_open, spec,
                              lfu_like, runs, ctr, sd, fe_min, lwtab + gtid, stride);
     ra = rb;
     rb = rn;
@@ -727,6 +788,68 @@ __global__ void __launch_bounds__(kTpsThreads, HKV_TPS_MINB) k_meta_tps(TableDev
     cp_async_commit();
   }
   cp_async_wait<0>();
+  if (fel_open) {
+    unsigned m = __reduce_min_sync(kFull, fe_min);
+    if ((threadIdx.x & 31) == 0 && m != 0xFFFFFFFFu) atomicMin(&a.sc->first_ev, m);
+  }
+  block_ctrs_flush(bc, t.counters, t.size, ctr, sd);
+}
+
+// Long segments (>= kLongSeg ops on one bucket: configs[0] puts ~128 ops on
+// every bucket, zipf batches pile thousands on their hot buckets): one thread
+// per segment as in k_meta_tps, but the bucket's keys, scores and last-writer
+// table live in shared memory for the whole segment, so each op's compares,
+// argmin scans and writes are shared-memory operations instead of global
+// round trips on lines the thread itself just wrote.  The bucket is written
+// back once at the end.  kLongThreads threads per block, one block per SM.
+constexpr int kLongThreads = 64;
+constexpr size_t kLongSmem = (size_t)kSlots * kLongThreads * (8 + 8 + 4) + (size_t)kLongThreads * 9 * 16;
+
+template <int OP, bool COLLECT>
+__global__ void __launch_bounds__(kLongThreads) k_meta_long(TableDev t, OpArgs a, const uint32_t* __restrict__ sb,
+                                                           const uint32_t* __restrict__ sidx, uint32_t* run_end,
+                                                           const uint64_t* __restrict__ skeys,
+                                                           const SegRec* __restrict__ lrecs, int64_t n,
+                                                           uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
+                                                           int32_t* __restrict__ rsrc) {
+  extern __shared__ uint4 long_smem[];
+  __shared__ BlockCtrs bc;
+  if (a.sc->err) return;
+  const unsigned nl = a.sc->nlong;
+  if (nl == 0) return;
+  block_ctrs_init(bc);
+  uint64_t* K = reinterpret_cast<uint64_t*>(long_smem);  // [slot][thread]
+  uint64_t* Sc = K + kSlots * kLongThreads;
+  int* LW = reinterpret_cast<int*>(Sc + kSlots * kLongThreads);
+  uint4* stage = reinterpret_cast<uint4*>(LW + kSlots * kLongThreads) + threadIdx.x * 9;
+  const uint64_t clock0 = *t.clock;
+  const bool fel_open = !*t.fel_set;
+  const bool lfu_like = t.policy == kLfu || t.policy == kEpochLfu;
+  const bool runs = a.sc->has_runs != 0;
+  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
+  int sd = 0;
+  uint32_t fe_min = 0xFFFFFFFFu;
+  for (int64_t j = (int64_t)blockIdx.x * kLongThreads + threadIdx.x; j < nl; j += (int64_t)gridDim.x * kLongThreads) {
+    const SegRec rec = lrecs[j];
+    const uint64_t rowbase = (uint64_t)rec.b * kSlots;
+    const uint4* dp = reinterpret_cast<const uint4*>(t.digests + rowbase);
+#pragma unroll
+    for (int k = 0; k < 8; k++) stage[k] = dp[k];
+    stage[8] = reinterpret_cast<const uint4*>(t.bits)[rec.b];
+    const ulonglong2* kp = reinterpret_cast<const ulonglong2*>(t.keys + rowbase);
+    const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(t.scores + rowbase);
+#pragma unroll 8
+    for (int s2 = 0; s2 < kSlots / 2; s2++) {
+      const ulonglong2 kk = kp[s2], ss = sp[s2];
+      K[(2 * s2) * kLongThreads + threadIdx.x] = kk.x;
+      K[(2 * s2 + 1) * kLongThreads + threadIdx.x] = kk.y;
+      Sc[(2 * s2) * kLongThreads + threadIdx.x] = ss.x;
+      Sc[(2 * s2 + 1) * kLongThreads + threadIdx.x] = ss.y;
+    }
+    tps_segment<OP, COLLECT, true>(t, a, rec, stage, sb, sidx, run_end, skeys, n, vrow, rrow, rsrc, clock0,
+                                   fel_open, false, lfu_like, runs, ctr, sd, fe_min, LW + threadIdx.x,
+                                   kLongThreads, K + threadIdx.x, Sc + threadIdx.x, kLongThreads);
+  }
   if (fel_open) {
     unsigned m = __reduce_min_sync(kFull, fe_min);
     if ((threadIdx.x & 31) == 0 && m != 0xFFFFFFFFu) atomicMin(&a.sc->first_ev, m);
@@ -1020,7 +1143,7 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual
   if (n > ws.cap_n) {
     const int64_t c = n + n / 4 + 1024;
     if ((e = grow(ws.bkt, c)) || (e = grow(ws.idx, c)) || (e = grow(ws.sbkt, c)) || (e = grow(ws.sidx, c)) ||
-        (e = grow(ws.seg, c)) || (e = grow(ws.aux, c)) || (e = grow(ws.aux2, c)) || (e = grow(ws.skey, 3 * c)) ||
+        (e = grow(ws.seg, c)) || (e = grow(ws.aux, c)) || (e = grow(ws.aux2, c)) || (e = grow(ws.skey, 3 * c)) || (e = grow(ws.lrec, 3 * (c / kLongSeg + 1))) ||
         (e = grow(ws.vrow, c)) || (e = grow(ws.rrow, c)) || (e = grow(ws.rsrc, c)) || (e = grow(ws.skeys, c)))
       return e;
     if (ws.b2) { cudaFree(ws.b2); ws.b2 = nullptr; }
@@ -1072,7 +1195,7 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual
 
 void ws_free(Workspace& ws) {
   ws_free_dual(ws);
-  void* ptrs[] = {ws.bkt, ws.idx, ws.sbkt, ws.sidx, ws.seg, ws.aux, ws.aux2, ws.skey, ws.skeys, ws.vrow, ws.rrow,
+  void* ptrs[] = {ws.bkt, ws.idx, ws.sbkt, ws.sidx, ws.seg, ws.aux, ws.aux2, ws.skey, ws.lrec, ws.skeys, ws.vrow, ws.rrow,
                   ws.lwtab,
                   ws.rsrc,
                   ws.b2, ws.pend,
@@ -1191,7 +1314,8 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       SegRec* recs = reinterpret_cast<SegRec*>(ws.skey);
       const uint8_t fcode = a.op == kOpErase ? kNotFound : a.op == kOpFindOrInsert ? kFound : kUpdated;
       ktimer_begin("segments", s, 2);
-      k_segments<<<(unsigned)((n + 1023) / 1024), 1024, 0, s>>>(ws.sbkt, ws.sidx, a.keys, n, recs, n, ws.sc, ws.aux2,
+      SegRec* lrecs = reinterpret_cast<SegRec*>(ws.lrec);
+      k_segments<<<(unsigned)((n + 1023) / 1024), 1024, 0, s>>>(ws.sbkt, ws.sidx, a.keys, n, recs, n, lrecs, ws.sc, ws.aux2,
                                                                  a.outcomes, ws.vrow, fcode, ws.skeys);
       g_launches++;
       if ((e = run_ends(ws, n, s))) return e;
@@ -1215,6 +1339,21 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       fn<<<(unsigned)(tb < 1 ? 1 : tb), kTpsThreads, smem, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, recs, n, n,
                                                                ws.vrow, ws.rrow, ws.rsrc,
                                                                ws.lwtab);
+      if (n >= kLongSeg) {  // long segments (none in uniform batches: the kernel exits at once)
+        auto* fl = a.op == kOpErase ? k_meta_long<kOpErase, false>
+                   : a.op == kOpFindOrInsert ? k_meta_long<kOpFindOrInsert, false>
+                   : a.collect ? k_meta_long<kOpUpsert, true> : k_meta_long<kOpUpsert, false>;
+        static bool lattr = false;
+        if (!lattr) {
+          for (auto* f : {k_meta_long<kOpErase, false>, k_meta_long<kOpFindOrInsert, false>,
+                          k_meta_long<kOpUpsert, true>, k_meta_long<kOpUpsert, false>})
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLongSmem);
+          lattr = true;
+        }
+        fl<<<(unsigned)num_sms, kLongThreads, kLongSmem, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, lrecs, n,
+                                                              ws.vrow, ws.rrow, ws.rsrc);
+        g_launches++;
+      }
       ktimer_end("apply", s);
       g_launches++;
     } else {
