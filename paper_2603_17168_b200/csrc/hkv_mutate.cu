@@ -1314,7 +1314,12 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       SegRec* recs = reinterpret_cast<SegRec*>(ws.skey);
       const uint8_t fcode = a.op == kOpErase ? kNotFound : a.op == kOpFindOrInsert ? kFound : kUpdated;
       ktimer_begin("segments", s, 2);
-      SegRec* lrecs = reinterpret_cast<SegRec*>(ws.lrec);
+      // The long-segment engine pays when long segments are the rule (batch
+      // >= 16 ops per bucket, configs[0]); in a batch that is sparse over the
+      // buckets (zipf hot buckets among ~1 op per bucket) the few long
+      // segments are better overlapped with everything else inside k_meta_tps.
+      const bool use_long = n >= kLongSeg && (n >> log2_buckets) >= 16;
+      SegRec* lrecs = use_long ? reinterpret_cast<SegRec*>(ws.lrec) : nullptr;
       k_segments<<<(unsigned)((n + 1023) / 1024), 1024, 0, s>>>(ws.sbkt, ws.sidx, a.keys, n, recs, n, lrecs, ws.sc, ws.aux2,
                                                                  a.outcomes, ws.vrow, fcode, ws.skeys);
       g_launches++;
@@ -1339,7 +1344,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       fn<<<(unsigned)(tb < 1 ? 1 : tb), kTpsThreads, smem, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, recs, n, n,
                                                                ws.vrow, ws.rrow, ws.rsrc,
                                                                ws.lwtab);
-      if (n >= kLongSeg) {  // long segments (none in uniform batches: the kernel exits at once)
+      if (use_long) {
         auto* fl = a.op == kOpErase ? k_meta_long<kOpErase, false>
                    : a.op == kOpFindOrInsert ? k_meta_long<kOpFindOrInsert, false>
                    : a.collect ? k_meta_long<kOpUpsert, true> : k_meta_long<kOpUpsert, false>;
