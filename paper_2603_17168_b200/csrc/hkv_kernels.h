@@ -40,8 +40,8 @@ struct Workspace {
   uint64_t* skeys = nullptr; // single mode: keys in sorted (bucket, batch index) order
   uint32_t* vrow = nullptr;  // single mode: destination row of final value writers
   uint32_t* rrow = nullptr;  // single mode: row of a value read
-  int32_t* rsrc = nullptr;
-  int* lwtab = nullptr;       // single mode: per-thread last-writer tables of the metadata pass   // single mode: provenance of a value read (-1 = pre-batch row)
+  int32_t* rsrc = nullptr;   // single mode: provenance of a value read (-1 = pre-batch row)
+  int* lwtab = nullptr;      // single mode: per-thread last-writer tables of the metadata pass
   uint32_t* b2 = nullptr;    // dual: second bucket
   uint32_t* pend = nullptr;  // dual: second pending list
   uint64_t* ek = nullptr;
