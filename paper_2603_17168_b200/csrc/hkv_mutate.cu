@@ -24,6 +24,7 @@
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
+#include <atomic>
 #include <cstdlib>
 #include <string>
 #include <thrust/iterator/reverse_iterator.h>
@@ -1330,12 +1331,16 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
                  : a.op == kOpFindOrInsert ? k_meta_tps<kOpFindOrInsert, false>
                  : a.collect ? k_meta_tps<kOpUpsert, true> : k_meta_tps<kOpUpsert, false>;
       const size_t smem = 2 * kTpsThreads * kTpsStageU4 * sizeof(uint4);
-      static bool attr_set = false;
-      if (!attr_set) {
+      // the dynamic shared-memory opt-in is per device (a process may drive several)
+      int dev = 0;
+      cudaGetDevice(&dev);
+      const unsigned long long dbit = 1ull << (dev & 63);
+      static std::atomic<unsigned long long> attr_set{0};
+      if (!(attr_set.load() & dbit)) {
         for (auto* f : {k_meta_tps<kOpErase, false>, k_meta_tps<kOpFindOrInsert, false>, k_meta_tps<kOpUpsert, true>,
                         k_meta_tps<kOpUpsert, false>})
           cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
+        attr_set.fetch_or(dbit);
       }
       int64_t tb = (n + kTpsThreads - 1) / kTpsThreads;
       const int64_t tcap = (int64_t)num_sms * HKV_TPS_MINB;  // one resident wave
@@ -1348,12 +1353,12 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
         auto* fl = a.op == kOpErase ? k_meta_long<kOpErase, false>
                    : a.op == kOpFindOrInsert ? k_meta_long<kOpFindOrInsert, false>
                    : a.collect ? k_meta_long<kOpUpsert, true> : k_meta_long<kOpUpsert, false>;
-        static bool lattr = false;
-        if (!lattr) {
+        static std::atomic<unsigned long long> lattr{0};
+        if (!(lattr.load() & dbit)) {
           for (auto* f : {k_meta_long<kOpErase, false>, k_meta_long<kOpFindOrInsert, false>,
                           k_meta_long<kOpUpsert, true>, k_meta_long<kOpUpsert, false>})
             cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLongSmem);
-          lattr = true;
+          lattr.fetch_or(dbit);
         }
         fl<<<(unsigned)num_sms, kLongThreads, kLongSmem, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, lrecs, n,
                                                               ws.vrow, ws.rrow, ws.rsrc);

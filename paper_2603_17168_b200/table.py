@@ -331,10 +331,11 @@ class CacheTable:
         k = self._host_keys(keys)
         n = k.numel()
         dim = self.config.value_dim
-        if tuple(values.shape) != (n, dim) or values.dtype != torch.float32:
+        if op == 1:
+            if tuple(values.shape) != (n, dim) or values.dtype != torch.float32 or not values.is_contiguous():
+                raise ValueError("values_inout must be a C-contiguous float32 array of shape (n, value_dim)")
+        elif tuple(values.shape) != (n, dim) or values.dtype != torch.float32:
             raise ValueError("values must have shape (len(keys), value_dim)")
-        if op == 1 and not values.is_contiguous():
-            raise ValueError("values_inout must be a C-contiguous float32 array of shape (n, value_dim)")
         v = values.contiguous()
         s = None  # table.py:178-188
         if self.config.score_policy is PolicyId.kCustomized:
@@ -509,6 +510,8 @@ class CacheTable:
     def find_or_insert(self, keys, values_inout, scores=None, *, ticks=None, clock_advance: int = 0):
         """Present keys: copy the stored value out and refresh the score;
         absent keys: upsert the caller's value (table.py:535-551)."""
+        if ticks is None and self._host_call(keys, values_inout, scores):
+            return self._upsert_host(1, keys, values_inout, scores, clock_advance)
         k, np_mode = self._keys_in(keys)
         n = k.numel()
         dim = self.config.value_dim

@@ -393,6 +393,16 @@ def test_host_buffer_entry_points(hkv, mode, pinned):
             assert v2 is out and np.array_equal(f2.numpy(), fo)
             exp = np.where(fo[:, None], vo, base)
             assert v2.numpy().tobytes() == exp.tobytes()
+            # find_or_insert with a host values_inout: found rows come back in place
+            fk = np.concatenate([keys[: n // 4], rng.integers(2**42, 2**43, size=n // 4, dtype=np.uint64)])
+            fv = rng.standard_normal((len(fk), dim)).astype(np.float32)
+            fsc = rng.integers(0, 2**20, size=len(fk), dtype=np.uint64) if policy == "kCustomized" else None
+            fvh = pin(torch.from_numpy(fv.copy()))
+            fo_t = t.find_or_insert(pin(torch.from_numpy(fk.view(np.int64))), fvh,
+                                    None if fsc is None else pin(torch.from_numpy(fsc.view(np.int64))))
+            fv_o = fv.copy()
+            fo_o = o.find_or_insert(fk, fv_o, fsc)
+            assert np.array_equal(fo_t.numpy(), fo_o) and fvh.numpy().tobytes() == fv_o.tobytes()
         assert_same_state(t, o)
     # sentinel keys through the host path: ValueError, no mutation
     t = make_table(hkv, 1024, 4, mode)

@@ -130,6 +130,25 @@ def c2_extras(reps, lg=27):
               "outcomes": outcome_mix(o)})
         ms, o = timed(lambda r: t.erase(q), reps, after=t.restore)
         emit({**base, "op": "erase_hit", "ms": ms, "bkvs": B / ms / 1e6, "outcomes": outcome_mix(o)})
+        # export_batch_if through the C-ABI into device buffers: 1M entries with
+        # score >= 1 (the service's native predicate) from cursor 0
+        import ctypes as C
+
+        ok = torch.empty(B, dtype=torch.int64, device="cuda")
+        ov = torch.empty((B, dim), dtype=torch.float32, device="cuda")
+        osc = torch.empty(B, dtype=torch.int64, device="cuda")
+        cnt, nxt = C.c_int64(), C.c_int64()
+
+        def exp(r):
+            hkv._lib.check(t._lib.hkv_export(t._h, 0, B, 1, 1, None, 0, C.c_void_p(ok.data_ptr()),
+                                             C.c_void_p(ov.data_ptr()), C.c_void_p(osc.data_ptr()), C.byref(cnt),
+                                             C.byref(nxt), t._sp()))
+
+        ms, _ = timed(exp, reps)
+        scanned = nxt.value if nxt.value > 0 else cap
+        emit({**base, "op": "export_batch_if_1M", "ms": ms, "rows_scanned": scanned, "exported": cnt.value,
+              "scan_gbs": round(scanned * 16 / ms / 1e6, 1),
+              "bkvs": cnt.value / ms / 1e6})
         del t
         torch.cuda.empty_cache()
 
