@@ -106,6 +106,7 @@ int cuda_fail(cudaError_t e, const char* where) {
 // hkv_upsert_host): a copy stream, a ring of chunk slots and their events.
 constexpr int kRing = 3;
 struct HostStage {
+  std::mutex mu;  // the staging buffers serve one host-buffer call at a time (readers may run concurrently)
   cudaStream_t copy = nullptr;
   cudaEvent_t ready[kRing] = {}, done[kRing] = {}, start = nullptr, vals = nullptr;
   uint64_t* keys = nullptr;  // find: kRing chunk slots; upsert: the batch
@@ -465,6 +466,7 @@ int hkv_find_host(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uin
   if (n == 0) return HKV_OK;
   cudaStream_t s = (cudaStream_t)stream;
   HostStage& h = t->stage(s);
+  std::lock_guard<std::mutex> hold(h.mu);
   cudaError_t e = h.init();
   if (e) return cuda_fail(e, "hkv_find_host init");
   const int64_t dim = t->cfg.value_dim;
@@ -520,6 +522,7 @@ int hkv_upsert_host(hkv_table* t, int32_t op, const uint64_t* keys, float* value
   if (n > 0xFFFFFFFEll) return fail(HKV_EINVAL, "batch too large");
   cudaStream_t s = (cudaStream_t)stream;
   HostStage& h = t->stage(s);
+  std::lock_guard<std::mutex> hold(h.mu);
   cudaError_t e = h.init();
   if (e) return cuda_fail(e, "hkv_upsert_host init");
   const int64_t dim = t->cfg.value_dim;

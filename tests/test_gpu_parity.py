@@ -414,3 +414,39 @@ def test_host_buffer_entry_points(hkv, mode, pinned):
     for k in ("keys", "digests", "scores", "values"):
         assert before[k].tobytes() == after[k].tobytes()
     assert before["clock"] == after["clock"] and before["size"] == after["size"]
+
+
+def test_host_buffer_concurrent_readers(hkv):
+    """Reader groups may overlap (gate.py role matrix): two host threads
+    calling find through the host-buffer path on one table and stream get
+    their own correct results (the staging ring is held per call)."""
+    import threading
+
+    cap, dim = 2**16, 16
+    t = make_table(hkv, cap, dim)
+    o = OracleTable(cap, dim)
+    rng = np.random.default_rng(5)
+    keys = rng.integers(1, 2**50, size=30_000, dtype=np.uint64)
+    vals = rng.standard_normal((len(keys), dim)).astype(np.float32)
+    t.insert_or_assign(keys, vals)
+    o.insert_or_assign(keys, vals)
+    qs = [np.concatenate([keys[j::7], rng.integers(2**51, 2**52, size=5000, dtype=np.uint64)]) for j in range(2)]
+    exp = [o.find(q) for q in qs]
+    errs = []
+
+    def worker(j):
+        try:
+            qh = torch.from_numpy(qs[j].view(np.int64)).pin_memory()
+            for _ in range(6):
+                f, v = t.find(qh)
+                if not (np.array_equal(f.numpy(), exp[j][0]) and v.numpy().tobytes() == exp[j][1].tobytes()):
+                    errs.append(j)
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(j,)) for j in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs, errs
