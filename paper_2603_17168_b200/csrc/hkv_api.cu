@@ -183,11 +183,27 @@ struct hkv_table {
   TableScalars* snap_sc = nullptr;
   std::mutex mu;
   std::map<cudaStream_t, Workspace> ws;
+  std::map<cudaStream_t, std::mutex> wsmu;
   std::map<cudaStream_t, HostStage> hs;
 
-  Workspace& workspace(cudaStream_t s) {
-    std::lock_guard<std::mutex> g(mu);
-    return ws[s];
+  // A stream's scratch serves one call at a time: the lease holds its lock
+  // from the (re)allocation through the launches that use it, so concurrent
+  // callers on one stream (overlapping reader groups) never see a buffer
+  // freed by another caller's growth.
+  struct WsLease {
+    std::unique_lock<std::mutex> lk;
+    Workspace& w;
+    operator Workspace&() { return w; }
+  };
+  WsLease workspace(cudaStream_t s) {
+    std::mutex* m;
+    Workspace* w;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      m = &wsmu[s];
+      w = &ws[s];
+    }
+    return WsLease{std::unique_lock<std::mutex>(*m), *w};
   }
   HostStage& stage(cudaStream_t s) {
     std::lock_guard<std::mutex> g(mu);
@@ -394,8 +410,9 @@ int hkv_find(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uint8_t*
   CHECK_T();
   if (n && (!keys || !found)) return fail(HKV_EINVAL, "null keys/found");
   uint32_t* rows = nullptr;
+  auto lease = t->workspace((cudaStream_t)stream);
   if (out && n > 0) {
-    Workspace& ws = t->workspace((cudaStream_t)stream);
+    Workspace& ws = lease.w;
     cudaError_t e0 = ws_reserve(ws, n, (int)t->cfg.value_dim, 0, false);
     if (e0) return cuda_fail(e0, "hkv_find workspace");
     rows = ws.vrow;
@@ -477,7 +494,8 @@ int hkv_find_host(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uin
   if ((e = grow_dev(h.bytes, h.bytes_cap, (size_t)(kRing * chunk)))) return cuda_fail(e, "hkv_find_host staging");
   if (out && (e = grow_dev(h.rows, h.rows_cap, (size_t)(kRing * chunk * dim))))
     return cuda_fail(e, "hkv_find_host staging");
-  Workspace& ws = t->workspace(s);
+  auto lease = t->workspace(s);
+  Workspace& ws = lease.w;
   if (out && (e = ws_reserve(ws, chunk, (int)dim, 0, false))) return cuda_fail(e, "hkv_find_host workspace");
   if ((e = cudaEventRecord(h.start, s)) || (e = cudaStreamWaitEvent(h.copy, h.start, 0)))
     return cuda_fail(e, "hkv_find_host");
