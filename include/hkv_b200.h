@@ -122,6 +122,24 @@ int hkv_upsert_host(hkv_table *t, int32_t op, const uint64_t *keys, float *value
                     const uint64_t *scores, int64_t n, uint8_t *outcomes, const uint64_t *ticks,
                     uint64_t clock_advance, hkv_stream stream);
 
+/* Sharded find over NVLink peer memory (no reference
+ * counterpart: the reference leaves sharding to the application).  A
+ * hash-sharded table of `world` (power of two) equal shards, contiguous
+ * bucket ranges: global bucket = fmix64(key) & (world * buckets - 1), owner =
+ * global bucket / buckets.  hkv_find_peer probes the owner shard's digest
+ * line and keys and copies its value row in place — no routing, no
+ * all-to-all — with results identical to the routed find.  Shards must keep
+ * every value row in HBM (fast_tier_budget == buckets), single mode, digest
+ * filter on.  Structural counters are not updated by peer finds.
+ *   hkv_ipc_handles   3 cudaIpcMemHandle_t (keys, digests, values) of a shard
+ *   hkv_set_peers     world x 3 handles gathered from every rank (own slot ignored)
+ *   hkv_set_peers_local  shards of the same process (other devices need P2P) */
+int hkv_ipc_handles(hkv_table *t, void *out, int64_t out_bytes);
+int hkv_set_peers(hkv_table *t, int32_t world, int32_t rank, const void *handles);
+int hkv_set_peers_local(hkv_table *t, int32_t world, hkv_table *const *shards);
+int hkv_find_peer(hkv_table *t, const uint64_t *keys, int64_t n, float *out, uint8_t *found,
+                  int32_t zero_misses, hkv_stream stream);
+
 /* assign (table.py:438-442) when values != NULL; assign_scores (444-449) with
  * explicit scores (kCustomized) or refresh != 0.  Last duplicate wins.
  * Refresh ticks: NULL -> clock + (found keys before i) + 1 and clock += found

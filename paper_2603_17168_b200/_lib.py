@@ -46,6 +46,10 @@ SIGNATURES = {
     "hkv_find_ptr": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "hkv_upsert": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _u64, _vp]),
     "hkv_find_host": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _i32, _vp]),
+    "hkv_ipc_handles": (C.c_int, [_vp, _vp, _i64]),
+    "hkv_set_peers": (C.c_int, [_vp, _i32, _i32, _vp]),
+    "hkv_set_peers_local": (C.c_int, [_vp, _i32, _vp]),
+    "hkv_find_peer": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _i32, _vp]),
     "hkv_upsert_host": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _u64, _vp]),
     "hkv_assign": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _u64, _vp]),
     "hkv_erase": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),

@@ -181,6 +181,11 @@ struct hkv_table {
   uint64_t* snap_smin = nullptr;
   uint32_t* snap_svalid = nullptr;
   TableScalars* snap_sc = nullptr;
+  // peer views of the other shards (hkv_set_peers*): device array + what was opened
+  PeerView* peers_dev = nullptr;
+  int peer_world = 0;
+  int peer_llog2b = 0;
+  std::vector<void*> ipc_opened;
   std::mutex mu;
   std::map<cudaStream_t, Workspace> ws;
   std::map<cudaStream_t, std::mutex> wsmu;
@@ -241,6 +246,8 @@ void free_table(hkv_table* t) {
   else if (t->vover) cudaFree(t->vover);
   for (auto& kv : t->ws) ws_free(kv.second);
   for (auto& kv : t->hs) kv.second.release();
+  for (void* p : t->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (t->peers_dev) cudaFree(t->peers_dev);
   delete t;
 }
 
@@ -579,6 +586,94 @@ int hkv_upsert_host(hkv_table* t, int32_t op, const uint64_t* keys, float* value
   }
   if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "hkv_upsert_host");
   return HKV_OK;
+}
+
+// ---- sharded find over peer memory ----------------------------------------
+static int peer_ready(hkv_table* t) {
+  if (t->cfg.mode != HKV_MODE_SINGLE) return fail(HKV_EINVAL, "peer find needs single mode");
+  if (!t->cfg.digest_filter) return fail(HKV_EINVAL, "peer find needs digest_filter");
+  if (t->fast_rows != (uint64_t)t->cfg.capacity)
+    return fail(HKV_EINVAL, "peer find needs every value row in HBM (fast_tier_budget == buckets)");
+  return HKV_OK;
+}
+
+static int install_peers(hkv_table* t, int world, const std::vector<PeerView>& v) {
+  if (t->peers_dev) cudaFree(t->peers_dev);
+  t->peers_dev = nullptr;
+  cudaError_t e = cudaMalloc((void**)&t->peers_dev, sizeof(PeerView) * (size_t)world);
+  if (!e) e = cudaMemcpy(t->peers_dev, v.data(), sizeof(PeerView) * (size_t)world, cudaMemcpyHostToDevice);
+  if (e) return cuda_fail(e, "hkv_set_peers");
+  t->peer_world = world;
+  t->peer_llog2b = t->log2b;
+  return HKV_OK;
+}
+
+int hkv_ipc_handles(hkv_table* t, void* out, int64_t out_bytes) {
+  if (!t || !out) return fail(HKV_EINVAL, "null argument");
+  if (out_bytes < 3 * (int64_t)sizeof(cudaIpcMemHandle_t)) return fail(HKV_EINVAL, "handle buffer too small");
+  if (int rc = peer_ready(t)) return rc;
+  DeviceGuard _g(t->cfg.device);
+  cudaIpcMemHandle_t* h = reinterpret_cast<cudaIpcMemHandle_t*>(out);
+  cudaError_t e;
+  if ((e = cudaIpcGetMemHandle(&h[0], t->keys)) || (e = cudaIpcGetMemHandle(&h[1], t->digests)) ||
+      (e = cudaIpcGetMemHandle(&h[2], t->vfast)))
+    return cuda_fail(e, "hkv_ipc_handles");
+  return HKV_OK;
+}
+
+int hkv_set_peers(hkv_table* t, int32_t world, int32_t rank, const void* handles) {
+  if (!t || !handles || world < 1 || rank < 0 || rank >= world || (world & (world - 1)))
+    return fail(HKV_EINVAL, "bad peer arguments (world must be a power of two)");
+  if (int rc = peer_ready(t)) return rc;
+  DeviceGuard _g(t->cfg.device);
+  const cudaIpcMemHandle_t* h = reinterpret_cast<const cudaIpcMemHandle_t*>(handles);
+  std::vector<PeerView> v((size_t)world);
+  for (int r = 0; r < world; r++) {
+    if (r == rank) {
+      v[r] = PeerView{t->keys, t->digests, t->vfast};
+      continue;
+    }
+    void* p[3];
+    for (int k = 0; k < 3; k++) {
+      cudaError_t e = cudaIpcOpenMemHandle(&p[k], h[3 * r + k], cudaIpcMemLazyEnablePeerAccess);
+      if (e) return cuda_fail(e, "hkv_set_peers: cudaIpcOpenMemHandle");
+      t->ipc_opened.push_back(p[k]);
+    }
+    v[r] = PeerView{(const uint64_t*)p[0], (const uint8_t*)p[1], (const float*)p[2]};
+  }
+  return install_peers(t, world, v);
+}
+
+int hkv_set_peers_local(hkv_table* t, int32_t world, hkv_table* const* shards) {
+  if (!t || !shards || world < 1 || (world & (world - 1))) return fail(HKV_EINVAL, "bad peer arguments");
+  if (int rc = peer_ready(t)) return rc;
+  DeviceGuard _g(t->cfg.device);
+  std::vector<PeerView> v((size_t)world);
+  for (int r = 0; r < world; r++) {
+    hkv_table* o = shards[r];
+    if (!o || o->cfg.capacity != t->cfg.capacity || o->cfg.value_dim != t->cfg.value_dim)
+      return fail(HKV_EINVAL, "shards must share capacity and value_dim");
+    if (int rc = peer_ready(o)) return rc;
+    if (o->cfg.device != t->cfg.device) {
+      cudaError_t e = cudaDeviceEnablePeerAccess(o->cfg.device, 0);
+      if (e && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "hkv_set_peers_local: peer access");
+      cudaGetLastError();
+    }
+    v[r] = PeerView{o->keys, o->digests, o->vfast};
+  }
+  return install_peers(t, world, v);
+}
+
+int hkv_find_peer(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uint8_t* found, int32_t zero_misses,
+                  hkv_stream stream) {
+  CHECK_T();
+  if (!t->peers_dev) return fail(HKV_EINVAL, "no peers set (hkv_set_peers)");
+  if (n && (!keys || !found || !out)) return fail(HKV_EINVAL, "null keys/out/found");
+  const uint64_t gmask = ((uint64_t)t->buckets * (uint64_t)t->peer_world) - 1;
+  launch_find_peer(t->peers_dev, gmask, t->peer_llog2b, (int)t->cfg.value_dim, keys, n, out, found, zero_misses,
+                   t->dev.err, (cudaStream_t)stream, t->num_sms);
+  cudaError_t e = cudaGetLastError();
+  return e ? cuda_fail(e, "hkv_find_peer") : HKV_OK;
 }
 
 int hkv_erase(hkv_table* t, const uint64_t* keys, int64_t n, uint8_t* outcomes, hkv_stream stream) {

@@ -224,6 +224,98 @@ __global__ void __launch_bounds__(256) k_find_fused(TableDev t, const uint64_t* 
   block_ctrs_flush(bc, t.counters, nullptr, ctr, 0);
 }
 
+// Sharded find over peer memory: each thread hashes its key,
+// finds the owner shard from the global bucket, probes the owner's digest
+// line and candidate keys in place (NVLink loads for a remote owner), and the
+// warp then copies its 32 rows out of the owners' value arenas, as
+// k_find_fused does locally.  Replaces route -> all-to-all -> local find ->
+// all-to-all; results are bit-identical to the routed path (the shard's
+// bucket is the global table's bucket).  Structural counters are not updated
+// (they belong to the owner shard).
+template <bool kZero, int VEC>
+__global__ void __launch_bounds__(256) k_find_peer(const PeerView* __restrict__ views, uint64_t gmask, int llog2b,
+                                                   int dim, const uint64_t* __restrict__ keys, int64_t n,
+                                                   uint8_t* __restrict__ found, float* __restrict__ out, int* err) {
+  using V = typename std::conditional<VEC == 4, uint4, float>::type;
+  const unsigned lane = threadIdx.x & 31u;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int nv = dim / VEC;
+  const uint64_t lmask = (1ull << llog2b) - 1;
+  int bad = 0;
+  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    const float* src = nullptr;
+    if (i < n) {
+      const uint64_t key = __ldg(keys + i);
+      bad |= key >= kLockedKey;
+      const uint64_t h = fmix64(key);
+      const uint32_t d = digest_of(h);
+      const uint64_t gb = h & gmask;
+      const PeerView v = views[gb >> llog2b];
+      const uint64_t rowbase = (gb & lmask) * kSlots;
+      const uint4* dp = reinterpret_cast<const uint4*>(v.digests + rowbase);
+      uint4 w[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) w[k] = dp[k];
+      int hit = -1;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        uint32_t m = hit < 0 ? (match16(w[2 * q], d) | (match16(w[2 * q + 1], d) << 16)) : 0u;
+        while (m) {
+          const int j = __ffs(m) - 1;
+          m &= m - 1;
+          const uint64_t k2 = v.keys[rowbase + 32 * q + j];
+          if (k2 == key) {
+            hit = 32 * q + j;
+            m = 0;
+          }
+        }
+      }
+      found[i] = hit >= 0;
+      if (hit >= 0) src = v.values + (rowbase + hit) * (uint64_t)dim;
+    }
+    const int nk = (n - base < 32) ? (int)(n - base) : 32;
+    const int total = nk * nv;
+    for (int v0 = 0; v0 < total; v0 += 32 * 8) {
+      V x[8];
+      const float* rs[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int e = v0 + 32 * u + (int)lane;
+        const int k = e < total ? e / nv : 0;
+        rs[u] = reinterpret_cast<const float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), k));
+        if (e < total && rs[u]) x[u] = reinterpret_cast<const V*>(rs[u])[e - k * nv];
+        else x[u] = V{};
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int e = v0 + 32 * u + (int)lane;
+        if (e >= total || (!kZero && !rs[u])) continue;
+        const int k = e / nv;
+        reinterpret_cast<V*>(out + (base + k) * (int64_t)dim)[e - k * nv] = x[u];
+      }
+    }
+  }
+  if (bad) atomicOr(err, 1);
+}
+
+void launch_find_peer(const PeerView* views, uint64_t gmask, int llog2b, int dim, const uint64_t* keys, int64_t n,
+                      float* out, uint8_t* found, int zero_misses, int* err, cudaStream_t s, int num_sms) {
+  if (n <= 0) return;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+  const bool v4 = dim % 4 == 0 && ((uintptr_t)out & 15) == 0;
+  if (v4) {
+    if (zero_misses) k_find_peer<true, 4><<<(unsigned)blocks, 256, 0, s>>>(views, gmask, llog2b, dim, keys, n, found, out, err);
+    else k_find_peer<false, 4><<<(unsigned)blocks, 256, 0, s>>>(views, gmask, llog2b, dim, keys, n, found, out, err);
+  } else {
+    if (zero_misses) k_find_peer<true, 1><<<(unsigned)blocks, 256, 0, s>>>(views, gmask, llog2b, dim, keys, n, found, out, err);
+    else k_find_peer<false, 1><<<(unsigned)blocks, 256, 0, s>>>(views, gmask, llog2b, dim, keys, n, found, out, err);
+  }
+  g_launches++;
+}
+
 template <int MODE>
 static void launch_probe(const TableDev& t, const uint64_t* keys, int64_t n, uint8_t* found, uint8_t* tier,
                          int64_t* offset, uint32_t* rows, cudaStream_t s, int num_sms) {

@@ -81,6 +81,19 @@ enum { kOpUpsert = 0, kOpFindOrInsert = 1, kOpErase = 2 };
 
 // mode 0: find (misses untouched), 3: find (misses zero-filled), 1: contains, 2: find_ptr.
 // rows: n-entry scratch for modes 0/3.
+// One shard of a hash-sharded table as seen by another rank (peer memory:
+// CUDA IPC over NVLink, or a table of the same process).
+struct PeerView {
+  const uint64_t* keys;
+  const uint8_t* digests;
+  const float* values;  // fast tier: every row of the shard (peer find needs fast_tier_budget == buckets)
+};
+// find over the whole sharded table by reading the owner shard's bucket
+// directly (no routing, no all-to-all): global bucket = h & gmask, owner =
+// global bucket >> llog2b.
+void launch_find_peer(const PeerView* views, uint64_t gmask, int llog2b, int dim, const uint64_t* keys, int64_t n,
+                      float* out, uint8_t* found, int zero_misses, int* err, cudaStream_t s, int num_sms);
+
 void launch_find(const TableDev& t, const uint64_t* keys, int64_t n, float* out, uint8_t* found,
                  uint8_t* tier, int64_t* offset, int mode, uint32_t* rows, cudaStream_t s, int num_sms);
 

@@ -107,7 +107,30 @@ class ShardedCacheTable:
         return x.to(torch.uint8) if x.dtype == torch.bool else x
 
     # ----- reader ops -----------------------------------------------------------
+    def enable_peer_find(self):
+        """Collective: exchange CUDA IPC handles of every shard's keys,
+        digests and value arena, so find() reads the owner shard over NVLink
+        instead of routing keys and rows through two all-to-alls
+        (hkv_find_peer; every value row must be in HBM)."""
+        from . import _lib
+
+        lib = self.local._lib
+        buf = (C.c_char * 192)()
+        _lib.check(lib.hkv_ipc_handles(self.local._h, buf, 192))
+        allh = [None] * self.world
+        dist.all_gather_object(allh, bytes(buf), group=self.group)
+        blob = b"".join(allh)
+        _lib.check(lib.hkv_set_peers(self.local._h, self.world, self.rank,
+                                     (C.c_char * len(blob)).from_buffer_copy(blob)))
+        self._peer = True
+
     def find(self, keys: torch.Tensor):
+        if getattr(self, "_peer", False):
+            # every rank is in the find phase (no shard mutates while peers read it)
+            dist.barrier(group=self.group)
+            f, v = self.local._find_peer(keys)
+            dist.barrier(group=self.group)
+            return f, v
         perm, send, recv = self._route(keys)
         rk = self._a2a(keys[perm], send, recv)
         f, v = self.local.find(rk)

@@ -353,6 +353,27 @@ class CacheTable:
         self._check_device_error()
         return outcomes
 
+    # ----- sharded find over peer memory (sharded.py) -------------------------
+    def _set_peers_local(self, shards):
+        """Shards of one process (same device, or P2P-capable devices) as the
+        peer set of a sharded table; shard r owns global buckets
+        [r * B, (r + 1) * B)."""
+        arr = (C.c_void_p * len(shards))(*[s._h.value for s in shards])
+        _lib.check(self._lib.hkv_set_peers_local(self._h, len(shards), arr))
+
+    def _find_peer(self, keys: torch.Tensor, out=None):
+        k = keys.contiguous().view(torch.int64)
+        n = k.numel()
+        dim = self.config.value_dim
+        zero = 1 if out is None else 0
+        if out is None:
+            out = torch.empty((n, dim), dtype=torch.float32, device=self.device)
+        found = torch.empty(n, dtype=torch.bool, device=self.device)
+        with self.gate.acquire(Role.Reader, self._stream()):
+            _lib.check(self._lib.hkv_find_peer(self._h, _ptr(k), n, _ptr(out), _ptr(found), zero, self._sp()))
+        self._check_device_error()
+        return found, out
+
     def contains(self, keys):
         k, np_mode = self._keys_in(keys)
         n = k.numel()

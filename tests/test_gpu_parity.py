@@ -450,3 +450,36 @@ def test_host_buffer_concurrent_readers(hkv):
     for x in th:
         x.join()
     assert not errs, errs
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_find_virtual_shards(hkv, world):
+    """hkv_find_peer over `world` shards of one process (same device: the
+    code path of NVLink peer memory, without IPC) equals the global oracle
+    table bucket for bucket: found flags and rows bit-exact, misses zeroed."""
+    from paper_2603_17168_b200.workloads import fmix64_array
+
+    cap_l, dim = 128 * 256, 12
+    shards = [make_table(hkv, cap_l, dim) for _ in range(world)]
+    o = OracleTable(cap_l * world, dim)
+    rng = np.random.default_rng(9)
+    bl = cap_l // 128
+    gmask = np.uint64(bl * world - 1)
+    for step in range(3):
+        keys = rng.integers(1, 2**60, size=40_000, dtype=np.uint64)
+        vals = rng.standard_normal((len(keys), dim)).astype(np.float32)
+        o.insert_or_assign(keys, vals)
+        owner = ((fmix64_array(keys) & gmask) // np.uint64(bl)).astype(np.int64)
+        for r in range(world):
+            sel = owner == r
+            if sel.any():
+                shards[r].insert_or_assign(keys[sel], vals[sel])
+    for s in shards:
+        s._set_peers_local(shards)
+    q = np.concatenate([keys[::3], rng.integers(2**61, 2**62, size=7000, dtype=np.uint64)])
+    fo, vo = o.find(q)
+    qd = torch.from_numpy(q.view(np.int64)).cuda()
+    for s in shards:  # every rank sees the whole table
+        f, v = s._find_peer(qd)
+        assert np.array_equal(f.cpu().numpy(), fo)
+        assert v.cpu().numpy().tobytes() == vo.tobytes()

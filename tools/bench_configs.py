@@ -248,15 +248,51 @@ def dual(reps, lg=27):
         torch.cuda.empty_cache()
 
 
+def peer(reps, lg=27, world=2):
+    """Sharded find over peer memory, `world` virtual shards of 2^lg / world
+    slots on this one GPU (hkv_find_peer with same-process peers: the kernel
+    path of NVLink peer reads, minus NVLink), vs the local find of one table
+    of the same total size."""
+    cap, dim = 2**lg, 64
+    cl = cap // world
+    bl = cl // 128
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    shards = [hkv.CacheTable(hkv.TableConfig(capacity=cl, value_dim=dim, score_policy="kLru")) for _ in range(world)]
+    for s in shards:
+        s.validate_keys = False
+    vals = torch.randn((B, dim), device="cuda", generator=gen)
+    off = 0
+    while sum(s.size() for s in shards) < cap // 2:
+        k = W.uniform_distinct_keys_torch(B, 0, stream_offset=off)
+        off += B
+        owner = torch.div(W.fmix64_torch(k) & (bl * world - 1), bl, rounding_mode="floor")
+        for r in range(world):
+            sel = owner == r
+            shards[r].insert_or_assign(k[sel].contiguous(), vals[: int(sel.sum())])
+    for s in shards:
+        s._set_peers_local(shards)
+    q = W.uniform_distinct_keys_torch(B, 0, stream_offset=int(torch.randint(0, off - B, (1,)).item()))
+    out = torch.empty((B, dim), device="cuda")
+    ms, (f, _) = timed(lambda r: shards[0]._find_peer(q, out), reps)
+    emit({"config": "C5-virtual", "op": "find_peer", "shards": world, "capacity": cap, "dim": dim,
+          "lambda": round(sum(s.size() for s in shards) / cap, 4), "hit_rate": float(f.float().mean().item()),
+          "ms": ms, "bkvs": B / ms / 1e6,
+          "note": "all shards on one GPU: measures the peer-find kernel, not NVLink"})
+    del shards
+    torch.cuda.empty_cache()
+
+
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--only", default="c1,c2x,c3,c4,dual")
+    p.add_argument("--only", default="c1,c2x,c3,c4,dual,peer")
     p.add_argument("--reps", type=int, default=5)
     p.add_argument("--lg", type=int, default=27)
     a = p.parse_args()
     torch.cuda.set_device(0)
     which = set(a.only.split(","))
     t0 = time.time()
+    if "peer" in which:
+        peer(a.reps, a.lg)
     if "c1" in which:
         c1(a.reps)
     if "c2x" in which:
