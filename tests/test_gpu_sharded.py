@@ -106,3 +106,55 @@ def test_sharded_one_rank_nccl_equals_oracle(policy):
         assert state["clock"] == g.clock and st.clock == g.clock
     finally:
         dist.destroy_process_group()
+
+
+def _peer_ipc_worker(rank, world, port, cap_l, dim, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2603_17168_b200 as hkv
+        from paper_2603_17168_b200.sharded import ShardedCacheTable
+        from paper_2603_17168_b200.workloads import fmix64_array
+
+        st = ShardedCacheTable(hkv.TableConfig(capacity=cap_l * world, value_dim=dim))
+        o = OracleTable(cap_l * world, dim)
+        rng = np.random.default_rng(3)  # same stream on every rank
+        bl = cap_l // 128
+        keys = rng.integers(1, 2**60, size=30_000, dtype=np.uint64)
+        vals = rng.standard_normal((len(keys), dim)).astype(np.float32)
+        o.insert_or_assign(keys, vals)
+        owner = ((fmix64_array(keys) & np.uint64(bl * world - 1)) // np.uint64(bl)).astype(np.int64)
+        sel = owner == rank
+        st.local.insert_or_assign(keys[sel], vals[sel])
+        st.enable_peer_find()  # IPC handles over the gloo group, opened across processes
+        q = np.concatenate([keys[rank::2], rng.integers(2**61, 2**62, size=3000, dtype=np.uint64)])
+        f, v = st.find(torch.from_numpy(q.view(np.int64)).cuda())
+        fo, vo = o.find(q)
+        ok = np.array_equal(f.cpu().numpy(), fo) and v.cpu().numpy().tobytes() == vo.tobytes()
+        ret[rank] = 1 if ok else 0
+        dist.barrier()  # keep every shard alive until all peers finished reading it
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_find_ipc_two_processes():
+    """hkv_find_peer across PROCESSES: two ranks (gloo plumbing) each own a
+    shard on this GPU, exchange CUDA IPC handles and find over the other
+    process's memory — the multi-GPU NVLink path with both ends on one
+    device.  Bit-exact against the global oracle table."""
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    ret = ctx.Array("i", [0, 0])
+    procs = [ctx.Process(target=_peer_ipc_worker, args=(r, 2, port, 128 * 128, 8, ret)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert list(ret) == [1, 1]
