@@ -65,6 +65,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--quick", action="store_true", help="2^24 slots, for profiling runs")
+    p.add_argument("--routed-find", action="store_true",
+                   help="sharded runs: route finds through two all-to-alls instead of reading the owner shard "
+                        "over NVLink peer memory (hkv_find_peer, the default)")
     p.add_argument("--force-sharded", action="store_true",
                    help="run the sharded (multi-GPU) path even at world size 1 (launch under torchrun)")
     a = p.parse_args()
@@ -558,6 +561,18 @@ def run_sharded(a, rank, world):
         t.insert_or_assign(k, vals[:n])
         off += n
     t.local.snapshot()
+    peer = False
+    if not a.routed_find:
+        try:
+            t.enable_peer_find()
+            peer = True
+        except Exception as ex:  # IPC unavailable (container policy, no P2P): keep the routed find
+            print(f"rank {rank}: peer find unavailable ({ex}); routed find", file=sys.stderr)
+        ok = torch.tensor([1 if peer else 0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if peer and not ok.item():
+            t._peer = False  # every rank must take the same path
+            peer = False
     gen = torch.Generator(device="cuda").manual_seed(100 + rank)
     n_steps = a.warmup + a.steps
     qidx = [torch.randint(0, target, (B,), device="cuda", generator=gen) for _ in range(n_steps)]
@@ -639,7 +654,9 @@ def run_sharded(a, rank, world):
                 "scaling": "weak", "vs_baseline": None, "dtype": "u64 keys, f32 values",
                 "data": "synthetic (uniform_distinct_keys fill; resident-key queries; fresh-key inserts)",
                 "config": {"workload": f"hash-sharded table {cap} slots over {world} GPUs "
-                                       "(contiguous bucket ranges, NCCL all-to-all routing), dim 64, lambda 0.5; "
+                                       "(contiguous bucket ranges, NCCL all-to-all routing"
+                                       + (", find over NVLink peer memory" if peer else "")
+                                       + "), dim 64, lambda 0.5; "
                                        "per rank and step: find 1M resident keys + insert_or_assign 1M fresh keys",
                            "capacity_per_gpu": cap_local, "batch_per_gpu": B,
                            "l2": "inputs larger than L2 (34 GB per GPU); metadata restore between steps",
