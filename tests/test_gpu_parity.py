@@ -483,3 +483,18 @@ def test_peer_find_virtual_shards(hkv, world):
         f, v = s._find_peer(qd)
         assert np.array_equal(f.cpu().numpy(), fo)
         assert v.cpu().numpy().tobytes() == vo.tobytes()
+
+
+def test_peer_find_preconditions(hkv):
+    """Peer find needs every shard's value rows in HBM, single mode and the
+    digest filter: anything else is a usage error before any launch."""
+    t = make_table(hkv, 128 * 64, 8)
+    tiered = make_table(hkv, 128 * 64, 8, budget=8)
+    dual = make_table(hkv, 128 * 64, 8, mode="dual")
+    for bad in (tiered, dual):
+        with pytest.raises(ValueError):
+            bad._set_peers_local([bad])
+    with pytest.raises(ValueError):
+        t._set_peers_local([t, tiered])
+    with pytest.raises(ValueError):  # no peers set yet
+        t._find_peer(torch.ones(4, dtype=torch.int64, device="cuda"))
