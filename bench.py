@@ -529,6 +529,9 @@ def run_single(a):
         "insert_or_assign_bkvs_mean": round(statistics.mean(ins_rates), 4),
         "find_variation_over_lambda": round((max(find_rates) - min(find_rates)) / max(find_rates), 4),
         "insert_variation_over_lambda": round((max(ins_rates) - min(ins_rates)) / max(ins_rates), 4),
+        # per-op context only (vs_baseline stays null: no published number for this combined metric):
+        # the paper's CUDA HierarchicalKV on one H100 NVL, BASELINE.md section 1
+        "paper_h100_context": _paper_context(breakdown, dim),
         "wall_ms_per_step_incl_restore": round(wall * 1e3 / a.steps, 3),
         "host_issue_us_per_op": round(host_s[0] * 1e6 / (a.steps * len(a.lambdas) * 2), 1),
         "fill_s": round(fill_s, 1),
@@ -540,6 +543,18 @@ def run_single(a):
 # ---------------------------------------------------------------------------
 # multi-GPU arm (hash-sharded, one process per GPU, NCCL all-to-all routing)
 # ---------------------------------------------------------------------------
+def _paper_context(breakdown, dim):
+    """Ratios to the per-op H100 NVL figures BASELINE.md quotes, where one exists."""
+    if dim != 64 or "0.50" not in breakdown:
+        return None
+    b = breakdown["0.50"]
+    return {"find_dim64_lambda0.5": {"b200": round(b["find_bkvs"], 3), "h100_nvl": 3.61,
+                                     "ratio": round(b["find_bkvs"] / 3.61, 2)},
+            "insert_or_assign_lambda0.5": {"b200": round(b["insert_or_assign_bkvs"], 3),
+                                           "h100_nvl_dim8_to_64": [1.72, 2.13],
+                                           "ratio_to_best": round(b["insert_or_assign_bkvs"] / 2.13, 2)}}
+
+
 def run_sharded(a, rank, world):
     import torch
     import torch.distributed as dist
