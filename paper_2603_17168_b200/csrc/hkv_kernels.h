@@ -37,6 +37,8 @@ struct Workspace {
   uint32_t* aux2 = nullptr;  // assign: found ranks
   uint64_t* skey = nullptr;  // single mode: bucket-segment records (3 u64 per item)
   uint64_t* lrec = nullptr;  // single mode: records of long segments (3 u64 each)
+  uint32_t* agg = nullptr;   // assign: per-row aggregation hash (row key | last op + 1 | count)
+  int64_t agg_cap = 0;
   uint64_t* skeys = nullptr; // single mode: keys in sorted (bucket, batch index) order
   uint32_t* vrow = nullptr;  // single mode: destination row of final value writers
   uint32_t* rrow = nullptr;  // single mode: row of a value read

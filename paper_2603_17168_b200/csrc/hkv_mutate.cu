@@ -1034,8 +1034,10 @@ __global__ void __launch_bounds__(256) k_assign_find(TableDev t, const uint64_t*
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
   const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / kG;
   ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
+  int bad = 0;
   for (int64_t i = gid; i < n; i += ngroups) {
     const uint64_t key = keys[i];
+    bad |= key >= kLockedKey;  // table.py:168-169: the apply pass then performs no mutation
     const uint64_t h = fmix64(key);
     const uint32_t d = digest_of(h);
     uint64_t b = h & t.mask;
@@ -1051,6 +1053,7 @@ __global__ void __launch_bounds__(256) k_assign_find(TableDev t, const uint64_t*
       outcomes[i] = slot >= 0 ? kUpdated : kNotFound;
     }
   }
+  if (bad && r == 0) atomicOr(&sc->err, 1);
   if (r != 0) {
 #pragma unroll
     for (int k = 0; k < 6; k++) ctr[k] = 0;
@@ -1122,6 +1125,80 @@ struct IsUpdated {
 __global__ void k_assign_count(Scalars* sc, const uint32_t* ranks, const uint8_t* outcomes, int64_t n) {
   if (sc->err || n <= 0) return;
   sc->nfound = (unsigned long long)ranks[n - 1] + (outcomes[n - 1] == kUpdated ? 1ull : 0ull);
+}
+
+// Sort-free duplicate resolution for assign / assign_scores.  Ops on the same
+// row (duplicate keys in a batch) are aggregated in an open-addressing hash
+// keyed by row: the last op (max batch index) and the count.  The apply pass
+// then walks the batch in order (inputs read sequentially) and only the last
+// op of each row writes: its value ("last duplicate wins", table.py:471-476)
+// and the score of `count` consecutive refreshes ending at its tick — the
+// closed form tps_run uses (LFU counts every duplicate, LRU keeps the last
+// tick), or its explicit score.
+__device__ __forceinline__ uint32_t agg_hash(uint32_t row) {
+  uint32_t x = row * 0x9E3779B1u;
+  return x ^ (x >> 15);
+}
+
+__global__ void k_assign_agg(const uint32_t* __restrict__ rows, int64_t n, uint32_t* __restrict__ akey,
+                             uint32_t* __restrict__ alast, uint32_t* __restrict__ acnt, uint32_t amask,
+                             uint32_t* __restrict__ aslot, const Scalars* sc, int count) {
+  if (sc->err) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t row = rows[i];
+  if (row == 0xFFFFFFFFu) return;
+  uint32_t h = agg_hash(row) & amask;
+  while (true) {
+    const uint32_t prev = atomicCAS(akey + h, 0xFFFFFFFFu, row);
+    if (prev == 0xFFFFFFFFu || prev == row) break;
+    h = (h + 1) & amask;
+  }
+  aslot[i] = h;
+  atomicMax(alast + h, (uint32_t)i + 1u);
+  if (count) atomicAdd(acnt + h, 1u);  // only the counting policies read it
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(256) k_assign_apply_agg(TableDev t, const float* __restrict__ values,
+                                                          const uint64_t* __restrict__ scores, int refresh,
+                                                          uint64_t epoch, const uint32_t* __restrict__ rows,
+                                                          const uint32_t* __restrict__ ranks,
+                                                          const uint64_t* __restrict__ ticks,
+                                                          const uint32_t* __restrict__ alast,
+                                                          const uint32_t* __restrict__ acnt,
+                                                          const uint32_t* __restrict__ aslot, int64_t n,
+                                                          const Scalars* sc) {
+  if (sc->err) return;
+  const Tile8 tile;
+  const int r = tile.thread_rank();
+  const int64_t tid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
+  const int64_t ntiles = (int64_t)gridDim.x * blockDim.x / kG;
+  const uint64_t clock0 = *t.clock;
+  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t i = tid; i < n; i += ntiles) {
+    const uint32_t row = rows[i];
+    if (row == 0xFFFFFFFFu) continue;
+    if (values) ctr[row < t.fast_rows ? kVFast : kVOver]++;
+    const uint32_t h = aslot[i];
+    if (alast[h] != (uint32_t)i + 1u) continue;  // a later duplicate writes this row
+    if (values) copy_row<kG, VEC>(value_row(t, row), values + (uint64_t)i * t.dim, t.dim, r);
+    if (r == 0) {
+      if (scores) {
+        t.scores[row] = scores[i];
+        summ_invalidate(t, row / kSlots, (int)(row % kSlots));
+      } else if (refresh) {
+        const uint64_t tick = ticks ? ticks[i] : clock0 + (uint64_t)ranks[i] + 1;
+        t.scores[row] = run_hit_score(t.policy, t.scores[row], epoch, tick, false, 0, acnt[h]);
+        summ_invalidate(t, row / kSlots, (int)(row % kSlots));
+      }
+    }
+  }
+  if (r != 0) {
+#pragma unroll
+    for (int k = 0; k < 6; k++) ctr[k] = 0;
+  }
+  flush_counters<256>(t.counters, ctr, 6);
 }
 
 // ---------------------------------------------------------------------------
@@ -1196,7 +1273,7 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual
 
 void ws_free(Workspace& ws) {
   ws_free_dual(ws);
-  void* ptrs[] = {ws.bkt, ws.idx, ws.sbkt, ws.sidx, ws.seg, ws.aux, ws.aux2, ws.skey, ws.lrec, ws.skeys, ws.vrow, ws.rrow,
+  void* ptrs[] = {ws.bkt, ws.idx, ws.sbkt, ws.sidx, ws.seg, ws.aux, ws.aux2, ws.skey, ws.lrec, ws.agg, ws.skeys, ws.vrow, ws.rrow,
                   ws.lwtab,
                   ws.rsrc,
                   ws.b2, ws.pend,
@@ -1450,8 +1527,6 @@ cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* val
   if ((e = cudaMemsetAsync(ws.sc, 0, sizeof(Scalars), s))) return e;
   const bool need_ticks = refresh && !scores && !ticks;
   if (n > 0) {
-    k_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(t, keys, n, ws.bkt, ws.idx, nullptr, ws.sc);
-    g_launches++;
     const int64_t blocks = tile_blocks(n, num_sms);
     k_assign_find<<<(unsigned)blocks, 256, 0, s>>>(t, keys, n, ws.aux, outcomes, ws.sc);
     g_launches++;
@@ -1465,18 +1540,56 @@ cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* val
       k_assign_count<<<1, 1, 0, s>>>(ws.sc, ws.aux2, outcomes, n);
       g_launches++;
     }
-    if ((e = sort_segments(ws, n, log2_buckets, s))) return e;
+    // Duplicate resolution.  Batches dense in duplicates (>= 16 ops per bucket,
+    // configs[0]) aggregate per row in a hash (random L2 atomics, but no
+    // sort); sparse batches sort by bucket and walk segments in order.
+    const bool agg = (n >> log2_buckets) >= 16;
     const int vec = vec_of(t.dim, values, t.vfast, t.vover, nullptr);
-    ktimer_begin("assign_apply", s);
-    if (vec == 4)
-      k_assign_apply<4><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks, ws.sbkt,
-                                                         ws.sidx, n, ws.sc);
-    else if (vec == 2)
-      k_assign_apply<2><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks, ws.sbkt,
-                                                         ws.sidx, n, ws.sc);
-    else
-      k_assign_apply<1><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks, ws.sbkt,
-                                                         ws.sidx, n, ws.sc);
+    if (agg) {
+      int64_t acap = 1024;
+      while (acap < 2 * n) acap <<= 1;
+      if (acap > ws.agg_cap) {
+        if (ws.agg) cudaFree(ws.agg);
+        ws.agg = nullptr;
+        ws.agg_cap = 0;
+        if ((e = cudaMalloc((void**)&ws.agg, (size_t)acap * 3 * sizeof(uint32_t)))) return e;
+        ws.agg_cap = acap;
+      }
+      uint32_t* akey = ws.agg;
+      uint32_t* alast = ws.agg + acap;
+      uint32_t* acnt = ws.agg + 2 * acap;
+      const int count = refresh && !scores && (t.policy == kLfu || t.policy == kEpochLfu);
+      if ((e = cudaMemsetAsync(akey, 0xFF, (size_t)acap * 4, s)) ||
+          (e = cudaMemsetAsync(alast, 0, (size_t)acap * (count ? 8 : 4), s)))
+        return e;
+      k_assign_agg<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ws.aux, n, akey, alast, acnt, (uint32_t)(acap - 1),
+                                                              ws.vrow, ws.sc, count);
+      g_launches++;
+      ktimer_begin("assign_apply", s);
+      if (vec == 4)
+        k_assign_apply_agg<4><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2,
+                                                               ticks, alast, acnt, ws.vrow, n, ws.sc);
+      else if (vec == 2)
+        k_assign_apply_agg<2><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2,
+                                                               ticks, alast, acnt, ws.vrow, n, ws.sc);
+      else
+        k_assign_apply_agg<1><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2,
+                                                               ticks, alast, acnt, ws.vrow, n, ws.sc);
+    } else {
+      k_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(t, keys, n, ws.bkt, ws.idx, nullptr, ws.sc);
+      g_launches++;
+      if ((e = sort_segments(ws, n, log2_buckets, s))) return e;
+      ktimer_begin("assign_apply", s);
+      if (vec == 4)
+        k_assign_apply<4><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks,
+                                                           ws.sbkt, ws.sidx, n, ws.sc);
+      else if (vec == 2)
+        k_assign_apply<2><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks,
+                                                           ws.sbkt, ws.sidx, n, ws.sc);
+      else
+        k_assign_apply<1><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks,
+                                                           ws.sbkt, ws.sidx, n, ws.sc);
+    }
     ktimer_end("assign_apply", s);
     g_launches++;
   }
