@@ -100,6 +100,10 @@ def c1(reps):
     ms_f, (f, _) = timed(lambda r: t.find(q), reps)
     emit({"config": "C1", "op": "find", "capacity": cap, "dim": dim, "lambda": round(t.load_factor(), 4),
           "ms": ms_f, "bkvs": B / ms_f / 1e6, "hit_rate": float(f.float().mean())})
+    # assign of the same mixed batch (half resident; 128 ops per bucket: the dense-duplicate path)
+    ms_a, o = timed(lambda r: t.assign(q, iv), reps)
+    emit({"config": "C1", "op": "assign", "capacity": cap, "dim": dim, "lambda": round(t.load_factor(), 4),
+          "ms": ms_a, "bkvs": B / ms_a / 1e6, "outcomes": outcome_mix(o)})
 
 
 def c2_extras(reps, lg=27):
