@@ -498,3 +498,21 @@ def test_peer_find_preconditions(hkv):
         t._set_peers_local([t, tiered])
     with pytest.raises(ValueError):  # no peers set yet
         t._find_peer(torch.ones(4, dtype=torch.int64, device="cuda"))
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("policy", ["kLru", "kLfu", "kCustomized"])
+def test_oracle_differential_sparse_duplicates(hkv, mode, policy):
+    """The sparse regime (a few ops per bucket: sorted-walk assign, no
+    long-segment engine) with in-batch duplicates, against the oracle."""
+    cap, dim = 128 * 1024, 4
+    t = make_table(hkv, cap, dim, mode, policy)
+    o = OracleTable(cap, dim, mode, policy)
+    for j, (op, a) in enumerate(make_script(700 + 10 * MODES.index(mode) + POLICIES.index(policy), cap, dim, policy,
+                                            n_batches=30, batch=4000, universe_scale=0.3, dup_frac=0.3)):
+        r_t = run_impl(t, op, a)
+        r_o = run_impl(o, op, a)
+        assert outputs_equal(r_o, r_t), f"op {j} {op}"
+    assert_same_state(t, o)
+    assert t.counters.as_dict() == o.counters
+    assert t.check_consistency()
