@@ -73,50 +73,6 @@ __global__ void __launch_bounds__(256) k_find_gather(TableDev t, const uint32_t*
   block_ctrs_flush(bc, t.counters, nullptr, ctr, 0);
 }
 
-// Thread-per-key probe (the default): one thread reads its key's whole
-// 128-B digest line (8 x 16 B, all in flight together), matches the 128
-// digests with __vcmpeq4, then checks candidate keys in slot order.  No
-// cross-lane collectives: ~2.5x fewer warp instructions per key than the
-// 8-lane tile, and 32 keys per warp in flight instead of 16.
-__device__ __forceinline__ int probe_line_thread(const TableDev& t, uint64_t b, uint64_t key, uint32_t d,
-                                                 unsigned& ncmp) {
-  const uint64_t rowbase = b * kSlots;
-  uint32_t c[4];
-  if (t.digest_filter) {
-    const uint4* dp = reinterpret_cast<const uint4*>(t.digests + rowbase);
-    uint4 w[8];
-#pragma unroll
-    for (int k = 0; k < 8; k++) w[k] = ld_stream(dp + k);
-    const uint32_t dd = d * 0x01010101u;
-    uint32_t any = 0;
-#pragma unroll
-    for (int k = 0; k < 8; k++) any |= any16(w[k], dd);
-    if ((any & 0x80808080u) == 0) return -1;  // no digest match: a miss without touching keys
-#pragma unroll
-    for (int q = 0; q < 4; q++) c[q] = match16(w[2 * q], d) | (match16(w[2 * q + 1], d) << 16);
-  } else {
-#pragma unroll
-    for (int q = 0; q < 4; q++) c[q] = ~0u;
-  }
-  int hit = -1;
-#pragma unroll
-  for (int q = 0; q < 4; q++) {
-    uint32_t m = hit < 0 ? c[q] : 0u;
-    while (m) {
-      const int j = __ffs(m) - 1;
-      m &= m - 1;
-      const uint64_t k = __ldg(t.keys + rowbase + 32 * q + j);
-      if (k == kEmptyKey) continue;  // candidates exclude EMPTY slots (table.py:243-247)
-      ncmp++;
-      if (k == key) {
-        hit = 32 * q + j;
-        m = 0;
-      }
-    }
-  }
-  return hit;
-}
-
 template <int MODE>
 __global__ void __launch_bounds__(256) k_find_tpk(TableDev t, const uint64_t* __restrict__ keys, int64_t n,
                                                   uint8_t* __restrict__ found, uint8_t* __restrict__ tier,

@@ -1028,37 +1028,33 @@ __global__ void k_zero_count(const Scalars* sc, long long* n_ev) {
 __global__ void __launch_bounds__(256) k_assign_find(TableDev t, const uint64_t* __restrict__ keys, int64_t n,
                                                      uint32_t* __restrict__ rows, uint8_t* __restrict__ outcomes,
                                                      Scalars* sc) {
+  // thread per key (the find path's probe: one digest line per thread, the
+  // candidate keys in slot order; counters as table.py:243-268)
   if (sc->err) return;
-  const Tile8 tile;
-  const int r = tile.thread_rank();
-  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
-  const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / kG;
+  __shared__ BlockCtrs bc;
+  block_ctrs_init(bc);
   ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
   int bad = 0;
-  for (int64_t i = gid; i < n; i += ngroups) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t key = keys[i];
     bad |= key >= kLockedKey;  // table.py:168-169: the apply pass then performs no mutation
     const uint64_t h = fmix64(key);
     const uint32_t d = digest_of(h);
     uint64_t b = h & t.mask;
-    int slot = probe_bucket<false, false>(t, tile, b, key, d, 0xFFFFu, ctr[kCompares]);
+    unsigned ncmp = 0;
+    int slot = probe_line_thread(t, b, key, d, ncmp);
     ctr[kLoads]++;
     if (slot < 0 && t.dual) {
       b = second_hash(h) & t.mask;
-      slot = probe_bucket<false, false>(t, tile, b, key, d, 0xFFFFu, ctr[kCompares]);
+      slot = probe_line_thread(t, b, key, d, ncmp);
       ctr[kLoads]++;
     }
-    if (r == 0) {
-      rows[i] = slot >= 0 ? (uint32_t)(b * kSlots + slot) : 0xFFFFFFFFu;
-      outcomes[i] = slot >= 0 ? kUpdated : kNotFound;
-    }
+    ctr[kCompares] += ncmp;
+    rows[i] = slot >= 0 ? (uint32_t)(b * kSlots + slot) : 0xFFFFFFFFu;
+    outcomes[i] = slot >= 0 ? kUpdated : kNotFound;
   }
-  if (bad && r == 0) atomicOr(&sc->err, 1);
-  if (r != 0) {
-#pragma unroll
-    for (int k = 0; k < 6; k++) ctr[k] = 0;
-  }
-  flush_counters<256>(t.counters, ctr, 6);
+  if (bad) atomicOr(&sc->err, 1);
+  block_ctrs_flush(bc, t.counters, nullptr, ctr, 0);
 }
 
 template <int VEC>
@@ -1528,7 +1524,9 @@ cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* val
   const bool need_ticks = refresh && !scores && !ticks;
   if (n > 0) {
     const int64_t blocks = tile_blocks(n, num_sms);
-    k_assign_find<<<(unsigned)blocks, 256, 0, s>>>(t, keys, n, ws.aux, outcomes, ws.sc);
+    int64_t fblocks = (n + 255) / 256;
+    if (fblocks > (int64_t)num_sms * 8) fblocks = (int64_t)num_sms * 8;
+    k_assign_find<<<(unsigned)(fblocks < 1 ? 1 : fblocks), 256, 0, s>>>(t, keys, n, ws.aux, outcomes, ws.sc);
     g_launches++;
     if (need_ticks) {
       size_t bytes = ws.cub_bytes;
