@@ -64,7 +64,9 @@ __device__ __forceinline__ void write_row(float* dst, const float* vin, const In
   }
 }
 
-// probe_bucket with the lane's digest slice already loaded
+// One bucket probed by an 8-lane tile (lane r: slots 16r..16r+15) with the
+// lane's digest slice and occupancy already loaded; compares counted as
+// table.py:243-268 (candidates in slot order, stopping at the match)
 __device__ __forceinline__ int probe_loaded(const TableDev& t, const Tile8& tile, uint64_t b, uint64_t key,
                                             uint32_t d, uint4 dw, uint32_t occ, ctr_t& n_compares) {
   const int r = tile.thread_rank();

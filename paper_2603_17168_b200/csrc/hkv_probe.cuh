@@ -1,10 +1,11 @@
-// hkv_probe.cuh — the digest probe shared by every kernel.
+// hkv_probe.cuh — probe helpers shared by the kernels.
 //
-// A tile of G = 8 lanes owns one bucket probe: lane r holds slots
-// [16r, 16r+16) — one 16-B slice of the 128-B digest line and one 16-bit
-// slice of the occupancy bitmap — so the digest line is one coalesced 128-B
-// transaction (Alg. 1) and a lane only ever reads or writes
-// its own slots' metadata (no cross-lane memory hazards inside a segment).
+// probe_line_thread: one thread reads a key's whole 128-B digest line and
+// checks candidate keys in slot order (find, contains, find_ptr, assign).
+// 8-lane tiles (kG): lane r holds slots [16r, 16r+16) — one 16-B slice of the
+// digest line and one 16-bit slice of the occupancy bitmap — for the kernels
+// that work a bucket with a tile (dual-mode ops, value copies, the occupancy
+// rebuild); a lane only reads or writes its own slots' metadata.
 #pragma once
 #include "hkv_common.cuh"
 
@@ -12,57 +13,6 @@ namespace hkv {
 
 constexpr int kG = 8;                 // lanes per bucket tile
 constexpr int kSPL = kSlots / kG;     // slots per lane (16)
-
-// Probe one bucket for `key` (digest d).  `occ` is this lane's 16-bit
-// occupancy slice (pass 0xFFFF to treat every slot as occupied — read-only
-// kernels skip the bitmap and test key != EMPTY instead).  Counts key
-// compares exactly as table.py:243-268: one per candidate (digest equal and
-// key != EMPTY) in slot order, stopping at the match.
-template <bool kUseBits, bool kReadOnly>
-__device__ __forceinline__ int probe_bucket(const TableDev& t, const Tile8& tile,
-                                            uint64_t b, uint64_t key, uint32_t d, uint32_t occ,
-                                            ctr_t& n_compares) {
-  const int r = tile.thread_rank();
-  uint32_t cand;
-  if (t.digest_filter) {
-    const uint4* dp = reinterpret_cast<const uint4*>(t.digests + b * kSlots) + r;
-    uint4 w;
-    if constexpr (kReadOnly) w = __ldg(dp); else w = *dp;
-    cand = match16(w, d);
-  } else {
-    cand = 0xFFFFu;
-  }
-  if constexpr (kUseBits) cand &= occ;
-  const uint64_t* kp = t.keys + b * kSlots + r * kSPL;
-  int hit = -1;
-  int ncmp = 0;
-  int ncmp_all = 0;
-  while (cand) {
-    const int j = __ffs(cand) - 1;
-    cand &= cand - 1;
-    uint64_t k;
-    if constexpr (kReadOnly) k = __ldg(kp + j); else k = kp[j];
-    if (!kUseBits && k == kEmptyKey) continue;
-    ncmp_all++;
-    if (k == key) {
-      hit = r * kSPL + j;
-      ncmp = ncmp_all;  // keys are unique within a bucket: at most one lane hits
-      break;
-    }
-  }
-  const uint32_t hm = tile.ballot(hit >= 0);
-  int slot = -1;
-  int contrib;
-  if (hm) {
-    const int hl = __ffs(hm) - 1;
-    slot = tile.shfl(hit, hl);
-    contrib = r < hl ? ncmp_all : (r == hl ? ncmp : 0);
-  } else {
-    contrib = ncmp_all;
-  }
-  n_compares += tile.sum((unsigned)contrib);
-  return slot;
-}
 
 // Lowest (score, slot) over the bucket — np.argmin semantics (first index on
 // ties), table.py:1080.  Each lane scans its 16 scores (128 contiguous bytes).
