@@ -20,6 +20,8 @@ struct Scalars {
   long long size_before;         // table size when the batch started
   unsigned long long nfound;     // assign: found ops (clock advance for refresh)
   long long n_sel;               // DeviceSelect count
+  unsigned long long fel_cnt;    // k_finalize: inserts before the first eviction (summed over blocks)
+  unsigned fel_done;             // k_finalize: blocks finished
 };
 
 // Per-stream scratch, grown on demand.

@@ -973,23 +973,34 @@ __global__ void __launch_bounds__(256) k_values_read(TableDev t, float* __restri
 }
 
 // Clock advance + first_eviction_lambda (table.py:986-991) + error latch.
-__global__ void k_finalize(TableDev t, Scalars* sc, const uint8_t* __restrict__ outcomes, int64_t n,
-                           unsigned long long clock_advance, int add_found) {
+// The lambda needs the inserts that precede the first eviction: counted by
+// every block over a strided share, the last block to finish publishes it.
+constexpr int kFinBlocks = 32;
+__global__ void __launch_bounds__(1024) k_finalize(TableDev t, Scalars* sc, const uint8_t* __restrict__ outcomes,
+                                                   int64_t n, unsigned long long clock_advance, int add_found) {
   if (sc->err) {
-    if (threadIdx.x == 0) atomicOr(t.err, sc->err);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(t.err, sc->err);
     return;
   }
-  if (threadIdx.x == 0) *t.clock += clock_advance + (add_found ? sc->nfound : 0ull);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *t.clock += clock_advance + (add_found ? sc->nfound : 0ull);
   const unsigned fe = sc->first_ev;
   if (*t.fel_set || fe == 0xFFFFFFFFu || outcomes == nullptr) return;
   unsigned cnt = 0;
-  for (int64_t j = threadIdx.x; j < (int64_t)fe; j += blockDim.x) cnt += outcomes[j] == kInserted;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < (int64_t)fe;
+       j += (int64_t)gridDim.x * blockDim.x)
+    cnt += outcomes[j] == kInserted;
   typedef cub::BlockReduce<unsigned, 1024> BR;
   __shared__ typename BR::TempStorage tmp;
   const unsigned tot = BR(tmp).Sum(cnt);
   if (threadIdx.x == 0) {
-    *t.fel = (double)(sc->size_before + (long long)tot) / (double)t.capacity;
-    *t.fel_set = 1;
+    if (tot) atomicAdd(&sc->fel_cnt, (unsigned long long)tot);
+    __threadfence();
+    if (atomicAdd(&sc->fel_done, 1u) == gridDim.x - 1) {
+      __threadfence();
+      const unsigned long long all = atomicAdd(&sc->fel_cnt, 0ull);
+      *t.fel = (double)(sc->size_before + (long long)all) / (double)t.capacity;
+      *t.fel_set = 1;
+    }
   }
 }
 
@@ -1448,7 +1459,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
     }
   }
   ktimer_begin("finalize", s, 2);
-  k_finalize<<<1, 1024, 0, s>>>(t, ws.sc, a.op == kOpErase ? nullptr : a.outcomes, n, clock_advance, 0);
+  k_finalize<<<kFinBlocks, 1024, 0, s>>>(t, ws.sc, a.op == kOpErase ? nullptr : a.outcomes, n, clock_advance, 0);
   ktimer_end("finalize", s, 2);
   g_launches++;
   long long* nev = reinterpret_cast<long long*>(n_evicted);
@@ -1591,7 +1602,7 @@ cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* val
     ktimer_end("assign_apply", s);
     g_launches++;
   }
-  k_finalize<<<1, 1024, 0, s>>>(t, ws.sc, nullptr, n, (refresh && !scores && ticks) ? clock_advance : 0,
+  k_finalize<<<kFinBlocks, 1024, 0, s>>>(t, ws.sc, nullptr, n, (refresh && !scores && ticks) ? clock_advance : 0,
                                 need_ticks ? 1 : 0);
   g_launches++;
   return cudaGetLastError();
