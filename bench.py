@@ -20,12 +20,15 @@ the timed region) so lambda stays fixed — SURVEY.md 8(d) C2.
   roofline   dominant kernel (largest share of step time), algorithmic bytes
              (SURVEY.md 8(d) byte model x outcome counts) / its live CUDA-event
              duration, against MEASURED_PEAKS.json hbm_gbs.
-  cpu_baseline  the C oracle (a restatement of the reference engine) on this
-             host's cores, bounded sample (see `sample`).
+  cpu_baseline  the reference package itself (cachekv.CacheTable, workers=1,
+             from baseline/_ref) on this host at the same configuration,
+             bounded to lambda 0.50 and one step; the C port of its engine
+             (oracle/, all host threads) beside it under "port".
 
---impl reference   times the reference's CPU algorithm (the oracle port;
-             the reference package is pure Python and cannot travel) on the
-             host cores, same metric.
+--impl reference   times the reference package at the C2 configuration on
+             the host (bench_ref.py: closed-form fill state injected, then
+             its own find / insert_or_assign timed); the oracle port stands in
+             only if baseline/_ref is absent.
 --gpus N (>1, under torchrun)   hash-sharded table (contiguous bucket ranges
              per rank, NCCL all-to-all routing): find + insert_or_assign of
              2^20 keys per rank at lambda 0.5 on a 2^27-slot-per-rank table.
@@ -236,20 +239,44 @@ def cpu_reference_run(dim, lambdas, steps, warmup, find_batch=2**20, ins_batch=2
     return tot_keys / tot_s / 1e9, threads, sample, detail
 
 
+def reference_baseline(a, lambdas, steps, warmup):
+    """The reference package itself (baseline/_ref, cachekv.CacheTable,
+    workers=1) at the bench configuration; None when it is not installed."""
+    import bench_ref
+
+    ck = bench_ref.import_reference()
+    if ck is None:
+        return None
+    log = (lambda m: print(m, file=sys.stderr, flush=True)) if os.environ.get("BENCH_DEBUG") else None
+    val, detail, setup = bench_ref.time_reference(ck, a.capacity, a.dim, a.batch, lambdas, steps, warmup, log=log)
+    sample = (f"reference package cachekv.CacheTable(workers=1) from baseline/_ref (numpy, 1 thread), "
+              f"{a.capacity}-slot dim-{a.dim} kLru table at lambda {lambdas} (fill state computed in closed form "
+              f"and injected, bench_ref.py; untimed set-up {setup:.0f} s); per step and lambda {a.batch} finds of "
+              f"resident keys + {a.batch} insert_or_assign of fresh keys; {steps} timed steps")
+    return {"value": val, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample,
+            "same_config": True, "detail": detail}
+
+
 def run_reference_arm(a, rank, world):
     if rank != 0:
         return
-    dim = a.dim
-    val, cores, sample, detail = cpu_reference_run(dim, a.lambdas, a.steps, a.warmup)
+    base = reference_baseline(a, a.lambdas, a.steps, a.warmup)
+    if base is None:  # reference not installed here: the oracle port stands in
+        val, cores, sample, detail = cpu_reference_run(a.dim, a.lambdas, a.steps, a.warmup)
+        base = {"value": val, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample, "same_config": False,
+                "detail": detail}
+    val = base["value"]
     line = {
         "metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64/f32",
         "data": "synthetic (uniform_distinct_keys, seed 0)",
-        "config": {"workload": "C2-shaped: find + insert_or_assign, dim 64, lambda 0.50/0.75/1.00 (bounded CPU "
-                               "sample)", "batch": 2**20},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "config": {"workload": "C2: 128M-slot table (configs[1]), dim 64 fp32, kLru, single mode; per step and "
+                               "lambda: find 1M resident keys + insert_or_assign 1M fresh keys"
+                               + ("" if base["same_config"] else " (oracle port, bounded sample: see cpu_baseline)"),
+                   "capacity": a.capacity, "dim": a.dim, "batch": a.batch, "lambdas": a.lambdas},
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "detail": detail,
+        "detail": base["detail"],
     }
     print(json.dumps(line), flush=True)
 
@@ -507,8 +534,16 @@ def run_single(a):
 
     cpu_base = None
     if not a.no_cpu_baseline:
-        v, cores, sample, detail = cpu_reference_run(dim, a.lambdas, steps=2, warmup=0)
-        cpu_base = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample, "detail": detail}
+        # the reference package itself at this configuration, bounded to one
+        # lambda and one step (bench.py --impl reference runs all lambdas);
+        # the C port of its engine on all host threads beside it
+        v, cores, sample, detail = cpu_reference_run(dim, a.lambdas, steps=1, warmup=0)
+        port = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample, "detail": detail}
+        cpu_base = reference_baseline(a, [a.lambdas[0]], steps=1, warmup=0)
+        if cpu_base is None:
+            cpu_base = port
+        else:
+            cpu_base["port"] = port
 
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": 1, "steps": a.steps,

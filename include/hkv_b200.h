@@ -38,6 +38,8 @@ enum hkv_status {
     HKV_EINVAL = 1,  /* usage error -> ValueError in the Python mirror */
     HKV_ECUDA = 2,   /* CUDA runtime error */
     HKV_ENOMEM = 3,  /* device / pinned host allocation failed */
+    HKV_EBUSY = 4,   /* hkv_gate_acquire(mode 0): the role would have to wait */
+    HKV_GATE_NESTED = 5, /* hkv_gate_acquire(mode 2): success, nested in a covering hold */
 };
 
 enum hkv_mode { HKV_MODE_SINGLE = 0, HKV_MODE_DUAL = 1 };            /* table.py:63-65 */
@@ -49,7 +51,10 @@ enum hkv_outcome {                                                    /* table.p
     HKV_FOUND = 4, HKV_NOTFOUND = 5, HKV_ERASED = 6
 };
 enum hkv_upsert_op { HKV_OP_INSERT_OR_ASSIGN = 0, HKV_OP_FIND_OR_INSERT = 1 };
-enum hkv_device_error_bits { HKV_DERR_SENTINEL_KEY = 1 };
+enum hkv_device_error_bits {
+    HKV_DERR_SENTINEL_KEY = 1, /* a key >= LOCKED: the batch performed no mutation */
+    HKV_DERR_ROLE = 2          /* a mutation kernel ran while the device mirror named a reader group */
+};
 
 /* TableConfig (table.py:94-131).  Validation errors mirror table.py:108-127. */
 typedef struct {
@@ -75,6 +80,43 @@ const char *hkv_version(void);
 /* CacheTable.__init__ (table.py:139-160) + TieredValueStore (store.py:41-79). */
 int hkv_create(const hkv_config *cfg, hkv_table **out);
 int hkv_destroy(hkv_table *t);
+
+/* ---- triple-group role gate (gate.py:60-157) ----
+ * Readers run with readers, updaters with updaters, an inserter alone;
+ * phase-fair FIFO admission.  Every table owns one gate and EVERY entry point
+ * below takes its role (find/contains/find_ptr/export/size/... reader,
+ * assign updater, upsert/erase/import/restore inserter) for the duration of
+ * its launches.  Device layer: each release records an event on its stream;
+ * the first entrant of a new group makes its stream wait on them and
+ * publishes (group, role) to a device mirror word with a one-thread kernel,
+ * so incompatible groups never overlap on the device even on different
+ * streams, and mutation kernels check the mirror (HKV_DERR_ROLE).
+ * A thread may hold a role across several calls (hkv_gate_acquire ...
+ * hkv_gate_release): entry points called by that thread with the same role,
+ * or under a held inserter role, nest in the hold (their streams are still
+ * fenced); an entry point whose role is incompatible with the thread's hold
+ * returns HKV_EINVAL instead of deadlocking.
+ * Standalone gates (hkv_gate_create) have the host layer only. */
+typedef struct hkv_gate hkv_gate;
+enum hkv_role { HKV_ROLE_READER = 0, HKV_ROLE_UPDATER = 1, HKV_ROLE_INSERTER = 2 };
+enum hkv_gate_event { HKV_GATE_ACQUIRE = 0, HKV_GATE_RELEASE = 1 };
+/* event hook (gate.py:61,70-73): called under the gate lock with the event
+ * sequence number, the event, the role and the active count after it */
+typedef void (*hkv_gate_hook)(void *user, int64_t seq, int32_t event, int32_t role, int32_t active_count);
+int hkv_gate_create(hkv_gate **out);
+int hkv_gate_destroy(hkv_gate *g);
+int hkv_table_gate(hkv_table *t, hkv_gate **out); /* owned by the table */
+int hkv_gate_set_hook(hkv_gate *g, hkv_gate_hook fn, void *user);
+/* mode 1: acquire (gate.py:90-104), blocks; mode 0: try_acquire (HKV_EBUSY
+ * instead of waiting, gate.py:106-116); mode 2: the scoped acquisition every
+ * entry point makes (returns HKV_GATE_NESTED when it nested in the thread's
+ * hold; pass nested = 1 to the matching release).
+ * has_stream = 0: no device fencing for this acquisition. */
+int hkv_gate_acquire(hkv_gate *g, int32_t role, int32_t mode, int32_t has_stream, hkv_stream stream);
+/* HKV_EINVAL when no matching acquisition is active (gate.py:128-130). */
+int hkv_gate_release(hkv_gate *g, int32_t role, int32_t nested, int32_t has_stream, hkv_stream stream);
+/* active role (-1 = idle), active count, groups admitted so far */
+int hkv_gate_state(hkv_gate *g, int32_t *role, int32_t *count, int64_t *groups);
 
 /* find (table.py:304-323): found[i] in {0,1}; out rows of misses untouched
  * (zero_misses = 0, the reference contract for a caller-provided `out`) or
@@ -186,6 +228,13 @@ int hkv_import_state(hkv_table *t, const uint64_t *keys, const uint8_t *digests,
                      int32_t fel_set, double fel);
 int hkv_export_state(hkv_table *t, uint64_t *keys, uint8_t *digests, uint64_t *scores,
                      float *values, int64_t *occupancy);
+
+/* Keys and scores of global rows [row0, row0 + nrows) (row = bucket * 128 +
+ * slot) into host or device buffers (either may be NULL).  SYNCHRONISING.
+ * Serves export_batch_if with a Python predicate (table.py:402-409): the
+ * predicate sees one chunk of rows at a time. */
+int hkv_read_rows(hkv_table *t, int64_t row0, int64_t nrows, uint64_t *keys, uint64_t *scores,
+                  hkv_stream stream);
 
 /* Metadata snapshot held in HBM (keys, digests, scores, occupancy bits, size,
  * clock): the bench restores it between timed repeats so the load factor

@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HKV_LIB") or os.path.join(_HERE, "libhkv_b200.so")  # HKV_LIB: experiment builds
 
-HKV_OK, HKV_EINVAL, HKV_ECUDA, HKV_ENOMEM = 0, 1, 2, 3
+HKV_OK, HKV_EINVAL, HKV_ECUDA, HKV_ENOMEM, HKV_EBUSY = 0, 1, 2, 3, 4
 
 
 class HkvConfig(C.Structure):
@@ -66,10 +66,18 @@ SIGNATURES = {
     "hkv_import_state": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _u64, _i32, C.c_double]),
     "hkv_export_state": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "hkv_snapshot": (C.c_int, [_vp, _vp]),
+    "hkv_read_rows": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "hkv_restore": (C.c_int, [_vp, _vp]),
     "hkv_check_consistency": (C.c_int, [_vp, C.POINTER(_i32), _vp]),
     "hkv_route": (C.c_int, [_vp, _i64, _i64, _i32, _vp, _vp, _vp]),
     "hkv_set_kernel_timing": (C.c_int, [_i32]),
+    "hkv_gate_create": (C.c_int, [C.POINTER(_vp)]),
+    "hkv_gate_destroy": (C.c_int, [_vp]),
+    "hkv_table_gate": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "hkv_gate_set_hook": (C.c_int, [_vp, _vp, _vp]),
+    "hkv_gate_acquire": (C.c_int, [_vp, _i32, _i32, _i32, _vp]),
+    "hkv_gate_release": (C.c_int, [_vp, _i32, _i32, _i32, _vp]),
+    "hkv_gate_state": (C.c_int, [_vp, _vp, _vp, _vp]),
     "hkv_kernel_times": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(_i64)]),
 }
 

@@ -11,10 +11,16 @@
 #include <vector>
 
 #include "../../include/hkv_b200.h"
+#include "hkv_gate.h"
 #include "hkv_kernels.h"
+
+namespace {
+thread_local std::string g_err;
+}
 
 namespace hkv {
 unsigned long long g_launches = 0;
+void set_error(const char* msg) { g_err = msg; }
 
 namespace {
 struct KTimer {
@@ -77,8 +83,6 @@ using namespace hkv;
 
 namespace {
 
-thread_local std::string g_err;
-
 struct TableScalars {
   unsigned long long size;
   unsigned long long clock;
@@ -93,6 +97,11 @@ struct TableScalars {
 int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
+}
+
+int gate_fail(int rc) {
+  if (rc != HKV_EINVAL) g_err = "role gate: CUDA fencing failed";
+  return rc;
 }
 
 int cuda_fail(cudaError_t e, const char* where) {
@@ -172,6 +181,8 @@ struct hkv_table {
   float* vover = nullptr;       // device pointer of the overflow arena
   float* vover_host = nullptr;  // pinned host allocation (mapped), if used
   TableScalars* sc = nullptr;
+  unsigned* role_word = nullptr;  // device mirror of the gate's group (never snapshotted)
+  hkv_gate* gate = nullptr;
   unsigned long long* lead = nullptr;
   // metadata snapshot
   uint64_t* snap_keys = nullptr;
@@ -237,7 +248,8 @@ struct DeviceGuard {
 void free_table(hkv_table* t) {
   if (!t) return;
   DeviceGuard g(t->cfg.device);
-  void* dptrs[] = {t->keys, t->digests, t->scores, t->bits, t->smin, t->svalid, t->vfast, t->sc, t->lead,
+  if (t->gate) gate_delete(t->gate);
+  void* dptrs[] = {t->keys, t->digests, t->scores, t->bits, t->smin, t->svalid, t->vfast, t->sc, t->role_word, t->lead,
                    t->snap_keys, t->snap_digests, t->snap_scores, t->snap_bits, t->snap_smin, t->snap_svalid,
                    t->snap_sc};
   for (void* p : dptrs)
@@ -330,7 +342,7 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
   if ((e = cudaMalloc((void**)&t->keys, cap * 8)) || (e = cudaMalloc((void**)&t->digests, cap)) ||
       (e = cudaMalloc((void**)&t->scores, cap * 8)) || (e = cudaMalloc((void**)&t->bits, (size_t)bc * 16)) ||
       (e = cudaMalloc((void**)&t->smin, (size_t)bc * 64)) || (e = cudaMalloc((void**)&t->svalid, (size_t)bc * 4)) ||
-      (e = cudaMalloc((void**)&t->sc, sizeof(TableScalars)))) {
+      (e = cudaMalloc((void**)&t->sc, sizeof(TableScalars))) || (e = cudaMalloc((void**)&t->role_word, 4))) {
     free_table(t);
     return fail(HKV_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e));
   }
@@ -359,7 +371,7 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
   if ((e = cudaMemset(t->keys, 0xFF, cap * 8)) || (e = cudaMemset(t->digests, 0, cap)) ||
       (e = cudaMemset(t->scores, 0, cap * 8)) || (e = cudaMemset(t->bits, 0, (size_t)bc * 16)) ||
       (e = cudaMemset(t->smin, 0, (size_t)bc * 64)) || (e = cudaMemset(t->svalid, 0, (size_t)bc * 4)) ||
-      (e = cudaMemset(t->sc, 0, sizeof(TableScalars))) ||
+      (e = cudaMemset(t->sc, 0, sizeof(TableScalars))) || (e = cudaMemset(t->role_word, 0, 4)) ||
       (t->vfast && (e = cudaMemset(t->vfast, 0, t->fast_rows * dim * 4))) ||
       (t->vover && (e = cudaMemset(t->vover, 0, over_rows * dim * 4))) ||
       (t->lead && (e = cudaMemset(t->lead, 0, (size_t)bc * 8)))) {
@@ -393,7 +405,15 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
   d.err = &t->sc->err;
   d.fel_set = &t->sc->fel_set;
   d.fel = &t->sc->fel;
+  d.role_word = t->role_word;
+  t->gate = gate_new_device(c.device, t->role_word);
   *out = t;
+  return HKV_OK;
+}
+
+int hkv_table_gate(hkv_table* t, hkv_gate** out) {
+  if (!t || !out) return fail(HKV_EINVAL, "null argument");
+  *out = t->gate;
   return HKV_OK;
 }
 
@@ -407,6 +427,10 @@ int hkv_destroy(hkv_table* t) {
   return HKV_OK;
 }
 
+// mutation batches index ops with uint32 and hand (int)n to CUB: cap them
+#define CHECK_MUT_N() \
+  if (n > 0x7FFFFFFFll) return fail(HKV_EINVAL, "batch too large (at most 2^31-1 keys per mutation call)")
+
 #define CHECK_T()                                   \
   if (!t) return fail(HKV_EINVAL, "null table");    \
   if (n < 0) return fail(HKV_EINVAL, "negative batch size"); \
@@ -416,6 +440,8 @@ int hkv_find(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uint8_t*
              hkv_stream stream) {
   CHECK_T();
   if (n && (!keys || !found)) return fail(HKV_EINVAL, "null keys/found");
+  GateScope _gs(t->gate, HKV_ROLE_READER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
   uint32_t* rows = nullptr;
   auto lease = t->workspace((cudaStream_t)stream);
   if (out && n > 0) {
@@ -433,6 +459,8 @@ int hkv_find(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uint8_t*
 int hkv_contains(hkv_table* t, const uint64_t* keys, int64_t n, uint8_t* found, hkv_stream stream) {
   CHECK_T();
   if (n && (!keys || !found)) return fail(HKV_EINVAL, "null keys/found");
+  GateScope _gs(t->gate, HKV_ROLE_READER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
   launch_find(t->dev, keys, n, nullptr, found, nullptr, nullptr, 1, nullptr, (cudaStream_t)stream, t->num_sms);
   cudaError_t e = cudaGetLastError();
   return e ? cuda_fail(e, "hkv_contains") : HKV_OK;
@@ -442,6 +470,8 @@ int hkv_find_ptr(hkv_table* t, const uint64_t* keys, int64_t n, uint8_t* found, 
                  hkv_stream stream) {
   CHECK_T();
   if (n && (!keys || !found || !tier || !offset)) return fail(HKV_EINVAL, "null argument");
+  GateScope _gs(t->gate, HKV_ROLE_READER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
   launch_find(t->dev, keys, n, nullptr, found, tier, offset, 2, nullptr, (cudaStream_t)stream, t->num_sms);
   cudaError_t e = cudaGetLastError();
   return e ? cuda_fail(e, "hkv_find_ptr") : HKV_OK;
@@ -461,7 +491,9 @@ int hkv_upsert(hkv_table* t, int32_t op, const uint64_t* keys, float* values, co
   if (collect && (!evicted_keys || !evicted_values || !evicted_scores || !n_evicted_dev))
     return fail(HKV_EINVAL, "insert_and_evict needs all evicted outputs");
   if (collect && op != HKV_OP_INSERT_OR_ASSIGN) return fail(HKV_EINVAL, "evicted outputs need insert_or_assign");
-  if (n > 0xFFFFFFFEll) return fail(HKV_EINVAL, "batch too large");
+  CHECK_MUT_N();
+  GateScope _gs(t->gate, HKV_ROLE_INSERTER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
   cudaStream_t s = (cudaStream_t)stream;
   OpArgs a{};
   a.keys = keys;
@@ -488,6 +520,8 @@ int hkv_find_host(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uin
   CHECK_T();
   if (n && (!keys || !found)) return fail(HKV_EINVAL, "null keys/found");
   if (n == 0) return HKV_OK;
+  GateScope _gs(t->gate, HKV_ROLE_READER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
   cudaStream_t s = (cudaStream_t)stream;
   HostStage& h = t->stage(s);
   std::lock_guard<std::mutex> hold(h.mu);
@@ -544,7 +578,9 @@ int hkv_upsert_host(hkv_table* t, int32_t op, const uint64_t* keys, float* value
   if (custom && !scores) return fail(HKV_EINVAL, "kCustomized requires explicit scores");
   if (!custom && scores) return fail(HKV_EINVAL, "explicit scores require the kCustomized policy");
   if (n && (!keys || !values || !outcomes)) return fail(HKV_EINVAL, "null keys/values/outcomes");
-  if (n > 0xFFFFFFFEll) return fail(HKV_EINVAL, "batch too large");
+  CHECK_MUT_N();
+  GateScope _gs(t->gate, HKV_ROLE_INSERTER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
   cudaStream_t s = (cudaStream_t)stream;
   HostStage& h = t->stage(s);
   std::lock_guard<std::mutex> hold(h.mu);
@@ -669,6 +705,8 @@ int hkv_find_peer(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uin
   CHECK_T();
   if (!t->peers_dev) return fail(HKV_EINVAL, "no peers set (hkv_set_peers)");
   if (n && (!keys || !found || !out)) return fail(HKV_EINVAL, "null keys/out/found");
+  GateScope _gs(t->gate, HKV_ROLE_READER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
   const uint64_t gmask = ((uint64_t)t->buckets * (uint64_t)t->peer_world) - 1;
   launch_find_peer(t->peers_dev, gmask, t->peer_llog2b, (int)t->cfg.value_dim, keys, n, out, found, zero_misses,
                    t->dev.err, (cudaStream_t)stream, t->num_sms);
@@ -679,6 +717,9 @@ int hkv_find_peer(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uin
 int hkv_erase(hkv_table* t, const uint64_t* keys, int64_t n, uint8_t* outcomes, hkv_stream stream) {
   CHECK_T();
   if (n && (!keys || !outcomes)) return fail(HKV_EINVAL, "null keys/outcomes");
+  CHECK_MUT_N();
+  GateScope _gs(t->gate, HKV_ROLE_INSERTER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
   cudaStream_t s = (cudaStream_t)stream;
   OpArgs a{};
   a.keys = keys;
@@ -704,6 +745,9 @@ int hkv_assign(hkv_table* t, const uint64_t* keys, const float* values, const ui
     refresh = 0;
   }
   if (n && (!keys || !outcomes)) return fail(HKV_EINVAL, "null keys/outcomes");
+  CHECK_MUT_N();
+  GateScope _gs(t->gate, HKV_ROLE_UPDATER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = run_assign(t->dev, keys, values, scores, refresh, t->epoch, n, outcomes, ticks, clock_advance,
                              t->log2b, t->workspace(s), s, t->num_sms);
@@ -720,6 +764,8 @@ int hkv_export(hkv_table* t, int64_t cursor, int64_t max_count, int32_t has_min_
   if (max_count < 1) return fail(HKV_EINVAL, "max_count must be >= 1");
   if (!count || !next_cursor || !out_keys || !out_values || !out_scores) return fail(HKV_EINVAL, "null output");
   if (row_mask && (mask_rows < 0 || cursor + mask_rows > t->cfg.capacity)) return fail(HKV_EINVAL, "mask range");
+  GateScope _gs(t->gate, HKV_ROLE_READER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = run_export(t->dev, cursor, max_count, has_min_score, min_score, row_mask, mask_rows, out_keys,
                              out_values, out_scores, count, next_cursor, t->workspace(s), s, t->num_sms);
@@ -736,6 +782,8 @@ static int read_scalars(hkv_table* t, TableScalars* h, hkv_stream stream) {
 int hkv_size(hkv_table* t, int64_t* size, hkv_stream stream) {
   if (!t || !size) return fail(HKV_EINVAL, "null argument");
   DeviceGuard _g(t->cfg.device);
+  GateScope _gs(t->gate, HKV_ROLE_READER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
   TableScalars h;
   int rc = read_scalars(t, &h, stream);
   if (rc) return rc;
@@ -813,6 +861,8 @@ int hkv_import_state(hkv_table* t, const uint64_t* keys, const uint8_t* digests,
                      const float* values, uint64_t clock, int32_t fel_set, double fel) {
   if (!t || !keys || !digests || !scores || !values) return fail(HKV_EINVAL, "null argument");
   DeviceGuard _g(t->cfg.device);
+  GateScope _gs(t->gate, HKV_ROLE_INSERTER, (cudaStream_t)0);
+  if (_gs.rc) return gate_fail(_gs.rc);
   const uint64_t cap = (uint64_t)t->cfg.capacity, dim = (uint64_t)t->cfg.value_dim;
   cudaError_t e;
   if ((e = cudaMemcpy(t->keys, keys, cap * 8, cudaMemcpyHostToDevice)) ||
@@ -840,6 +890,8 @@ int hkv_export_state(hkv_table* t, uint64_t* keys, uint8_t* digests, uint64_t* s
                      int64_t* occupancy) {
   if (!t) return fail(HKV_EINVAL, "null table");
   DeviceGuard _g(t->cfg.device);
+  GateScope _gs(t->gate, HKV_ROLE_READER, (cudaStream_t)0);
+  if (_gs.rc) return gate_fail(_gs.rc);
   const uint64_t cap = (uint64_t)t->cfg.capacity, dim = (uint64_t)t->cfg.value_dim;
   cudaError_t e = cudaDeviceSynchronize();
   if (e) return cuda_fail(e, "export sync");
@@ -868,9 +920,25 @@ int hkv_export_state(hkv_table* t, uint64_t* keys, uint8_t* digests, uint64_t* s
   return HKV_OK;
 }
 
+int hkv_read_rows(hkv_table* t, int64_t row0, int64_t nrows, uint64_t* keys, uint64_t* scores, hkv_stream stream) {
+  if (!t) return fail(HKV_EINVAL, "null table");
+  if (row0 < 0 || nrows < 0 || row0 + nrows > t->cfg.capacity) return fail(HKV_EINVAL, "row range out of bounds");
+  DeviceGuard _g(t->cfg.device);
+  GateScope _gs(t->gate, HKV_ROLE_READER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  if (keys && nrows) e = cudaMemcpyAsync(keys, t->keys + row0, (size_t)nrows * 8, cudaMemcpyDefault, s);
+  if (!e && scores && nrows) e = cudaMemcpyAsync(scores, t->scores + row0, (size_t)nrows * 8, cudaMemcpyDefault, s);
+  if (!e) e = cudaStreamSynchronize(s);
+  return e ? cuda_fail(e, "hkv_read_rows") : HKV_OK;
+}
+
 int hkv_snapshot(hkv_table* t, hkv_stream stream) {
   if (!t) return fail(HKV_EINVAL, "null table");
   DeviceGuard _g(t->cfg.device);
+  GateScope _gs(t->gate, HKV_ROLE_READER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
   const uint64_t cap = (uint64_t)t->cfg.capacity;
   cudaError_t e;
   if (!t->snap_keys) {
@@ -898,6 +966,8 @@ int hkv_restore(hkv_table* t, hkv_stream stream) {
   if (!t) return fail(HKV_EINVAL, "null table");
   if (!t->snap_keys) return fail(HKV_EINVAL, "no snapshot taken");
   DeviceGuard _g(t->cfg.device);
+  GateScope _gs(t->gate, HKV_ROLE_INSERTER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
   const uint64_t cap = (uint64_t)t->cfg.capacity;
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
@@ -915,6 +985,8 @@ int hkv_restore(hkv_table* t, hkv_stream stream) {
 int hkv_check_consistency(hkv_table* t, int32_t* ok, hkv_stream stream) {
   if (!t || !ok) return fail(HKV_EINVAL, "null argument");
   DeviceGuard _g(t->cfg.device);
+  GateScope _gs(t->gate, HKV_ROLE_READER, (cudaStream_t)stream);
+  if (_gs.rc) return gate_fail(_gs.rc);
   cudaStream_t s = (cudaStream_t)stream;
   int init[4] = {1, 0, 0, 0};
   cudaError_t e = cudaMemcpyAsync(t->sc->check, init, sizeof(init), cudaMemcpyHostToDevice, s);

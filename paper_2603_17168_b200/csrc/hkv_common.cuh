@@ -62,7 +62,14 @@ struct TableDev {
   int* err;                      // error latch
   int* fel_set;
   double* fel;
+  const unsigned* role_word;     // device mirror of the role gate: (group << 2) | (role + 1)
 };
+
+// Mutation kernels refuse to run while the gate's device mirror names a
+// reader group (hkv_gate.cu; HKV_DERR_ROLE = 2 in the error latch).
+__device__ __forceinline__ bool role_forbids_mutation(const TableDev& t) {
+  return t.role_word != nullptr && ((*(volatile const unsigned*)t.role_word) & 3u) == 1u;
+}
 
 // hashing.py:21-29 fmix64 (Murmur3 finalizer)
 __device__ __forceinline__ uint64_t fmix64(uint64_t x) {

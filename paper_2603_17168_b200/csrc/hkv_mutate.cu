@@ -43,6 +43,7 @@ __global__ void k_prep(TableDev t, const uint64_t* __restrict__ keys, int64_t n,
   if (i == 0) {
     sc->first_ev = 0xFFFFFFFFu;
     sc->size_before = (long long)*t.size;
+    if (role_forbids_mutation(t)) atomicOr(&sc->err, 2);
   }
   if (i >= n) return;
   const uint64_t key = keys[i];
@@ -1046,6 +1047,7 @@ __global__ void __launch_bounds__(256) k_assign_find(TableDev t, const uint64_t*
   block_ctrs_init(bc);
   ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
   int bad = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && role_forbids_mutation(t)) atomicOr(&sc->err, 2);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t key = keys[i];
     bad |= key >= kLockedKey;  // table.py:168-169: the apply pass then performs no mutation
@@ -1459,7 +1461,10 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
     }
   }
   ktimer_begin("finalize", s, 2);
-  k_finalize<<<kFinBlocks, 1024, 0, s>>>(t, ws.sc, a.op == kOpErase ? nullptr : a.outcomes, n, clock_advance, 0);
+  // an empty batch never runs k_prep, which seeds first_ev: no outcomes, so
+  // first_eviction_lambda cannot latch from the zeroed scratch
+  k_finalize<<<kFinBlocks, 1024, 0, s>>>(t, ws.sc, (a.op == kOpErase || n == 0) ? nullptr : a.outcomes, n,
+                                         clock_advance, 0);
   ktimer_end("finalize", s, 2);
   g_launches++;
   long long* nev = reinterpret_cast<long long*>(n_evicted);

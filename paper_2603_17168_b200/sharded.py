@@ -260,7 +260,9 @@ class ShardedCacheTable:
                 k, v, s, n = self.local.export_batch_if(min_score, max(cursor - lo, 0), max_count - taken)
                 payload = (np.asarray(k), np.asarray(v), np.asarray(s), None if n is None else n + lo)
             box = [payload]
-            dist.broadcast_object_list(box, src=r, group=self.group)
+            # src is a GLOBAL rank even when the table lives on a subgroup
+            src = r if self.group is None else dist.get_global_rank(self.group, r)
+            dist.broadcast_object_list(box, src=src, group=self.group)
             k, v, s, n = box[0]
             ks.append(k)
             vs.append(v)

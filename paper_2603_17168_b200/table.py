@@ -31,7 +31,7 @@ import torch
 
 from . import _lib
 from .gate import Role, RoleGate
-from .metrics import TxnCounters
+from .metrics import DeviceTxnCounters, TxnCounters
 from .scoring import EpochState, PolicyId
 
 BUCKET_SLOTS = 128
@@ -142,7 +142,9 @@ class CacheTable:
         self._h = h
         self._bucket_mask = config.bucket_count - 1
         self.epoch = EpochState(0)
-        self.gate = RoleGate(event_hook=gate_event_hook)
+        gh = C.c_void_p()
+        _lib.check(self._lib.hkv_table_gate(h, C.byref(gh)))
+        self.gate = RoleGate(event_hook=gate_event_hook, _handle=gh)  # the table's native gate (hkv_gate.cu)
         self.events = None  # record_events: event logs are a CPU-reference debug feature
         self.validate_keys = True
 
@@ -223,6 +225,8 @@ class CacheTable:
             return
         bits = C.c_int32()
         _lib.check(self._lib.hkv_device_error(self._h, C.byref(bits), self._sp()))
+        if bits.value & 2:
+            raise RuntimeError("a mutation kernel ran outside an inserter/updater group (role gate violated)")
         if bits.value & 1:
             raise ValueError("keys must not equal a reserved sentinel value")
 
@@ -264,7 +268,7 @@ class CacheTable:
         found = torch.empty(n, dtype=torch.bool, device=self.device)
         _t1 = time.perf_counter() if _TRACE else 0.0
         st = self._stream()
-        with self.gate.acquire(Role.Reader, st):
+        with self.gate.scope(Role.Reader, st):
             _t2 = time.perf_counter() if _TRACE else 0.0
             _lib.check(self._lib.hkv_find(self._h, _ptr(k), n, _ptr(out_d), _ptr(found), zero_misses, self._sp()))
             _t3 = time.perf_counter() if _TRACE else 0.0
@@ -321,7 +325,7 @@ class CacheTable:
         elif tuple(out.shape) != (n, dim) or out.dtype != torch.float32 or not out.is_contiguous():
             raise ValueError("out must be float32 with shape (len(keys), value_dim)")
         found = torch.empty(n, dtype=torch.bool, pin_memory=True)
-        with self.gate.acquire(Role.Reader, self._stream()):
+        with self.gate.scope(Role.Reader, self._stream()):
             _lib.check(self._lib.hkv_find_host(self._h, _ptr(k), n, _ptr(out), _ptr(found), zero_misses,
                                                self._sp()))
         self._check_device_error()
@@ -347,7 +351,7 @@ class CacheTable:
         elif scores is not None:
             raise ValueError("explicit scores require the kCustomized policy")
         outcomes = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-        with self.gate.acquire(Role.Inserter, self._stream()):
+        with self.gate.scope(Role.Inserter, self._stream()):
             _lib.check(self._lib.hkv_upsert_host(self._h, op, _ptr(k), _ptr(v), _ptr(s), n, _ptr(outcomes), None,
                                                  int(clock_advance), self._sp()))
         self._check_device_error()
@@ -369,7 +373,7 @@ class CacheTable:
         if out is None:
             out = torch.empty((n, dim), dtype=torch.float32, device=self.device)
         found = torch.empty(n, dtype=torch.bool, device=self.device)
-        with self.gate.acquire(Role.Reader, self._stream()):
+        with self.gate.scope(Role.Reader, self._stream()):
             _lib.check(self._lib.hkv_find_peer(self._h, _ptr(k), n, _ptr(out), _ptr(found), zero, self._sp()))
         self._check_device_error()
         return found, out
@@ -378,7 +382,7 @@ class CacheTable:
         k, np_mode = self._keys_in(keys)
         n = k.numel()
         found = torch.empty(n, dtype=torch.bool, device=self.device)
-        with self.gate.acquire(Role.Reader, self._stream()):
+        with self.gate.scope(Role.Reader, self._stream()):
             _lib.check(self._lib.hkv_contains(self._h, _ptr(k), n, _ptr(found), self._sp()))
         if not np_mode:
             self._check_device_error()
@@ -391,7 +395,7 @@ class CacheTable:
         found = torch.empty(n, dtype=torch.bool, device=self.device)
         tier = torch.empty(n, dtype=torch.uint8, device=self.device)
         off = torch.empty(n, dtype=torch.int64, device=self.device)
-        with self.gate.acquire(Role.Reader, self._stream()):
+        with self.gate.scope(Role.Reader, self._stream()):
             _lib.check(self._lib.hkv_find_ptr(self._h, _ptr(k), n, _ptr(found), _ptr(tier), _ptr(off), self._sp()))
         if not np_mode:
             self._check_device_error()
@@ -418,7 +422,7 @@ class CacheTable:
         osc = torch.empty(m, dtype=torch.int64, device=self.device)
         cnt = C.c_int64()
         nxt = C.c_int64()
-        with self.gate.acquire(Role.Reader, self._stream()):
+        with self.gate.scope(Role.Reader, self._stream()):
             if predicate is None or isinstance(predicate, (int, np.integer)):
                 has = predicate is not None
                 _lib.check(self._lib.hkv_export(self._h, cursor, m, int(has), int(predicate) if has else 0, None, 0,
@@ -438,17 +442,20 @@ class CacheTable:
         taken = 0
         pos = cursor
         next_cursor = -1
-        keys_flat = None
+        kbuf = np.empty(chunk, dtype=np.uint64)
+        sbuf = np.empty(chunk, dtype=np.uint64)
         while pos < cap and taken < m:
             hi = min(pos + chunk, cap)
-            kc = self._dev_keys_flat()[pos:hi].cpu().numpy().view(np.uint64)
-            sc = self._dev_scores_flat()[pos:hi].cpu().numpy().view(np.uint64)
+            # only this chunk's keys and scores cross PCIe (hkv_read_rows)
+            kc, sc = kbuf[: hi - pos], sbuf[: hi - pos]
+            _lib.check(self._lib.hkv_read_rows(self._h, pos, hi - pos, kc.ctypes.data_as(C.c_void_p),
+                                               sc.ctypes.data_as(C.c_void_p), self._sp()))
             # reference evaluates the predicate per 64-bucket chunk (table.py:402-409)
             mask = np.zeros(hi - pos, dtype=bool)
             sub = 64 * BUCKET_SLOTS
             for a in range(0, hi - pos, sub):
                 b = min(a + sub, hi - pos)
-                mask[a:b] = np.asarray(predicate(kc[a:b], sc[a:b]), dtype=bool)
+                mask[a:b] = np.asarray(predicate(kc[a:b].copy(), sc[a:b].copy()), dtype=bool)
             md = torch.from_numpy(mask.view(np.uint8)).to(self.device)
             cnt = C.c_int64()
             nxt = C.c_int64()
@@ -479,7 +486,7 @@ class CacheTable:
         n = k.numel()
         outcomes = torch.empty(n, dtype=torch.uint8, device=self.device)
         tk = None if ticks is None else ticks.to(self.device).contiguous()
-        with self.gate.acquire(Role.Updater, self._stream()):
+        with self.gate.scope(Role.Updater, self._stream()):
             _lib.check(self._lib.hkv_assign(self._h, _ptr(k), _ptr(v), _ptr(s), int(refresh), n, _ptr(outcomes),
                                             _ptr(tk), int(clock_advance), self._sp()))
         self._check_device_error()
@@ -495,7 +502,7 @@ class CacheTable:
         s = self._scores_in(scores, n)
         outcomes = torch.empty(n, dtype=torch.uint8, device=self.device)
         tk = None if ticks is None else ticks.to(self.device).contiguous()
-        with self.gate.acquire(Role.Inserter, self._stream()):
+        with self.gate.scope(Role.Inserter, self._stream()):
             _lib.check(self._lib.hkv_upsert(self._h, 0, _ptr(k), _ptr(v), _ptr(s), n, _ptr(outcomes), None, None,
                                             None, None, _ptr(tk), int(clock_advance), self._sp()))
         self._check_device_error()
@@ -515,7 +522,7 @@ class CacheTable:
         es = torch.empty(n, dtype=torch.int64, device=self.device)
         ne = torch.zeros(1, dtype=torch.int64, device=self.device)
         tk = None if ticks is None else ticks.to(self.device).contiguous()
-        with self.gate.acquire(Role.Inserter, self._stream()):
+        with self.gate.scope(Role.Inserter, self._stream()):
             _lib.check(self._lib.hkv_upsert(self._h, 0, _ptr(k), _ptr(v), _ptr(s), n, _ptr(outcomes), _ptr(ek),
                                             _ptr(ev), _ptr(es), _ptr(ne), _ptr(tk), int(clock_advance), self._sp()))
         self._check_device_error()
@@ -552,7 +559,7 @@ class CacheTable:
         s = self._scores_in(scores, n)
         outcomes = torch.empty(n, dtype=torch.uint8, device=self.device)
         tk = None if ticks is None else ticks.to(self.device).contiguous()
-        with self.gate.acquire(Role.Inserter, self._stream()):
+        with self.gate.scope(Role.Inserter, self._stream()):
             _lib.check(self._lib.hkv_upsert(self._h, 1, _ptr(k), _ptr(vd), _ptr(s), n, _ptr(outcomes), None, None,
                                             None, None, _ptr(tk), int(clock_advance), self._sp()))
         self._check_device_error()
@@ -564,7 +571,7 @@ class CacheTable:
         k, np_mode = self._keys_in(keys)
         n = k.numel()
         outcomes = torch.empty(n, dtype=torch.uint8, device=self.device)
-        with self.gate.acquire(Role.Inserter, self._stream()):
+        with self.gate.scope(Role.Inserter, self._stream()):
             _lib.check(self._lib.hkv_erase(self._h, _ptr(k), n, _ptr(outcomes), self._sp()))
         self._check_device_error()
         return self._out(outcomes, np_mode)
@@ -572,7 +579,7 @@ class CacheTable:
     # ----- size / clock / epoch (table.py:192-215) ---------------------------
     def size(self) -> int:
         v = C.c_int64()
-        with self.gate.acquire(Role.Reader, self._stream()):
+        with self.gate.scope(Role.Reader, self._stream()):
             _lib.check(self._lib.hkv_size(self._h, C.byref(v), self._sp()))
         return int(v.value)
 
@@ -604,9 +611,18 @@ class CacheTable:
 
     @property
     def counters(self) -> TxnCounters:
+        """Live device counters (metrics.py:14-39): reset() / snapshot() /
+        field reads go to the device."""
+        c = self.__dict__.get("_counters")
+        if c is None:
+            c = self.__dict__["_counters"] = DeviceTxnCounters(self)
+        return c
+
+    def _device_counters(self) -> dict:
         arr = (C.c_int64 * 6)()
         _lib.check(self._lib.hkv_counters(self._h, arr, self._sp()))
-        return TxnCounters(*[int(x) for x in arr])
+        return dict(zip(("digest_line_loads", "full_key_compares", "score_scans", "slot_lock_retries",
+                         "value_copies_fast", "value_copies_overflow"), (int(x) for x in arr)))
 
     def reset_counters(self) -> None:
         _lib.check(self._lib.hkv_reset_counters(self._h, self._sp()))
@@ -695,7 +711,7 @@ class CacheTable:
     def check_consistency(self) -> bool:
         """Device full scan (table.py:1284-1299)."""
         ok = C.c_int32()
-        with self.gate.acquire(Role.Reader, self._stream()):
+        with self.gate.scope(Role.Reader, self._stream()):
             _lib.check(self._lib.hkv_check_consistency(self._h, C.byref(ok), self._sp()))
         if not ok.value:
             raise ConsistencyError("occupancy / size / digest disagree with bucket contents")
