@@ -190,6 +190,35 @@ int hkv_assign(hkv_table *t, const uint64_t *keys, const float *values, const ui
                int32_t refresh, int64_t n, uint8_t *outcomes, const uint64_t *ticks,
                uint64_t clock_advance, hkv_stream stream);
 
+/* ---- single-key API (table.py:562-620; LookupResult / UpsertResult 78-91) ----
+ * One key per call, synchronous, host arguments.  Reader role for the
+ * lookups, inserter role for the upserts.
+ *   hkv_lookup          probe h1, then h2 in dual mode (table.py:562-568, 621-631)
+ *   hkv_find_in_bucket  probe one bucket; a miss is definitive for it (570-582)
+ *   hkv_upsert_single   update / insert / reject / evict in bucket h1 only,
+ *                       also on a dual-mode table (584-599, 695-735)
+ *   hkv_upsert_dual     dual-mode two-bucket upsert (601-620, 859-924);
+ *                       HKV_EINVAL on a single-mode table
+ * has_score / score: the optional explicit score (kCustomized).  As in the
+ * scalar engine, a score given to a non-kCustomized table is an error only
+ * when the key is absent (table.py:662-672).  Ticks: one per non-custom hit
+ * or insert decision.  result->kind is an hkv_outcome; bucket / slot are -1
+ * for misses and rejections; evicted_key / evicted_score are valid for
+ * HKV_EVICTED. */
+typedef struct {
+    int32_t kind;
+    int32_t slot;
+    int64_t bucket;
+    uint64_t evicted_key;
+    uint64_t evicted_score;
+} hkv_one_result;
+int hkv_lookup(hkv_table *t, uint64_t key, hkv_one_result *result, hkv_stream stream);
+int hkv_find_in_bucket(hkv_table *t, int64_t bucket, uint64_t key, hkv_one_result *result, hkv_stream stream);
+int hkv_upsert_single(hkv_table *t, uint64_t key, const float *value, int32_t has_score, uint64_t score,
+                      hkv_one_result *result, hkv_stream stream);
+int hkv_upsert_dual(hkv_table *t, uint64_t key, const float *value, int32_t has_score, uint64_t score,
+                    hkv_one_result *result, hkv_stream stream);
+
 /* erase (table.py:553-558, 1006-1023). */
 int hkv_erase(hkv_table *t, const uint64_t *keys, int64_t n, uint8_t *outcomes, hkv_stream stream);
 
@@ -235,6 +264,11 @@ int hkv_export_state(hkv_table *t, uint64_t *keys, uint8_t *digests, uint64_t *s
  * predicate sees one chunk of rows at a time. */
 int hkv_read_rows(hkv_table *t, int64_t row0, int64_t nrows, uint64_t *keys, uint64_t *scores,
                   hkv_stream stream);
+
+/* Value rows [row0, row0 + nrows) (global rows; either tier) into host or
+ * device memory.  SYNCHRONISING.  Reads a LookupResult's value handle
+ * (store.py:96-100). */
+int hkv_read_value_rows(hkv_table *t, int64_t row0, int64_t nrows, float *out, hkv_stream stream);
 
 /* Metadata snapshot held in HBM (keys, digests, scores, occupancy bits, size,
  * clock): the bench restores it between timed repeats so the load factor

@@ -481,6 +481,113 @@ int64_t ot_export(ot_table *t, int64_t cursor, int64_t max_count, int32_t has_mi
 }
 
 /* Accessors for ctypes. */
+/* ---- scalar single-key API (table.py:562-620) ----------------------------
+ * ot_lookup_one: lookup (bucket < 0: h1 then h2 in dual mode, table.py:621-631)
+ * or find_in_bucket (table.py:570-582).  res = {kind, bucket, slot}.
+ * ot_upsert_one: upsert_single (dual = 0: bucket h1 only, 584-599 ->
+ * _scalar_upsert_bucket 695-735, locked=False) or upsert_dual (dual = 1,
+ * 601-620 -> _scalar_upsert_dual 859-924).  Ticks only where the scalar
+ * engine takes them (_scalar_hit 760-762, _score_for_insert 662-672).
+ * Returns 0, or 1 (kCustomized without a score) / 2 (a score without
+ * kCustomized) before any mutation.  res = {kind, bucket, slot}, ev = {key, score}. */
+void ot_lookup_one(ot_table *t, int64_t bucket, uint64_t key, int64_t *res) {
+    uint64_t h = fmix64(key);
+    uint8_t d = digest_of(h);
+    int64_t mask = t->buckets - 1;
+    int64_t b = bucket >= 0 ? bucket : (int64_t)(h & (uint64_t)mask);
+    int s = probe(t, b, key, d, t->ctr);
+    if (s < 0 && bucket < 0 && t->dual) {
+        b = (int64_t)(second_hash(h) & (uint64_t)mask);
+        s = probe(t, b, key, d, t->ctr);
+    }
+    res[0] = s >= 0 ? O_FOUND : O_NOTFOUND;
+    res[1] = s >= 0 ? b : -1;
+    res[2] = s;
+}
+
+static void evict_publish(ot_table *t, int64_t b, int m, uint64_t minv, uint64_t key, uint8_t d, uint64_t s_in,
+                          const float *val, int64_t *res, uint64_t *ev, int64_t *ctr) {
+    /* _scalar_evict 834-857: first eviction recorded at the decision's size */
+    if (!t->fel_set) { t->fel_set = 1; t->fel = (double)t->size / (double)t->capacity; }
+    ev[0] = t->keys[b * SLOTS + m];
+    ev[1] = minv;
+    publish(t, b, m, key, d, s_in, val, ctr);
+    res[0] = O_EVICTED; res[1] = b; res[2] = m;
+}
+
+static int32_t upsert_one(ot_table *t, int32_t dual, uint64_t key, const float *val, int32_t has_score,
+                          uint64_t score, int64_t *res, uint64_t *ev, int64_t *ctr) {
+    uint64_t h = fmix64(key);
+    uint8_t d = digest_of(h);
+    int64_t mask = t->buckets - 1;
+    int64_t b1 = (int64_t)(h & (uint64_t)mask), b2 = (int64_t)(second_hash(h) & (uint64_t)mask);
+    int64_t b = b1;
+    int s = probe(t, b1, key, d, ctr);
+    if (s < 0 && dual) { b = b2; s = probe(t, b2, key, d, ctr); }
+    int custom = t->policy == POL_CUSTOM;
+    ev[0] = ev[1] = 0;
+    res[1] = -1; res[2] = -1;
+    if (s >= 0) {  /* _scalar_hit 749-772 */
+        int64_t row = b * SLOTS + s;
+        if (custom) {
+            if (has_score) t->scores[row] = score;
+        } else {
+            uint64_t tick = ++t->clock;
+            t->scores[row] = hit_score(t->policy, t->scores[row], t->epoch, tick, 0, 0);
+        }
+        memcpy(t->values + row * t->dim, val, sizeof(float) * t->dim);
+        count_row(t, row, ctr);
+        res[0] = O_UPDATED; res[1] = b; res[2] = s;
+        return 0;
+    }
+    if (custom && !has_score) return 1;
+    if (!custom && has_score) return 2;
+    uint64_t s_in = custom ? score : insert_score(t->policy, t->epoch, ++t->clock, 0);
+    if (dual) {
+        if (t->occ[b1] < SLOTS || t->occ[b2] < SLOTS) {  /* D1 */
+            int64_t tb = t->occ[b1] <= t->occ[b2] ? b1 : b2;
+            int f = lowest_empty(t, tb);
+            publish(t, tb, f, key, d, s_in, val, ctr);
+            t->occ[tb]++; t->size++;
+            res[0] = O_INSERTED; res[1] = tb; res[2] = f;
+            return 0;
+        }
+        uint64_t n1, n2;
+        int m1 = argmin_score(t, b1, &n1), m2 = argmin_score(t, b2, &n2);
+        ctr[C_SCANS] += 2;
+        uint64_t both = n1 < n2 ? n1 : n2;
+        int admit = t->admit_ties_unified ? s_in >= both : s_in > both;
+        if (!admit) { res[0] = O_REJECTED; return 0; }
+        if (n2 < n1) evict_publish(t, b2, m2, n2, key, d, s_in, val, res, ev, ctr);
+        else evict_publish(t, b1, m1, n1, key, d, s_in, val, res, ev, ctr);
+        return 0;
+    }
+    if (t->occ[b1] < SLOTS) {  /* _scalar_claim_free 678-693 */
+        int f = lowest_empty(t, b1);
+        publish(t, b1, f, key, d, s_in, val, ctr);
+        t->occ[b1]++; t->size++;
+        res[0] = O_INSERTED; res[1] = b1; res[2] = f;
+        return 0;
+    }
+    uint64_t mn;
+    int m = argmin_score(t, b1, &mn);
+    ctr[C_SCANS]++;
+    if (s_in < mn) { res[0] = O_REJECTED; return 0; }
+    evict_publish(t, b1, m, mn, key, d, s_in, val, res, ev, ctr);
+    return 0;
+}
+
+/* a usage error leaves the table counters untouched: the reference merges a
+ * call's local counters only when it returns (table.py:588-598) */
+int32_t ot_upsert_one(ot_table *t, int32_t dual, uint64_t key, const float *val, int32_t has_score,
+                      uint64_t score, int64_t *res, uint64_t *ev) {
+    int64_t ctr[6] = {0};
+    int32_t rc = upsert_one(t, dual, key, val, has_score, score, res, ev, ctr);
+    if (rc == 0)
+        for (int k = 0; k < 6; k++) t->ctr[k] += ctr[k];
+    return rc;
+}
+
 uint64_t *ot_keys(ot_table *t) { return t->keys; }
 uint8_t *ot_digests(ot_table *t) { return t->digests; }
 uint64_t *ot_scores(ot_table *t) { return t->scores; }

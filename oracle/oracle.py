@@ -82,6 +82,9 @@ def lib():
         L.ot_fel.restype = C.c_int32
         L.ot_fel.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
         L.ot_set_fel.argtypes = [C.c_void_p, C.c_int32, C.c_double]
+        L.ot_lookup_one.argtypes = [C.c_void_p, C.c_int64, C.c_uint64, _i64p]
+        L.ot_upsert_one.restype = C.c_int32
+        L.ot_upsert_one.argtypes = [C.c_void_p, C.c_int32, C.c_uint64, _f32p, C.c_int32, C.c_uint64, _i64p, _u64p]
         L.ot_snapshot.restype = C.c_void_p
         L.ot_snapshot.argtypes = [C.c_void_p]
         L.ot_restore.argtypes = [C.c_void_p, C.c_void_p]
@@ -338,6 +341,54 @@ class OracleTable:
         out = np.zeros(len(k), dtype=np.uint8)
         lib().ot_erase(self._h, _p(k, _u64p), len(k), _p(out, _u8p))
         return out
+
+    # ----- single-key API (table.py:562-620) ---------------------------------
+    def _lookup_one(self, bucket, key):
+        res = np.zeros(3, dtype=np.int64)
+        lib().ot_lookup_one(self._h, bucket, int(key), _p(res, _i64p))
+        if res[0] != 4:
+            return (False, -1, -1, None, None)
+        b, s = int(res[1]), int(res[2])
+        row = b * SLOTS + s
+        fast = b < self.fast_tier_budget
+        off = row * self.dim if fast else (row - self.fast_tier_budget * SLOTS) * self.dim
+        return (True, b, s, 0 if fast else 1, off)
+
+    def lookup(self, key):
+        """-> (found, bucket, slot, tier, offset) (table.py:562-568)."""
+        return self._lookup_one(-1, key)
+
+    def find_in_bucket(self, bucket_index, key):
+        if not (0 <= bucket_index < self.bucket_count):
+            raise IndexError("bucket index out of range")
+        return self._lookup_one(int(bucket_index), key)
+
+    def _upsert_one(self, dual, key, value, score):
+        key = int(key)
+        if key >= LOCKED_KEY:
+            raise ValueError("keys must not equal a reserved sentinel value")
+        v = np.ascontiguousarray(value, dtype=np.float32).reshape(-1)
+        if v.shape != (self.dim,):
+            raise ValueError("value must have value_dim elements")
+        res = np.zeros(3, dtype=np.int64)
+        ev = np.zeros(2, dtype=np.uint64)
+        rc = lib().ot_upsert_one(self._h, dual, key, _p(v, _f32p), int(score is not None),
+                                 0 if score is None else int(score), _p(res, _i64p), _p(ev, _u64p))
+        if rc == 1:
+            raise ValueError("kCustomized requires an explicit score")
+        if rc == 2:
+            raise ValueError("explicit scores require the kCustomized policy")
+        kind = int(res[0])
+        return (kind, int(ev[0]), int(ev[1])) if kind == 3 else (kind, None, None)
+
+    def upsert_single(self, key, value, score=None):
+        """-> (kind, evicted_key, evicted_score) (table.py:584-599)."""
+        return self._upsert_one(0, key, value, score)
+
+    def upsert_dual(self, key, value, score=None):
+        if self.mode != "dual":
+            raise ValueError("upsert_dual requires dual mode")
+        return self._upsert_one(1, key, value, score)
 
     def export_batch_if(self, min_score=None, cursor=None, max_count=1):
         """export_batch_if with the native `score >= min_score` predicate

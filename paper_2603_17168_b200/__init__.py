@@ -14,16 +14,19 @@ from .table import (
     LOCKED_KEY,
     CacheTable,
     ConsistencyError,
+    LookupResult,
     Mode,
     Outcome,
     TableConfig,
     Tier,
+    UpsertResult,
+    ValueHandle,
 )
 
 __all__ = [
     "ALL_POLICIES", "BUCKET_SLOTS", "CacheTable", "ConsistencyError", "EMPTY_KEY", "EpochState", "LOCKED_KEY",
-    "MAX_SCORE", "Mode", "Outcome", "PolicyId", "ROLE_OF_OPERATION", "Role", "RoleGate", "RoleGuard",
-    "TableConfig", "Tier", "TxnCounters",
+    "LookupResult", "MAX_SCORE", "Mode", "Outcome", "PolicyId", "ROLE_OF_OPERATION", "Role", "RoleGate", "RoleGuard",
+    "TableConfig", "Tier", "TxnCounters", "UpsertResult", "ValueHandle",
 ]
 
 __version__ = "0.1.0"

@@ -67,6 +67,11 @@ SIGNATURES = {
     "hkv_export_state": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "hkv_snapshot": (C.c_int, [_vp, _vp]),
     "hkv_read_rows": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
+    "hkv_read_value_rows": (C.c_int, [_vp, _i64, _i64, _vp, _vp]),
+    "hkv_lookup": (C.c_int, [_vp, _u64, _vp, _vp]),
+    "hkv_find_in_bucket": (C.c_int, [_vp, _i64, _u64, _vp, _vp]),
+    "hkv_upsert_single": (C.c_int, [_vp, _u64, _vp, _i32, _u64, _vp, _vp]),
+    "hkv_upsert_dual": (C.c_int, [_vp, _u64, _vp, _i32, _u64, _vp, _vp]),
     "hkv_restore": (C.c_int, [_vp, _vp]),
     "hkv_check_consistency": (C.c_int, [_vp, C.POINTER(_i32), _vp]),
     "hkv_route": (C.c_int, [_vp, _i64, _i64, _i32, _vp, _vp, _vp]),

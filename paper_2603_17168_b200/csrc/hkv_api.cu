@@ -3,6 +3,7 @@
 // entry points that replace cachekv.CacheTable's methods.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -13,6 +14,7 @@
 #include "../../include/hkv_b200.h"
 #include "hkv_gate.h"
 #include "hkv_kernels.h"
+#include "hkv_single.h"
 
 namespace {
 thread_local std::string g_err;
@@ -182,6 +184,8 @@ struct hkv_table {
   float* vover_host = nullptr;  // pinned host allocation (mapped), if used
   TableScalars* sc = nullptr;
   unsigned* role_word = nullptr;  // device mirror of the gate's group (never snapshotted)
+  OneResult* one = nullptr;       // single-key API: result + value row staging (lazy)
+  float* one_val = nullptr;
   hkv_gate* gate = nullptr;
   unsigned long long* lead = nullptr;
   // metadata snapshot
@@ -249,6 +253,8 @@ void free_table(hkv_table* t) {
   if (!t) return;
   DeviceGuard g(t->cfg.device);
   if (t->gate) gate_delete(t->gate);
+  if (t->one) cudaFree(t->one);
+  if (t->one_val) cudaFree(t->one_val);
   void* dptrs[] = {t->keys, t->digests, t->scores, t->bits, t->smin, t->svalid, t->vfast, t->sc, t->role_word, t->lead,
                    t->snap_keys, t->snap_digests, t->snap_scores, t->snap_bits, t->snap_smin, t->snap_svalid,
                    t->snap_sc};
@@ -714,6 +720,76 @@ int hkv_find_peer(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uin
   return e ? cuda_fail(e, "hkv_find_peer") : HKV_OK;
 }
 
+// ---- single-key API -------------------------------------------------------
+static int one_ready(hkv_table* t) {
+  cudaError_t e = cudaSuccess;
+  if (!t->one) e = cudaMalloc((void**)&t->one, sizeof(OneResult));
+  if (!e && !t->one_val) e = cudaMalloc((void**)&t->one_val, (size_t)t->cfg.value_dim * 4);
+  return e ? cuda_fail(e, "single-key staging") : HKV_OK;
+}
+
+static int one_finish(hkv_table* t, hkv_one_result* result, cudaStream_t s, const char* where) {
+  OneResult h;
+  cudaError_t e = cudaMemcpyAsync(&h, t->one, sizeof(h), cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaStreamSynchronize(s);
+  if (e) return cuda_fail(e, where);
+  if (h.status == 1) return fail(HKV_EINVAL, "kCustomized requires an explicit score");
+  if (h.status == 2) return fail(HKV_EINVAL, "explicit scores require the kCustomized policy");
+  result->kind = h.kind;
+  result->slot = h.slot;
+  result->bucket = h.bucket;
+  result->evicted_key = h.evicted_key;
+  result->evicted_score = h.evicted_score;
+  return HKV_OK;
+}
+
+static int lookup_one(hkv_table* t, int64_t bucket, uint64_t key, hkv_one_result* result, hkv_stream stream) {
+  if (!t || !result) return fail(HKV_EINVAL, "null argument");
+  DeviceGuard _g(t->cfg.device);
+  if (bucket >= t->buckets) return fail(HKV_EINVAL, "bucket index out of range");
+  cudaStream_t s = (cudaStream_t)stream;
+  GateScope _gs(t->gate, HKV_ROLE_READER, s);
+  if (_gs.rc) return gate_fail(_gs.rc);
+  if (int rc = one_ready(t)) return rc;
+  launch_lookup_one(t->dev, key, bucket, t->one, s);
+  return one_finish(t, result, s, "hkv_lookup");
+}
+
+int hkv_lookup(hkv_table* t, uint64_t key, hkv_one_result* result, hkv_stream stream) {
+  return lookup_one(t, -1, key, result, stream);
+}
+
+int hkv_find_in_bucket(hkv_table* t, int64_t bucket, uint64_t key, hkv_one_result* result, hkv_stream stream) {
+  if (bucket < 0) return fail(HKV_EINVAL, "bucket index out of range");
+  return lookup_one(t, bucket, key, result, stream);
+}
+
+static int upsert_one(hkv_table* t, int dual, uint64_t key, const float* value, int32_t has_score, uint64_t score,
+                      hkv_one_result* result, hkv_stream stream) {
+  if (!t || !value || !result) return fail(HKV_EINVAL, "null argument");
+  if (dual && t->cfg.mode != HKV_MODE_DUAL) return fail(HKV_EINVAL, "upsert_dual requires dual mode");
+  if (key >= 0xFFFFFFFFFFFFFFFEull) return fail(HKV_EINVAL, "keys must not equal a reserved sentinel value");
+  DeviceGuard _g(t->cfg.device);
+  cudaStream_t s = (cudaStream_t)stream;
+  GateScope _gs(t->gate, HKV_ROLE_INSERTER, s);
+  if (_gs.rc) return gate_fail(_gs.rc);
+  if (int rc = one_ready(t)) return rc;
+  cudaError_t e = cudaMemcpyAsync(t->one_val, value, (size_t)t->cfg.value_dim * 4, cudaMemcpyDefault, s);
+  if (e) return cuda_fail(e, "single-key value");
+  launch_upsert_one(t->dev, key, t->one_val, dual, has_score != 0, score, t->epoch, t->one, s);
+  return one_finish(t, result, s, dual ? "hkv_upsert_dual" : "hkv_upsert_single");
+}
+
+int hkv_upsert_single(hkv_table* t, uint64_t key, const float* value, int32_t has_score, uint64_t score,
+                      hkv_one_result* result, hkv_stream stream) {
+  return upsert_one(t, 0, key, value, has_score, score, result, stream);
+}
+
+int hkv_upsert_dual(hkv_table* t, uint64_t key, const float* value, int32_t has_score, uint64_t score,
+                    hkv_one_result* result, hkv_stream stream) {
+  return upsert_one(t, 1, key, value, has_score, score, result, stream);
+}
+
 int hkv_erase(hkv_table* t, const uint64_t* keys, int64_t n, uint8_t* outcomes, hkv_stream stream) {
   CHECK_T();
   if (n && (!keys || !outcomes)) return fail(HKV_EINVAL, "null keys/outcomes");
@@ -932,6 +1008,26 @@ int hkv_read_rows(hkv_table* t, int64_t row0, int64_t nrows, uint64_t* keys, uin
   if (!e && scores && nrows) e = cudaMemcpyAsync(scores, t->scores + row0, (size_t)nrows * 8, cudaMemcpyDefault, s);
   if (!e) e = cudaStreamSynchronize(s);
   return e ? cuda_fail(e, "hkv_read_rows") : HKV_OK;
+}
+
+int hkv_read_value_rows(hkv_table* t, int64_t row0, int64_t nrows, float* out, hkv_stream stream) {
+  if (!t || (nrows && !out)) return fail(HKV_EINVAL, "null argument");
+  if (row0 < 0 || nrows < 0 || row0 + nrows > t->cfg.capacity) return fail(HKV_EINVAL, "row range out of bounds");
+  DeviceGuard _g(t->cfg.device);
+  cudaStream_t s = (cudaStream_t)stream;
+  GateScope _gs(t->gate, HKV_ROLE_READER, s);
+  if (_gs.rc) return gate_fail(_gs.rc);
+  const uint64_t dim = (uint64_t)t->cfg.value_dim;
+  cudaError_t e = cudaSuccess;
+  for (int64_t r = row0; r < row0 + nrows && !e;) {  // a range may straddle the tier boundary
+    const bool fast = (uint64_t)r < t->fast_rows;
+    const int64_t end = fast ? std::min<int64_t>(row0 + nrows, (int64_t)t->fast_rows) : row0 + nrows;
+    const float* src = fast ? t->vfast + (uint64_t)r * dim : t->vover + ((uint64_t)r - t->fast_rows) * dim;
+    e = cudaMemcpyAsync(out + (uint64_t)(r - row0) * dim, src, (size_t)(end - r) * dim * 4, cudaMemcpyDefault, s);
+    r = end;
+  }
+  if (!e) e = cudaStreamSynchronize(s);
+  return e ? cuda_fail(e, "hkv_read_value_rows") : HKV_OK;
 }
 
 int hkv_snapshot(hkv_table* t, hkv_stream stream) {

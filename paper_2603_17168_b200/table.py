@@ -65,6 +65,33 @@ class ConsistencyError(RuntimeError):
     pass
 
 
+@dataclass(frozen=True)
+class ValueHandle:  # store.py:30-33
+    tier: Tier
+    offset: int  # element index into the tier arena
+
+
+@dataclass(frozen=True)
+class LookupResult:  # table.py:78-83
+    found: bool
+    bucket_index: int = -1
+    slot_index: int = -1
+    value_handle: Optional[ValueHandle] = None
+
+
+@dataclass(frozen=True)
+class UpsertResult:  # table.py:86-91
+    kind: Outcome
+    evicted_key: Optional[int] = None
+    evicted_score: Optional[int] = None
+    evicted_value: Optional[np.ndarray] = None
+
+
+class _OneResult(C.Structure):  # hkv_one_result (include/hkv_b200.h)
+    _fields_ = [("kind", C.c_int32), ("slot", C.c_int32), ("bucket", C.c_int64), ("evicted_key", C.c_uint64),
+                ("evicted_score", C.c_uint64)]
+
+
 _POLICY_CODE = {PolicyId.kLru: 0, PolicyId.kLfu: 1, PolicyId.kEpochLru: 2, PolicyId.kEpochLfu: 3,
                 PolicyId.kCustomized: 4}
 
@@ -575,6 +602,81 @@ class CacheTable:
             _lib.check(self._lib.hkv_erase(self._h, _ptr(k), n, _ptr(outcomes), self._sp()))
         self._check_device_error()
         return self._out(outcomes, np_mode)
+
+    # ----- single-key API (table.py:562-620) ---------------------------------
+    def value_address(self, bucket_index: int, slot_index: int) -> ValueHandle:
+        """(bucket, slot) -> (tier, element offset) (store.py:84-94)."""
+        if not (0 <= bucket_index < self.config.bucket_count):
+            raise ValueError("bucket index out of range")
+        if not (0 <= slot_index < BUCKET_SLOTS):
+            raise ValueError("slot index out of range")
+        dim, budget = self.config.value_dim, self.config.fast_tier_budget
+        off = (bucket_index * BUCKET_SLOTS + slot_index) * dim
+        if bucket_index < budget:
+            return ValueHandle(Tier.Fast, off)
+        return ValueHandle(Tier.Overflow, off - budget * BUCKET_SLOTS * dim)
+
+    def _lookup_result(self, r: "_OneResult") -> LookupResult:
+        if r.kind != int(Outcome.Found):
+            return LookupResult(False)
+        return LookupResult(True, int(r.bucket), int(r.slot), self.value_address(int(r.bucket), int(r.slot)))
+
+    def lookup(self, key: int) -> LookupResult:
+        """Single-key find returning slot coordinates and a value handle."""
+        r = _OneResult()
+        with self.gate.scope(Role.Reader, self._stream()):
+            _lib.check(self._lib.hkv_lookup(self._h, int(key) & EMPTY_KEY, C.byref(r), self._sp()))
+        return self._lookup_result(r)
+
+    def find_in_bucket(self, bucket_index: int, key: int) -> LookupResult:
+        """Digest-accelerated probe of one bucket; a miss is definitive for
+        this bucket."""
+        b = int(bucket_index)
+        if not (0 <= b < self.config.bucket_count):
+            raise IndexError("bucket index out of range")
+        r = _OneResult()
+        with self.gate.scope(Role.Reader, self._stream()):
+            _lib.check(self._lib.hkv_find_in_bucket(self._h, b, int(key) & EMPTY_KEY, C.byref(r), self._sp()))
+        return self._lookup_result(r)
+
+    def _upsert_one(self, fn, key, value, score) -> UpsertResult:
+        key = int(key)
+        if key >= LOCKED_KEY:
+            raise ValueError("keys must not equal a reserved sentinel value")
+        v = np.ascontiguousarray(value, dtype=np.float32).reshape(-1)
+        if v.shape != (self.config.value_dim,):
+            raise ValueError("value must have value_dim elements")
+        r = _OneResult()
+        with self.gate.scope(Role.Inserter, self._stream()):
+            _lib.check(fn(self._h, key, v.ctypes.data_as(C.c_void_p), int(score is not None),
+                          0 if score is None else int(score), C.byref(r), self._sp()))
+        kind = Outcome(int(r.kind))
+        if kind is Outcome.Evicted:
+            return UpsertResult(kind, int(r.evicted_key), int(r.evicted_score))
+        return UpsertResult(kind)
+
+    def upsert_single(self, key: int, value, score: Optional[int] = None) -> UpsertResult:
+        """One-key single-bucket upsert (update / insert / reject / evict)
+        in bucket h1 -- also on a dual-mode table (table.py:584-599)."""
+        return self._upsert_one(self._lib.hkv_upsert_single, key, value, score)
+
+    def upsert_dual(self, key: int, value, score: Optional[int] = None) -> UpsertResult:
+        """One-key dual-bucket upsert: fill the less-occupied candidate while
+        space remains, then evict in the bucket with the lower minimum score
+        (ties rejected unless unified) (table.py:601-620)."""
+        if self.config.mode is not Mode.dual:
+            raise ValueError("upsert_dual requires dual mode")
+        return self._upsert_one(self._lib.hkv_upsert_dual, key, value, score)
+
+    def read_value(self, handle: ValueHandle, out_buffer: Optional[np.ndarray] = None) -> np.ndarray:
+        """The value row a handle addresses (store.py:96-100)."""
+        dim, budget = self.config.value_dim, self.config.fast_tier_budget
+        row = handle.offset // dim + (0 if handle.tier is Tier.Fast else budget * BUCKET_SLOTS)
+        out = np.empty(dim, dtype=np.float32) if out_buffer is None else out_buffer
+        if out.shape != (dim,):
+            raise ValueError("buffer length must equal value_dim")
+        _lib.check(self._lib.hkv_read_value_rows(self._h, row, 1, out.ctypes.data_as(C.c_void_p), self._sp()))
+        return out
 
     # ----- size / clock / epoch (table.py:192-215) ---------------------------
     def size(self) -> int:

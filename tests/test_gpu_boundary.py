@@ -223,3 +223,61 @@ def test_reference_stress_gate_runs_on_b200(ref_bench_on_b200):
     rep = ref_bench_on_b200.stress_gate(threads=6, total_ops=3000, capacity=2**13, dim=4, check=True)
     assert rep.metric("matrix_violations") == [0] and rep.metric("dual_inserters") == [0]
     assert rep.metric("torn_reads") == [0] and rep.metric("gate_events")[0] >= 6000
+
+
+# ----- single-key API (table.py:562-620) vs the oracle ----------------------------------
+MODES = ["single", "dual"]
+POLICIES = ["kLru", "kLfu", "kEpochLru", "kEpochLfu", "kCustomized"]
+
+
+def _norm(r):
+    if hasattr(r, "found"):
+        if not r.found:
+            return (False, -1, -1, None, None)
+        return (True, r.bucket_index, r.slot_index, int(r.value_handle.tier), r.value_handle.offset)
+    return (int(r.kind), r.evicted_key, r.evicted_score)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("policy", POLICIES)
+def test_single_key_api_matches_oracle(hkv, mode, policy):
+    """lookup / find_in_bucket / upsert_single / upsert_dual interleaved with
+    batch upserts: every result, then the raw state and counters, equal the
+    oracle's (pinned to the reference by test_oracle_reference.py)."""
+    from test_oracle_reference import single_key_script
+
+    cap, dim = 128 * 8, 2
+    t = hkv.CacheTable(hkv.TableConfig(capacity=cap, value_dim=dim, mode=mode, score_policy=policy,
+                                       fast_tier_budget=5))
+    o = OracleTable(cap, dim, mode, policy, 5)
+    rng = np.random.default_rng(5)
+    for j, op in enumerate(single_key_script(4, cap, dim, mode, policy, n=2500)):
+        if j % 500 == 499:  # a batch in between: the summary the single-key ops invalidated is rebuilt
+            k = rng.integers(1, 2**63, size=300, dtype=np.uint64)
+            v = rng.standard_normal((300, dim)).astype(np.float32)
+            s = rng.integers(0, 50, size=300, dtype=np.uint64) if policy == "kCustomized" else None
+            assert np.array_equal(t.insert_and_evict(k, v, s)[0], o.insert_and_evict(k, v, s)[0])
+        results = []
+        for impl in (t, o):
+            try:
+                if op[0] == "lookup":
+                    r = impl.lookup(op[1])
+                elif op[0] == "find_in_bucket":
+                    r = impl.find_in_bucket(op[1], op[2])
+                else:
+                    r = getattr(impl, op[0])(op[1], op[2], op[3])
+                results.append(_norm(r) if impl is t else r)
+            except ValueError as e:
+                results.append(("ValueError", str(e)))
+        assert results[0] == results[1], (j, op[0], results)
+    st = t.export_state()
+    assert st["keys"].tobytes() == o.keys.tobytes() and st["scores"].tobytes() == o.scores.tobytes()
+    assert st["values"].tobytes() == o.values.tobytes() and st["digests"].tobytes() == o.digests.tobytes()
+    assert st["size"] == o.size() and st["clock"] == o.clock and st["fel"] == o.first_eviction_lambda
+    assert t.counters.as_dict() == o.counters
+    assert t.check_consistency()
+    # a value handle reads the row the lookup found
+    res = o.occupied_keys()
+    r = t.lookup(int(res[0]))
+    f, v = o.find(res[:1])
+    assert r.found and np.array_equal(t.read_value(r.value_handle), v[0])

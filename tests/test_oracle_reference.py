@@ -56,3 +56,79 @@ def test_oracle_workload_sizes(reference_pkg):
     fr, vr = ref.find(q)
     fo, vo = ora.find(q, threads=4)
     assert np.array_equal(fr, fo) and vr.tobytes() == vo.tobytes()
+
+
+def _norm_lookup(r):
+    if not r.found:
+        return (False, -1, -1, None, None)
+    return (True, r.bucket_index, r.slot_index, int(r.value_handle.tier), r.value_handle.offset)
+
+
+def _norm_upsert(r):
+    return (int(r.kind), r.evicted_key, r.evicted_score)
+
+
+def single_key_script(seed, cap, dim, mode, policy, n=4000):
+    """Mixed single-key ops (lookup / find_in_bucket / upsert_single /
+    upsert_dual) on a small key universe so buckets fill, hits repeat and
+    full-bucket decisions happen; explicit scores where the policy allows
+    (and sometimes where it does not: a usage error only on the miss path)."""
+    rng = np.random.default_rng(seed)
+    universe = rng.integers(1, 2**63, size=3 * cap, dtype=np.uint64)
+    ops = []
+    for i in range(n):
+        key = int(universe[rng.integers(0, len(universe))])
+        val = rng.standard_normal(dim).astype(np.float32)
+        r = rng.random()
+        score = None
+        if policy == "kCustomized":
+            score = int(rng.integers(0, 50)) if rng.random() < 0.95 else None
+        elif rng.random() < 0.03:
+            score = 7
+        if r < 0.25:
+            ops.append(("lookup", key))
+        elif r < 0.35:
+            ops.append(("find_in_bucket", int(rng.integers(0, cap // 128)), key))
+        elif r < 0.7 or mode == "single":
+            ops.append(("upsert_single", key, val, score))
+        else:
+            ops.append(("upsert_dual", key, val, score))
+    return ops
+
+
+def apply_single(t, op, ref):
+    try:
+        if op[0] == "lookup":
+            r = t.lookup(op[1])
+            return _norm_lookup(r) if ref else r
+        if op[0] == "find_in_bucket":
+            r = t.find_in_bucket(op[1], op[2])
+            return _norm_lookup(r) if ref else r
+        r = getattr(t, op[0])(op[1], op[2], op[3])
+        return _norm_upsert(r) if ref else r
+    except ValueError as e:
+        return ("ValueError", str(e))
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("policy", POLICIES)
+def test_oracle_single_key_api_matches_reference(reference_pkg, mode, policy):
+    cap, dim = 128 * 8, 2
+    ref = reference_pkg.CacheTable(reference_pkg.TableConfig(capacity=cap, value_dim=dim, mode=mode,
+                                                             score_policy=policy, fast_tier_budget=5))
+    ora = OracleTable(cap, dim, mode, policy, 5)
+    kinds = set()
+    for j, op in enumerate(single_key_script(3, cap, dim, mode, policy)):
+        a = apply_single(ref, op, True)
+        b = apply_single(ora, op, False)
+        assert a == b, (j, op[0], a, b)
+        if op[0].startswith("upsert") and a[0] != "ValueError":
+            kinds.add(a[0])
+    st = ref_state(ref)
+    assert st["keys"].tobytes() == ora.keys.tobytes()
+    assert st["scores"].tobytes() == ora.scores.tobytes()
+    assert st["values"].tobytes() == ora.values.tobytes()
+    assert int(st["size"]) == ora.size() and int(st["clock"]) == ora.clock
+    assert ref.counters.as_dict() == ora.counters
+    assert ref.first_eviction_lambda == ora.first_eviction_lambda
+    assert {0, 1}.issubset(kinds) and (3 in kinds or 2 in kinds)
