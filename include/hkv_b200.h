@@ -67,6 +67,11 @@ typedef struct {
     int32_t admit_ties_unified;/* dual mode: admit score == min (table.py:1112-1115) */
     int32_t overflow_in_hbm;   /* 0 = overflow arena in mapped pinned host memory (tiering), 1 = HBM */
     int32_t device;            /* CUDA device ordinal */
+    int32_t workers;           /* 1: serial batch-order upserts (bit-exact with the reference's
+                                  workers=1 engine); > 1: concurrent LOCKED-sentinel slot-CAS
+                                  upserts, the reference's threaded engine (table.py:1185-1241):
+                                  serializable, policy invariants hold, order under contention
+                                  unspecified */
 } hkv_config;
 
 /* TxnCounters (metrics.py:14-20), in this order. */

@@ -26,6 +26,7 @@ class HkvConfig(C.Structure):
         ("admit_ties_unified", C.c_int32),
         ("overflow_in_hbm", C.c_int32),
         ("device", C.c_int32),
+        ("workers", C.c_int32),
     ]
 
 

@@ -23,7 +23,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompil
 
 # per-file extra flags: the dual-mode dataflow hands buckets between SMs
 # through acquire/release turn counters, so its global loads bypass L1
-EXTRA = {"hkv_dual.cu": ["-Xptxas", "-dlcm=cg"]}
+EXTRA = {"hkv_dual.cu": ["-Xptxas", "-dlcm=cg"], "hkv_cas.cu": ["-Xptxas", "-dlcm=cg"]}
 # experiments: extra nvcc flags for every file (e.g. HKV_NVCC_EXTRA="-DHKV_TPS_MINB=3")
 FLAGS += os.environ.get("HKV_NVCC_EXTRA", "").split()
 

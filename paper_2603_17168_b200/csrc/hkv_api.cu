@@ -184,6 +184,7 @@ struct hkv_table {
   float* vover_host = nullptr;  // pinned host allocation (mapped), if used
   TableScalars* sc = nullptr;
   unsigned* role_word = nullptr;  // device mirror of the gate's group (never snapshotted)
+  unsigned* locks = nullptr;      // CAS engine bucket locks (workers > 1)
   OneResult* one = nullptr;       // single-key API: result + value row staging (lazy)
   float* one_val = nullptr;
   hkv_gate* gate = nullptr;
@@ -254,6 +255,7 @@ void free_table(hkv_table* t) {
   DeviceGuard g(t->cfg.device);
   if (t->gate) gate_delete(t->gate);
   if (t->one) cudaFree(t->one);
+  if (t->locks) cudaFree(t->locks);
   if (t->one_val) cudaFree(t->one_val);
   void* dptrs[] = {t->keys, t->digests, t->scores, t->bits, t->smin, t->svalid, t->vfast, t->sc, t->role_word, t->lead,
                    t->snap_keys, t->snap_digests, t->snap_scores, t->snap_bits, t->snap_smin, t->snap_svalid,
@@ -332,6 +334,7 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
   if (c.mode != HKV_MODE_SINGLE && c.mode != HKV_MODE_DUAL) return fail(HKV_EINVAL, "unknown mode");
   if (c.score_policy < HKV_LRU || c.score_policy > HKV_CUSTOMIZED) return fail(HKV_EINVAL, "unknown policy");
   if (c.value_dim > (1 << 20)) return fail(HKV_EINVAL, "value_dim too large");
+  if (c.workers < 1) return fail(HKV_EINVAL, "workers must be >= 1");
 
   DeviceGuard g(c.device);
   hkv_table* t = new hkv_table();
@@ -368,6 +371,11 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
       free_table(t);
       return fail(HKV_ENOMEM, std::string("overflow arena allocation failed: ") + cudaGetErrorString(e));
     }
+  }
+  if (c.workers > 1 && ((e = cudaMalloc((void**)&t->locks, (size_t)bc * 4)) ||
+                         (e = cudaMemset(t->locks, 0, (size_t)bc * 4)))) {
+    free_table(t);
+    return fail(HKV_ENOMEM, "bucket lock allocation failed");
   }
   if (c.mode == HKV_MODE_DUAL && (e = cudaMalloc((void**)&t->lead, (size_t)bc * 8))) {
     free_table(t);
@@ -412,6 +420,8 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
   d.fel_set = &t->sc->fel_set;
   d.fel = &t->sc->fel;
   d.role_word = t->role_word;
+  d.cas = c.workers > 1;
+  d.locks = t->locks;
   t->gate = gate_new_device(c.device, t->role_word);
   *out = t;
   return HKV_OK;

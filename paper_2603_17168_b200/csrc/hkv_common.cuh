@@ -63,6 +63,8 @@ struct TableDev {
   int* fel_set;
   double* fel;
   const unsigned* role_word;     // device mirror of the role gate: (group << 2) | (role + 1)
+  int cas;                       // workers > 1: concurrent slot-CAS upserts (hkv_cas.cu)
+  unsigned* locks;               // [B] bucket locks of the CAS engine (structural changes)
 };
 
 // Mutation kernels refuse to run while the gate's device mirror names a

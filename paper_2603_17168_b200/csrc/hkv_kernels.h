@@ -131,5 +131,8 @@ void ws_free_dual(Workspace& ws);
 cudaError_t run_dual(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, Workspace& ws,
                      unsigned long long* turn, unsigned long long tag, int vec, cudaStream_t s, int num_sms);
 void ws_free(Workspace& ws);
+// concurrent upserts (workers > 1): LOCKED-sentinel slot CAS + bucket locks
+cudaError_t run_cas(const TableDev& t, OpArgs a, int64_t n, unsigned* locks, int vec, cudaStream_t s,
+                    int num_sms);
 
 }  // namespace hkv

@@ -1380,8 +1380,11 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
   // (dual mode: the dataflow) reads them.
   cudaError_t e;
   const bool collect = a.collect != 0;
-  if ((e = ws_reserve(ws, n, t.dim, collect ? (t.dual ? 2 : 1) : 0, t.dual != 0))) return e;
-  if (t.dual && (e = ws_reserve_dual(ws, n, log2_buckets))) return e;
+  // in-place engines move value rows inside the op (dual dataflow, CAS engine)
+  const bool cas = t.cas && a.op != kOpErase;
+  const bool inplace = t.dual || cas;
+  if ((e = ws_reserve(ws, n, t.dim, collect ? (inplace ? 2 : 1) : 0, t.dual != 0))) return e;
+  if (t.dual && !cas && (e = ws_reserve_dual(ws, n, log2_buckets))) return e;
   a.sc = ws.sc;
   a.ek = ws.ek;
   a.es = ws.es;
@@ -1394,7 +1397,13 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
     ktimer_end("prep", s, 2);
     g_launches++;
     const int vec = vec_of(t.dim, a.values, t.vfast, t.vover, collect ? ws.ev : nullptr);
-    if (!t.dual) {
+    if (cas) {
+      if (values_ready && (e = cudaStreamWaitEvent(s, values_ready, 0))) return e;
+      values_ready = nullptr;
+      ktimer_begin("cas_upsert", s);
+      if ((e = run_cas(t, a, n, t.locks, vec, s, num_sms))) return e;
+      ktimer_end("cas_upsert", s);
+    } else if (!t.dual) {
       ktimer_begin("sort", s, 2);
       if ((e = sort_segments(ws, n, log2_buckets, s))) return e;
       ktimer_end("sort", s, 2);
@@ -1476,7 +1485,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
     g_launches += 2;
   }
   const int64_t vblocks = tile_blocks(n, num_sms);
-  if (!t.dual && n > 0 && a.op != kOpErase) {
+  if (!inplace && n > 0 && a.op != kOpErase) {
     if (values_ready && (e = cudaStreamWaitEvent(s, values_ready, 0))) return e;
     // value reads (provenance-resolved) strictly before value writes
     const int vr = vec_of(t.dim, a.values, t.vfast, t.vover, collect ? ev_out : nullptr);
@@ -1508,7 +1517,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
     g_launches++;
   }
   if (collect) {
-    if (n > 0 && t.dual) {
+    if (n > 0 && inplace) {
       const int vec = vec_of(t.dim, ev_out, ws.ev, nullptr, nullptr);
       if (vec == 4)
         k_evict_gather<4><<<(unsigned)vblocks, 256, 0, s>>>(ws.sc, ws.aux, nev, ws.ek, ws.es, ws.ev, ek_out, es_out,

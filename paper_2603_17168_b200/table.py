@@ -99,8 +99,11 @@ _POLICY_CODE = {PolicyId.kLru: 0, PolicyId.kLfu: 1, PolicyId.kEpochLru: 2, Polic
 @dataclass
 class TableConfig:
     """table.py:94-131; `allocator` is accepted only as None (values live in
-    HBM or mapped pinned host memory), `workers` is accepted and ignored
-    (results are always the serial-equivalent ones)."""
+    HBM or mapped pinned host memory).  `workers` picks the upsert engine as
+    in the reference: 1 = serial batch-order semantics (bit-exact with the
+    reference's default engine), > 1 = concurrent slot-CAS upserts (the
+    reference's threaded engine, table.py:1185-1241: serializable, order under
+    contention unspecified)."""
 
     capacity: int
     value_dim: int
@@ -163,7 +166,7 @@ class CacheTable:
             capacity=config.capacity, value_dim=config.value_dim, mode=0 if config.mode is Mode.single else 1,
             score_policy=_POLICY_CODE[config.score_policy], fast_tier_budget=config.fast_tier_budget,
             digest_filter=int(config.digest_filter), admit_ties_unified=int(config.admit_ties_unified),
-            overflow_in_hbm=int(config.overflow_in_hbm), device=dev)
+            overflow_in_hbm=int(config.overflow_in_hbm), device=dev, workers=int(config.workers))
         h = C.c_void_p()
         _lib.check(self._lib.hkv_create(C.byref(cfg), C.byref(h)))
         self._h = h
