@@ -5,10 +5,14 @@
 // that engine it is serializable but not serial-in-batch-order under
 // contention, so tests check the policy invariants.
 //
-// One 8-lane tile per op (lane r: slots 16r..16r+15 of a bucket):
-//   probe      lock-free: digest slice + occupancy slice per lane, candidate
-//              keys in slot order.  A candidate whose key is LOCKED may be
-//              this very key mid-update: the probe retries until it resolves.
+// One THREAD per op (HKV's TLPv1 shape): an op's chain is a
+// handful of dependent round trips (probe, lock, claim, publish), so what
+// pays is the number of ops in flight -- 32 per warp instead of 4 with an
+// 8-lane tile (measured: 1M hits 0.51 -> see DESIGN.md).
+//   probe      lock-free: the 128-B digest line and the 16-B occupancy word,
+//              candidate keys in slot order.  A candidate whose key is LOCKED
+//              may be this very key mid-update: the probe retries until it
+//              resolves.
 //   hit        CAS key -> LOCKED on the matched slot (a lost race retries the
 //              whole op), refresh the score, write (or, find_or_insert, read)
 //              the value row, release-store the key back (_scalar_hit,
@@ -33,283 +37,367 @@ namespace {
 
 constexpr int kBusy = -2;
 
+__device__ __forceinline__ void fence_rel() {
+#ifndef HKV_CAS_NOFENCE
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned cas_acquire_u32(unsigned* p, unsigned cmp, unsigned val) {
+  unsigned old;
+  asm volatile("atom.acquire.gpu.global.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "l"(p), "r"(cmp), "r"(val) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ uint64_t ld_key(const TableDev& t, uint64_t row) {
+#ifdef HKV_CAS_KEYLDCG
+  return __ldcg(t.keys + row);
+#else
   return *(volatile const uint64_t*)(t.keys + row);
+#endif
 }
-
-// Lock-free probe of bucket b: slot of `key`, -1 (absent), or kBusy (a
-// digest candidate is LOCKED: an op holds it mid-update).
-__device__ __forceinline__ int probe_cas(const TableDev& t, const Tile8& tile, uint64_t b, uint64_t key, uint32_t d,
-                                         ctr_t& ncmp) {
-  const int r = tile.thread_rank();
-  const uint4 dw = __ldcg(reinterpret_cast<const uint4*>(t.digests + b * kSlots) + r);
-  const uint32_t occ = __ldcg(reinterpret_cast<const unsigned short*>(t.bits + b * 4) + r);
-  uint32_t cand = (t.digest_filter ? match16(dw, d) : 0xFFFFu) & occ;
-  int hit = -1, cmp = 0, cmp_all = 0;
-  bool busy = false;
-  while (cand) {
-    const int j = __ffs(cand) - 1;
-    cand &= cand - 1;
-    const uint64_t k = ld_key(t, b * kSlots + r * kSPL + j);
-    if (k == kLockedKey) {
-      busy = true;
-      continue;
-    }
-    if (k == kEmptyKey) continue;
-    cmp_all++;
-    if (k == key) {
-      hit = r * kSPL + j;
-      cmp = cmp_all;
-      break;
-    }
-  }
-  const uint32_t hm = tile.ballot(hit >= 0);
-  int contrib = cmp_all;
-  int slot = -1;
-  if (hm) {
-    const int hl = __ffs(hm) - 1;
-    slot = tile.shfl(hit, hl);
-    contrib = r < hl ? cmp_all : (r == hl ? cmp : 0);
-  } else if (tile.any(busy)) {
-    slot = kBusy;
-  }
-  ncmp += tile.sum((unsigned)contrib);
-  return slot;
-}
-
-__device__ __forceinline__ void lock_bucket(unsigned* locks, uint64_t b) {
-  while (atomicCAS(locks + b, 0u, 1u) != 0u) __nanosleep(64);
-  __threadfence();
-}
-__device__ __forceinline__ void unlock_bucket(unsigned* locks, uint64_t b) {
-  __threadfence();
-  atomicExch(locks + b, 0u);
-}
-
-// slot CAS by the owning lane, result broadcast to the tile
-__device__ __forceinline__ bool cas_slot(const TableDev& t, const Tile8& tile, uint64_t row, int slot,
-                                         uint64_t expect) {
-  int ok = 0;
-  if (tile.thread_rank() == slot / kSPL)
-    ok = atomicCAS((unsigned long long*)(t.keys + row), (unsigned long long)expect,
+__device__ __forceinline__ bool cas_key(const TableDev& t, uint64_t row, uint64_t expect) {
+  return atomicCAS((unsigned long long*)(t.keys + row), (unsigned long long)expect,
                    (unsigned long long)kLockedKey) == (unsigned long long)expect;
-  return tile.shfl(ok, slot / kSPL) != 0;
 }
 
-// publish: digest, score (and the value row, written by the caller), then
-// the key with release semantics
-__device__ __forceinline__ void publish_key(const TableDev& t, const Tile8& tile, uint64_t row, int slot,
-                                            uint64_t key) {
-  __threadfence();
-  tile.sync();
-  if (tile.thread_rank() == slot / kSPL) *(volatile uint64_t*)(t.keys + row) = key;
-}
-
-template <int VEC>
-__device__ __forceinline__ void copy_in(float* dst, const float* vin, int dim, int r) {
-  copy_row<kG, VEC>(dst, vin, dim, r);
-}
-
-// the hit path on (hb, slot) once its key is LOCKED by this tile
-template <int VEC>
-__device__ __forceinline__ uint8_t do_hit(const TableDev& t, const OpArgs& a, const Tile8& tile, uint32_t i,
-                                          uint64_t hb, int slot, uint64_t key, uint64_t tick, uint64_t cs,
-                                          ctr_t* ctr) {
-  const int r = tile.thread_rank();
-  const uint64_t row = hb * kSlots + slot;
-  if (r == slot / kSPL) {
-    const uint64_t old = hit_needs_old(t.policy) ? *(volatile uint64_t*)(t.scores + row) : 0;
-    t.scores[row] = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
-    summ_invalidate(t, hb, slot);
-  }
-  float* vr = value_row(t, row);
-  float* vin = a.values + (uint64_t)i * t.dim;
-  uint8_t outcome;
-  if (a.op == kOpFindOrInsert) {
-    copy_row<kG, VEC>(vin, vr, t.dim, r);
-    outcome = kFound;
-  } else {
-    copy_in<VEC>(vr, vin, t.dim, r);
-    outcome = kUpdated;
-  }
-  ctr[row < t.fast_rows ? kVFast : kVOver]++;
-  publish_key(t, tile, row, slot, key);
-  return outcome;
-}
-
-template <int VEC>
-__device__ void process_cas(const TableDev& t, const OpArgs& a, unsigned* locks, const Tile8& tile, uint32_t i,
-                            uint64_t clock0, bool fel_open, ctr_t* ctr, int& size_delta) {
-  const int r = tile.thread_rank();
-  const int dim = t.dim;
-  const uint64_t key = a.keys[i];
-  const uint64_t h = fmix64(key);
-  const uint32_t d = digest_of(h);
-  const uint64_t b1 = h & t.mask;
-  const uint64_t b2 = t.dual ? second_hash(h) & t.mask : b1;
-  const uint64_t tick = a.ticks ? a.ticks[i] : clock0 + (uint64_t)i + 1;
-  const uint64_t cs = a.scores ? a.scores[i] : 0;
-  float* vin = a.values + (uint64_t)i * dim;
-  uint8_t outcome = kRejected;
+// Bucket locks are sequence locks: even = free, odd = held; every holder
+// advances the word by 2 (lock +1, unlock +1).  An op reads the word before
+// its lock-free probe; if it can take the lock from that same even value, no
+// structural change touched the bucket in between and the probe stands (no
+// second probe under the lock).
+__device__ __forceinline__ unsigned lock_bucket(unsigned* locks, uint64_t b, unsigned seen, bool& unchanged) {
+  unchanged = (seen & 1u) == 0 && cas_acquire_u32(locks + b, seen, seen + 1) == seen;
+  if (unchanged) return seen;
   for (;;) {
-    // ---- lock-free probe + hit ----
-    uint64_t hb = b1;
-    int slot = probe_cas(t, tile, b1, key, d, ctr[kCompares]);
-    ctr[kLoads]++;
-    if (slot == -1 && t.dual) {
-      hb = b2;
-      slot = probe_cas(t, tile, b2, key, d, ctr[kCompares]);
-      ctr[kLoads]++;
-    }
-    if (slot == kBusy) {
-      ctr[kRetries]++;
-      __nanosleep(32);
-      continue;
-    }
-    if (slot >= 0) {
-      if (!cas_slot(t, tile, hb * kSlots + slot, slot, key)) {
-        ctr[kRetries]++;  // lost the slot race; the key may have moved
+    const unsigned v = ld_acquire_u32(locks + b);
+    if ((v & 1u) == 0 && cas_acquire_u32(locks + b, v, v + 1) == v) return v;
+    __nanosleep(64);
+  }
+}
+__device__ __forceinline__ void unlock_bucket(unsigned* locks, uint64_t b, unsigned from) {
+  st_release_u32(locks + b, from + 2);
+}
+
+// Lock-free probe of bucket b by one thread: slot of `key`, -1 (absent), or
+// kBusy (a digest candidate is LOCKED: an op holds it mid-update).  Compares
+// counted as table.py:243-268 (candidates in slot order, up to the match).
+__device__ __forceinline__ int probe_cas(const TableDev& t, uint64_t b, uint64_t key, uint32_t d, ctr_t& ncmp) {
+  const uint4* dp = reinterpret_cast<const uint4*>(t.digests + b * kSlots);
+  const uint4 ow = __ldcg(reinterpret_cast<const uint4*>(t.bits + b * 4));
+  const uint32_t occ[4] = {ow.x, ow.y, ow.z, ow.w};
+  uint32_t c[4];
+  {
+    uint4 w[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) w[k] = __ldcg(dp + k);
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+      c[q] = (t.digest_filter ? (match16(w[2 * q], d) | (match16(w[2 * q + 1], d) << 16)) : ~0u) & occ[q];
+  }
+  bool busy = false;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    uint32_t m = c[q];
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const uint64_t k = ld_key(t, b * kSlots + 32 * q + j);
+      if (k == kLockedKey) {
+        busy = true;
         continue;
       }
-      outcome = do_hit<VEC>(t, a, tile, i, hb, slot, key, tick, cs, ctr);
-      break;
+      if (k == kEmptyKey) continue;
+      ncmp++;
+      if (k == key) return 32 * q + j;
     }
-    // ---- miss: structural change under the bucket lock(s) ----
-    const uint64_t lo = b1 < b2 ? b1 : b2, hi = b1 < b2 ? b2 : b1;
-    if (r == 0) {
-      lock_bucket(locks, lo);
-      if (hi != lo) lock_bucket(locks, hi);
-    }
-    tile.sync();
-    // probe again under the lock: a same-key insert may have won meanwhile;
-    // an in-flight hit (no lock) is waited out
-    hb = b1;
-    do {
-      slot = probe_cas(t, tile, b1, key, d, ctr[kCompares]);
-      ctr[kLoads]++;
-      hb = b1;
-      if (slot == -1 && t.dual) {
-        slot = probe_cas(t, tile, b2, key, d, ctr[kCompares]);
-        ctr[kLoads]++;
-        hb = b2;
-      }
-    } while (slot == kBusy);
-    if (slot >= 0) {
-      while (!cas_slot(t, tile, hb * kSlots + slot, slot, key)) ctr[kRetries]++;
-      outcome = do_hit<VEC>(t, a, tile, i, hb, slot, key, tick, cs, ctr);
-    } else {
-      const uint64_t s_in = insert_score(t.policy, a.epoch, tick, cs);
-      const uint32_t occ1 = __ldcg(reinterpret_cast<const unsigned short*>(t.bits + b1 * 4) + r);
-      const uint32_t occ2 =
-          t.dual ? __ldcg(reinterpret_cast<const unsigned short*>(t.bits + b2 * 4) + r) : occ1;
-      const int o1 = tile_sum<kG>(tile, __popc(occ1));
-      const int o2 = t.dual ? tile_sum<kG>(tile, __popc(occ2)) : kSlots;
-      if (o1 < kSlots || (t.dual && o2 < kSlots)) {
-        // free insert: single -> b1; dual D1 -> the less-occupied bucket
-        const uint64_t tb = (!t.dual || o1 <= o2) ? b1 : b2;
-        const uint32_t occ = tb == b1 ? occ1 : occ2;
-        const uint32_t hasfree = tile.ballot(occ != 0xFFFFu);
-        const int fl = __ffs(hasfree) - 1;
-        int s = 0;
-        if (r == fl) s = r * kSPL + __ffs(~occ & 0xFFFFu) - 1;
-        s = tile.shfl(s, fl);
-        const uint64_t row = tb * kSlots + s;
-        // claim EMPTY -> LOCKED (table.py:678-693); under the bucket lock
-        // nothing else can claim it
-        while (!cas_slot(t, tile, row, s, kEmptyKey)) ctr[kRetries]++;
-        if (r == fl) {
-          store_occ(t, tb, r, occ | (1u << (s % kSPL)));
-          t.digests[row] = (uint8_t)d;
-          t.scores[row] = s_in;
-        }
-        if (r == 0) atomicAnd(t.svalid + tb, 0u);
-        copy_in<VEC>(value_row(t, row), vin, dim, r);
-        ctr[row < t.fast_rows ? kVFast : kVOver]++;
-        publish_key(t, tile, row, s, key);
-        size_delta++;
-        outcome = kInserted;
-      } else {
-        for (;;) {
-          uint64_t tb = b1, minv;
-          int m;
-          bool admit;
-          if (!t.dual) {
-            bucket_min(t, tile, b1, minv, m);
-            ctr[kScans]++;
-            admit = s_in >= minv;  // the single-bucket path admits ties
-          } else {
-            uint64_t n1, n2;
-            int m1, m2;
-            bucket_min(t, tile, b1, n1, m1);
-            bucket_min(t, tile, b2, n2, m2);
-            ctr[kScans] += 2;
-            const bool use2 = n2 < n1;  // D2: the bucket with the lower minimum
-            tb = use2 ? b2 : b1;
-            m = use2 ? m2 : m1;
-            minv = use2 ? n2 : n1;
-            admit = t.admit_unified ? s_in >= minv : s_in > minv;
-          }
-          if (!admit) {
-            outcome = kRejected;
-            break;
-          }
-          const uint64_t row = tb * kSlots + m;
-          uint64_t old = 0;
-          if (r == m / kSPL) old = ld_key(t, row);
-          old = tile.shfl(old, m / kSPL);
-          if (old == kLockedKey || !cas_slot(t, tile, row, m, old)) {
-            ctr[kRetries]++;  // a hit holds the minimum slot: wait it out, rescan
-            __nanosleep(32);
-            continue;
-          }
-          float* vr = value_row(t, row);
-          if (a.collect) {
-            if (r == 0) {
-              a.ek[i] = old;
-              a.es[i] = minv;
-            }
-            copy_row<kG, VEC>(a.ev + (uint64_t)i * dim, vr, dim, r);
-            ctr[row < t.fast_rows ? kVFast : kVOver]++;
-          }
-          if (r == m / kSPL) {
-            t.digests[row] = (uint8_t)d;
-            t.scores[row] = s_in;
-          }
-          if (r == 0) atomicAnd(t.svalid + tb, 0u);
-          copy_in<VEC>(vr, vin, dim, r);
-          ctr[row < t.fast_rows ? kVFast : kVOver]++;
-          publish_key(t, tile, row, m, key);
-          if (fel_open && r == 0) atomicMin(&a.sc->first_ev, i);
-          outcome = kEvicted;
-          break;
-        }
-      }
-    }
-    tile.sync();
-    if (r == 0) {
-      if (hi != lo) unlock_bucket(locks, hi);
-      unlock_bucket(locks, lo);
-    }
-    break;
   }
-  if (r == 0) a.outcomes[i] = outcome;
+  return busy ? kBusy : -1;
 }
 
+// ---------------------------------------------------------------------------
+// Warp-synchronous rounds.  A warp owns 32 ops (one per lane).  Each round,
+// every unfinished op makes one NON-BLOCKING attempt: probe; hit -> CAS the
+// slot; miss -> try the bucket lock(s), claim a free slot or (after a
+// warp-cooperative score scan) CAS the victim, write the slot's metadata and
+// drop the bucket lock(s) -- the slot itself stays LOCKED.  Then the warp
+// moves every claimed op's value row with coalesced copies, fences, and
+// publishes the keys.  An op that met a LOCKED candidate, a held lock or a
+// lost CAS simply tries again next round; nothing is ever waited on while a
+// lock or a LOCKED slot is held, so the rounds cannot deadlock.
+// ---------------------------------------------------------------------------
+enum : int { kTaskNone = 0, kTaskHit = 1, kTaskRead = 2, kTaskInsert = 3, kTaskEvict = 4 };
+constexpr unsigned kFullMask = 0xFFFFFFFFu;
+
+// first-index minimum (np.argmin, table.py:1080) of bucket b's 128 scores,
+// read by the whole warp (lane j: slots 4j..4j+3, 1 KB coalesced)
+__device__ __forceinline__ void warp_min(const TableDev& t, uint64_t b, int lane, uint64_t& minv, int& mslot) {
+  const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(t.scores + b * kSlots + 4 * lane);
+  const ulonglong2 x = __ldcg(sp), y = __ldcg(sp + 1);
+  uint64_t v = x.x;
+  int m = 4 * lane;
+  if (x.y < v) { v = x.y; m = 4 * lane + 1; }
+  if (y.x < v) { v = y.x; m = 4 * lane + 2; }
+  if (y.y < v) { v = y.y; m = 4 * lane + 3; }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t ov = __shfl_xor_sync(kFullMask, v, o);
+    const int om = __shfl_xor_sync(kFullMask, m, o);
+    if (ov < v || (ov == v && om < m)) { v = ov; m = om; }
+  }
+  minv = v;
+  mslot = m;
+}
+
+// the warp copies the rows of every lane in `mask`: dst/src per lane
 template <int VEC>
-__global__ void __launch_bounds__(256) k_cas_upsert(TableDev t, OpArgs a, unsigned* locks, int64_t n) {
+__device__ __forceinline__ void warp_copy_rows(unsigned mask, float* dst, const float* src, int dim, int lane) {
+  using V = typename std::conditional<VEC == 4, uint4, typename std::conditional<VEC == 2, float2, float>::type>::type;
+  const int nv = dim / VEC;
+  if (nv <= 16) {
+    // two rows per step, a half warp each
+    const int half = lane >> 4, hl = lane & 15;
+    while (mask) {
+      const int l0 = __ffs(mask) - 1;
+      mask &= mask - 1;
+      int l1 = -1;
+      if (mask) {
+        l1 = __ffs(mask) - 1;
+        mask &= mask - 1;
+      }
+      const int src_l = half ? l1 : l0;
+      float* d = (float*)__shfl_sync(kFullMask, (unsigned long long)dst, src_l < 0 ? l0 : src_l);
+      const float* sp = (const float*)__shfl_sync(kFullMask, (unsigned long long)src, src_l < 0 ? l0 : src_l);
+      if (src_l >= 0 && hl < nv) reinterpret_cast<V*>(d)[hl] = reinterpret_cast<const V*>(sp)[hl];
+    }
+  } else {
+    while (mask) {
+      const int l = __ffs(mask) - 1;
+      mask &= mask - 1;
+      float* d = (float*)__shfl_sync(kFullMask, (unsigned long long)dst, l);
+      const float* sp = (const float*)__shfl_sync(kFullMask, (unsigned long long)src, l);
+      copy_row<32, VEC, 2>(d, sp, dim, lane);
+    }
+  }
+}
+
+#ifndef HKV_CAS_MINB
+#define HKV_CAS_MINB 2
+#endif
+template <int VEC>
+__global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, OpArgs a, unsigned* locks, int64_t n) {
   if (a.sc->err) return;
-  const Tile8 tile;
+  const int lane = threadIdx.x & 31;
   const uint64_t clock0 = *t.clock;
   const bool fel_open = !*t.fel_set;
+  const int dim = t.dim;
   ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
   int sd = 0;
-  const int64_t tiles = (int64_t)gridDim.x * (blockDim.x / kG);
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x / kG) + threadIdx.x / kG; i < n; i += tiles)
-    process_cas<VEC>(t, a, locks, tile, (uint32_t)i, clock0, fel_open, ctr, sd);
-  if (tile.thread_rank() != 0) {
-#pragma unroll
-    for (int k = 0; k < 6; k++) ctr[k] = 0;
-    sd = 0;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t base = ((int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32) * 32; base < n;
+       base += nwarps * 32) {
+    const int64_t i = base + lane;
+    bool done = i >= n;
+    uint64_t key = 0, b1 = 0, b2 = 0, tick = 0, cs = 0;
+    uint32_t d = 0;
+    if (!done) {
+      key = a.keys[i];
+      const uint64_t h = fmix64(key);
+      d = digest_of(h);
+      b1 = h & t.mask;
+      b2 = t.dual ? second_hash(h) & t.mask : b1;
+      tick = a.ticks ? a.ticks[i] : clock0 + (uint64_t)i + 1;
+      cs = a.scores ? a.scores[i] : 0;
+    }
+    const uint64_t lo = b1 < b2 ? b1 : b2, hi = b1 < b2 ? b2 : b1;
+    float* vin = done ? nullptr : a.values + (uint64_t)i * dim;
+    uint8_t outcome = kRejected;
+    unsigned idle_rounds = 0;
+    while (__any_sync(kFullMask, !done)) {
+      int task = kTaskNone;
+      bool need_scan = false, locked = false, retry = false;
+      unsigned from_lo = 0, from_hi = 0;
+      uint64_t row = 0, tb = b1, s_in = 0, victim = 0, minv = 0;
+      int slot = -1;
+      if (!done) {
+        const unsigned seen_lo = ld_acquire_u32(locks + lo);
+        const unsigned seen_hi = hi != lo ? ld_acquire_u32(locks + hi) : 0u;
+        uint64_t hb = b1;
+        slot = probe_cas(t, b1, key, d, ctr[kCompares]);
+        ctr[kLoads]++;
+        if (slot == -1 && t.dual) {
+          hb = b2;
+          slot = probe_cas(t, b2, key, d, ctr[kCompares]);
+          ctr[kLoads]++;
+        }
+        if (slot == -1) {
+          // try the bucket lock(s) once; from the value seen before the
+          // probe, the probe stands, else probe again under the lock
+          const bool same_lo = (seen_lo & 1u) == 0 && cas_acquire_u32(locks + lo, seen_lo, seen_lo + 1) == seen_lo;
+          if (same_lo) {
+            from_lo = seen_lo;
+          } else {
+            const unsigned v = ld_acquire_u32(locks + lo);
+            if ((v & 1u) == 0 && cas_acquire_u32(locks + lo, v, v + 1) == v) from_lo = v | 0x80000000u;
+            else retry = true;
+          }
+          bool same_hi = true;
+          if (!retry && hi != lo) {
+            same_hi = (seen_hi & 1u) == 0 && cas_acquire_u32(locks + hi, seen_hi, seen_hi + 1) == seen_hi;
+            if (same_hi) {
+              from_hi = seen_hi;
+            } else {
+              const unsigned v = ld_acquire_u32(locks + hi);
+              if ((v & 1u) == 0 && cas_acquire_u32(locks + hi, v, v + 1) == v) {
+                from_hi = v;
+              } else {
+                unlock_bucket(locks, lo, from_lo & 0x7FFFFFFFu);
+                retry = true;
+              }
+            }
+          }
+          if (!retry) {
+            locked = true;
+            from_lo &= 0x7FFFFFFFu;
+            if (!(same_lo && same_hi)) {
+              hb = b1;
+              slot = probe_cas(t, b1, key, d, ctr[kCompares]);
+              ctr[kLoads]++;
+              if (slot == -1 && t.dual) {
+                hb = b2;
+                slot = probe_cas(t, b2, key, d, ctr[kCompares]);
+                ctr[kLoads]++;
+              }
+            }
+          }
+        }
+        if (retry || slot == kBusy) {
+          retry = true;
+        } else if (slot >= 0) {
+          // hit (table.py:749-772): hold the slot
+          row = hb * kSlots + slot;
+          if (cas_key(t, row, key)) {
+            const uint64_t old = hit_needs_old(t.policy) ? __ldcg(t.scores + row) : 0;
+            t.scores[row] = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
+            summ_invalidate(t, hb, slot);
+            task = a.op == kOpFindOrInsert ? kTaskRead : kTaskHit;
+          } else {
+            retry = true;
+          }
+        } else {
+          s_in = insert_score(t.policy, a.epoch, tick, cs);
+          const uint4 w1 = __ldcg(reinterpret_cast<const uint4*>(t.bits + b1 * 4));
+          const uint4 w2 = t.dual ? __ldcg(reinterpret_cast<const uint4*>(t.bits + b2 * 4)) : w1;
+          const int o1 = __popc(w1.x) + __popc(w1.y) + __popc(w1.z) + __popc(w1.w);
+          const int o2 = t.dual ? __popc(w2.x) + __popc(w2.y) + __popc(w2.z) + __popc(w2.w) : kSlots;
+          if (o1 < kSlots || o2 < kSlots) {
+            // free insert (table.py:678-693, 1165-1181): single -> b1, dual D1
+            const bool first = !t.dual || o1 <= o2;
+            tb = first ? b1 : b2;
+            const uint4 w = first ? w1 : w2;
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+            int q = 0;
+            while (ws[q] == 0xFFFFFFFFu) q++;
+            slot = 32 * q + __ffs(~ws[q]) - 1;  // the lowest EMPTY slot
+            row = tb * kSlots + slot;
+            // EMPTY -> LOCKED; under the bucket lock nothing else claims it
+            atomicCAS((unsigned long long*)(t.keys + row), (unsigned long long)kEmptyKey,
+                      (unsigned long long)kLockedKey);
+            t.bits[tb * 4 + q] = ws[q] | (1u << (slot & 31));
+            t.digests[row] = (uint8_t)d;
+            t.scores[row] = s_in;
+            t.svalid[tb] = 0u;
+            task = kTaskInsert;
+          } else {
+            need_scan = true;
+          }
+        }
+      }
+      // ---- warp-cooperative score scans for full-bucket decisions ----
+      unsigned sm = __ballot_sync(kFullMask, need_scan);
+      while (sm) {
+        const int l = __ffs(sm) - 1;
+        sm &= sm - 1;
+        const uint64_t lb1 = __shfl_sync(kFullMask, b1, l), lb2 = __shfl_sync(kFullMask, b2, l);
+        uint64_t n1, n2 = kMaxScore;
+        int m1, m2 = 0;
+        warp_min(t, lb1, lane, n1, m1);
+        if (t.dual) warp_min(t, lb2, lane, n2, m2);
+        if (lane == l) {
+          if (!t.dual) {
+            ctr[kScans]++;
+            minv = n1, slot = m1, tb = b1;
+          } else {
+            ctr[kScans] += 2;
+            const bool use2 = n2 < n1;  // D2: the bucket with the lower minimum
+            minv = use2 ? n2 : n1, slot = use2 ? m2 : m1, tb = use2 ? b2 : b1;
+          }
+        }
+      }
+      if (need_scan) {
+        const bool admit = t.dual ? (t.admit_unified ? s_in >= minv : s_in > minv) : s_in >= minv;
+        if (!admit) {
+          outcome = kRejected;
+          done = true;
+        } else {
+          row = tb * kSlots + slot;
+          victim = ld_key(t, row);
+          if (victim == kLockedKey || !cas_key(t, row, victim)) {
+            retry = true;  // an op holds the minimum slot: rescan next round
+          } else {
+            if (a.collect) {
+              a.ek[i] = victim;
+              a.es[i] = minv;
+            }
+            t.digests[row] = (uint8_t)d;
+            t.scores[row] = s_in;
+            t.svalid[tb] = 0u;
+            task = kTaskEvict;
+          }
+        }
+      }
+      // structure is settled: drop the bucket locks (claimed slots stay LOCKED)
+      if (locked) {  // st.release: this thread's metadata writes before the unlock
+        if (hi != lo) unlock_bucket(locks, hi, from_hi);
+        unlock_bucket(locks, lo, from_lo);
+      }
+      if (retry) ctr[kRetries]++;
+      // ---- warp-cooperative value movement ----
+      float* vr = task != kTaskNone ? value_row(t, row) : nullptr;
+      const unsigned cap_mask = __ballot_sync(kFullMask, task == kTaskEvict && a.collect);
+      if (cap_mask) warp_copy_rows<VEC>(cap_mask, a.collect && task == kTaskEvict ? a.ev + (uint64_t)i * dim : nullptr,
+                                        vr, dim, lane);
+      const unsigned rd_mask = __ballot_sync(kFullMask, task == kTaskRead);
+      if (rd_mask) warp_copy_rows<VEC>(rd_mask, vin, vr, dim, lane);
+      const unsigned wr_mask = __ballot_sync(kFullMask, task == kTaskHit || task == kTaskInsert || task == kTaskEvict);
+      if (wr_mask) warp_copy_rows<VEC>(wr_mask, vr, vin, dim, lane);
+      if (task != kTaskNone) {
+        ctr[row < t.fast_rows ? kVFast : kVOver] += (task == kTaskEvict && a.collect) ? 2 : 1;
+        if (task == kTaskInsert) sd++;
+        if (task == kTaskEvict && fel_open) atomicMin(&a.sc->first_ev, (unsigned)i);
+        outcome = task == kTaskHit ? kUpdated : task == kTaskRead ? kFound : task == kTaskInsert ? kInserted : kEvicted;
+        done = true;
+      }
+      __syncwarp();
+      fence_rel();  // rows (every lane's stores) before the keys
+      __syncwarp();
+      if (task != kTaskNone) st_release_u64(t.keys + row, key);
+      if (!__any_sync(kFullMask, task != kTaskNone) && !__all_sync(kFullMask, done)) {
+        if (++idle_rounds > 2) __nanosleep(64);
+      } else {
+        idle_rounds = 0;
+      }
+    }
+    if (i < n) a.outcomes[i] = outcome;
   }
   flush_counters<256>(t.counters, ctr, 6);
   long long v = sd;
@@ -327,7 +415,7 @@ cudaError_t run_cas(const TableDev& t, OpArgs a, int64_t n, unsigned* locks, int
   if (e) return e;
   if (per_sm < 1) per_sm = 1;
   int64_t blocks = (int64_t)per_sm * num_sms;
-  const int64_t want = (n * kG + 255) / 256;
+  const int64_t want = (n + 255) / 256;
   if (blocks > want) blocks = want < 1 ? 1 : want;
   if (vec == 4) k_cas_upsert<4><<<(unsigned)blocks, 256, 0, s>>>(t, a, locks, n);
   else if (vec == 2) k_cas_upsert<2><<<(unsigned)blocks, 256, 0, s>>>(t, a, locks, n);

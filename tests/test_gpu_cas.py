@@ -173,7 +173,7 @@ def test_cas_contended_invariants(hkv, mode, policy):
     f, v = t.find(resident)
     assert f.all()
     vi = np.zeros((len(resident), dim), np.float32)
-    oi = t.find_or_insert(resident, vi)
+    oi = t.find_or_insert(resident, vi, np.zeros(len(resident), np.uint64) if custom else None)
     assert (oi == 4).all() and np.array_equal(vi, v)
 
 

@@ -252,6 +252,33 @@ def dual(reps, lg=27):
         torch.cuda.empty_cache()
 
 
+def cas(reps, lg=27):
+    """The concurrent slot-CAS engine (workers > 1, hkv_cas.cu) on the C2
+    shape: insert_or_assign / insert_and_evict of 1M fresh keys, single mode
+    at lambda 0.5 / 0.75 / 1 and dual mode at 0.5 / 1."""
+    cap, dim = 2**lg, 64
+    gen = torch.Generator(device="cuda").manual_seed(6)
+    for mode, lams in (("single", (0.5, 0.75, 1.0)), ("dual", (0.5, 1.0))):
+        for lam in lams:
+            t = hkv.CacheTable(hkv.TableConfig(capacity=cap, value_dim=dim, score_policy="kLru", mode=mode,
+                                               workers=8))
+            t.validate_keys = False
+            fill(t, lam, cap, dim)
+            t.snapshot()
+            vals = torch.randn((B, dim), device="cuda", generator=gen)
+            base = {"config": f"cas-{mode}", "capacity": cap, "dim": dim, "lambda": round(t.load_factor(), 4)}
+            fresh = [W.uniform_distinct_keys_torch(B, 0, stream_offset=2**44 + r * B) for r in range(reps + 1)]
+            ms, o = timed(lambda r: t.insert_or_assign(fresh[r], vals), reps, after=t.restore)
+            emit({**base, "op": "insert_or_assign_fresh", "ms": ms, "bkvs": B / ms / 1e6, "outcomes": outcome_mix(o)})
+            ms, o = timed(lambda r: t.insert_and_evict(fresh[r], vals)[0], reps, after=t.restore)
+            emit({**base, "op": "insert_and_evict_fresh", "ms": ms, "bkvs": B / ms / 1e6, "outcomes": outcome_mix(o)})
+            q = resident_sample(t, B, gen)
+            ms, o = timed(lambda r: t.insert_or_assign(q, vals), reps, after=t.restore)
+            emit({**base, "op": "insert_or_assign_hits", "ms": ms, "bkvs": B / ms / 1e6, "outcomes": outcome_mix(o)})
+            del t
+            torch.cuda.empty_cache()
+
+
 def peer(reps, lg=27, world=2):
     """Sharded find over peer memory, `world` virtual shards of 2^lg / world
     slots on this one GPU (hkv_find_peer with same-process peers: the kernel
@@ -288,7 +315,7 @@ def peer(reps, lg=27, world=2):
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--only", default="c1,c2x,c3,c4,dual,peer")
+    p.add_argument("--only", default="c1,c2x,c3,c4,dual,cas,peer")
     p.add_argument("--reps", type=int, default=5)
     p.add_argument("--lg", type=int, default=27)
     a = p.parse_args()
@@ -297,6 +324,8 @@ def main():
     t0 = time.time()
     if "peer" in which:
         peer(a.reps, a.lg)
+    if "cas" in which:
+        cas(a.reps, a.lg)
     if "c1" in which:
         c1(a.reps)
     if "c2x" in which:
