@@ -137,12 +137,34 @@ __device__ __forceinline__ int probe_cas(const TableDev& t, uint64_t b, uint64_t
 // ---------------------------------------------------------------------------
 enum : int { kTaskNone = 0, kTaskHit = 1, kTaskRead = 2, kTaskInsert = 3, kTaskEvict = 4 };
 constexpr unsigned kFullMask = 0xFFFFFFFFu;
+#ifndef HKV_CAS_SCANB
+#define HKV_CAS_SCANB 2
+#endif
+constexpr int kScanBatch = HKV_CAS_SCANB;  // full-bucket scans per warp pass
 
 // first-index minimum (np.argmin, table.py:1080) of bucket b's 128 scores,
 // read by the whole warp (lane j: slots 4j..4j+3, 1 KB coalesced)
 __device__ __forceinline__ void warp_min(const TableDev& t, uint64_t b, int lane, uint64_t& minv, int& mslot) {
   const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(t.scores + b * kSlots + 4 * lane);
   const ulonglong2 x = __ldcg(sp), y = __ldcg(sp + 1);
+  uint64_t v = x.x;
+  int m = 4 * lane;
+  if (x.y < v) { v = x.y; m = 4 * lane + 1; }
+  if (y.x < v) { v = y.x; m = 4 * lane + 2; }
+  if (y.y < v) { v = y.y; m = 4 * lane + 3; }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t ov = __shfl_xor_sync(kFullMask, v, o);
+    const int om = __shfl_xor_sync(kFullMask, m, o);
+    if (ov < v || (ov == v && om < m)) { v = ov; m = om; }
+  }
+  minv = v;
+  mslot = m;
+}
+
+// first-index minimum over a bucket whose 128 scores the warp holds four
+// per lane (x, y = slots 4 lane .. 4 lane + 3)
+__device__ __forceinline__ void lane_min4(ulonglong2 x, ulonglong2 y, int lane, uint64_t& minv, int& mslot) {
   uint64_t v = x.x;
   int m = 4 * lane;
   if (x.y < v) { v = x.y; m = 4 * lane + 1; }
@@ -325,21 +347,45 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
       // ---- warp-cooperative score scans for full-bucket decisions ----
       unsigned sm = __ballot_sync(kFullMask, need_scan);
       while (sm) {
-        const int l = __ffs(sm) - 1;
-        sm &= sm - 1;
-        const uint64_t lb1 = __shfl_sync(kFullMask, b1, l), lb2 = __shfl_sync(kFullMask, b2, l);
-        uint64_t n1, n2 = kMaxScore;
-        int m1, m2 = 0;
-        warp_min(t, lb1, lane, n1, m1);
-        if (t.dual) warp_min(t, lb2, lane, n2, m2);
-        if (lane == l) {
-          if (!t.dual) {
-            ctr[kScans]++;
-            minv = n1, slot = m1, tb = b1;
-          } else {
-            ctr[kScans] += 2;
-            const bool use2 = n2 < n1;  // D2: the bucket with the lower minimum
-            minv = use2 ? n2 : n1, slot = use2 ? m2 : m1, tb = use2 ? b2 : b1;
+        // kScanBatch ops' buckets per pass, all loads in flight before the reductions
+        int ls[kScanBatch];
+        uint64_t p1[kScanBatch], p2[kScanBatch];
+#pragma unroll
+        for (int k = 0; k < kScanBatch; k++) {
+          ls[k] = sm ? __ffs(sm) - 1 : -1;
+          if (sm) sm &= sm - 1;
+          p1[k] = __shfl_sync(kFullMask, b1, ls[k] < 0 ? 0 : ls[k]);
+          p2[k] = __shfl_sync(kFullMask, b2, ls[k] < 0 ? 0 : ls[k]);
+        }
+        ulonglong2 x1[kScanBatch], y1[kScanBatch], x2[kScanBatch], y2[kScanBatch];
+#pragma unroll
+        for (int k = 0; k < kScanBatch; k++) {
+          if (ls[k] < 0) continue;
+          const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(t.scores + p1[k] * kSlots + 4 * lane);
+          x1[k] = __ldcg(sp);
+          y1[k] = __ldcg(sp + 1);
+          if (t.dual) {
+            const ulonglong2* sq = reinterpret_cast<const ulonglong2*>(t.scores + p2[k] * kSlots + 4 * lane);
+            x2[k] = __ldcg(sq);
+            y2[k] = __ldcg(sq + 1);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kScanBatch; k++) {
+          if (ls[k] < 0) continue;
+          uint64_t n1, n2 = kMaxScore;
+          int m1, m2 = 0;
+          lane_min4(x1[k], y1[k], lane, n1, m1);
+          if (t.dual) lane_min4(x2[k], y2[k], lane, n2, m2);
+          if (lane == ls[k]) {
+            if (!t.dual) {
+              ctr[kScans]++;
+              minv = n1, slot = m1, tb = b1;
+            } else {
+              ctr[kScans] += 2;
+              const bool use2 = n2 < n1;  // D2: the bucket with the lower minimum
+              minv = use2 ? n2 : n1, slot = use2 ? m2 : m1, tb = use2 ? b2 : b1;
+            }
           }
         }
       }
