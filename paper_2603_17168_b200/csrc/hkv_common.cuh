@@ -19,6 +19,7 @@
 #include <cooperative_groups.h>
 #include <cstdint>
 #include <type_traits>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace hkv {
@@ -285,5 +286,29 @@ __device__ __forceinline__ void block_ctrs_flush(BlockCtrs& s, unsigned long lon
 }
 
 extern unsigned long long g_launches;  // host-side launch counter (hkv_api.cu)
+
+// Programmatic dependent launch (PDL): pipeline kernels are launched with
+// programmatic stream serialization, so a kernel's launch overlaps its
+// predecessor's tail; it must not read the predecessor's output before this
+// wait (a no-op for a normally launched kernel).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+#if defined(__CUDACC__)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+#endif
 
 }  // namespace hkv

@@ -39,6 +39,7 @@ namespace hkv {
 // ---------------------------------------------------------------------------
 __global__ void k_prep(TableDev t, const uint64_t* __restrict__ keys, int64_t n, uint32_t* __restrict__ bkt,
                        uint32_t* __restrict__ idx, uint32_t* __restrict__ b2, Scalars* sc) {
+  griddep_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) {
     sc->first_ev = 0xFFFFFFFFu;
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(1024) k_segments(const uint32_t* __restrict__ 
                                                    uint32_t* __restrict__ brk, uint8_t* __restrict__ outcomes,
                                                    uint32_t* __restrict__ vrow, uint8_t fcode,
                                                    uint64_t* __restrict__ skeys) {
+  griddep_wait();
   __shared__ unsigned wcount[2][32];
   __shared__ unsigned block_base[2];
   if (sc->err) return;
@@ -234,6 +236,8 @@ struct TpsState {
   uint32_t smdirty;  // sm entries to write back
   bool sloaded;      // sm / sv loaded
   bool svdirty;
+  uint64_t pk[2];    // k_meta_tps: keys of the head op's first two digest candidates, loaded one
+  int npk;           //   segment ahead (register software pipelining); npk of them valid
 };
 
 // Register-array helpers written as masked arithmetic over every element:
@@ -423,14 +427,16 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
   tps_cand(t, S, d, c);
   int hit = -1;
   unsigned ncmp = 0;
+  const int npk = (!C && q == S.p0) ? S.npk : 0;  // the head op's first candidates are prefetched
 #pragma unroll
   for (int w = 0; w < 4; w++) {
     uint32_t m = hit < 0 ? c[w] : 0u;
     while (m) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
+      const uint64_t k = (int)ncmp < npk ? (ncmp == 0 ? S.pk[0] : S.pk[1]) : bkey<C>(t, S, 32 * w + j);
       ncmp++;
-      if (bkey<C>(t, S, 32 * w + j) == key) {
+      if (k == key) {
         hit = 32 * w + j;
         m = 0;
       }
@@ -664,9 +670,13 @@ __device__ __forceinline__ void tps_segment(const TableDev& t, const OpArgs& a, 
                                             int32_t* __restrict__ rsrc, uint64_t clock0, bool fel_open,
                                             bool spec, bool lfu_like, bool runs, ctr_t* ctr, int& sd,
                                             uint32_t& fe_min, int* lw, int64_t lws, uint64_t* K = nullptr,
-                                            uint64_t* Sc = nullptr, int cs = 0) {
+                                            uint64_t* Sc = nullptr, int cs = 0, uint64_t pk0 = 0, uint64_t pk1 = 0,
+                                            int npk = 0) {
   const uint64_t b = rec.b;
   TpsState S;
+  S.pk[0] = pk0;
+  S.pk[1] = pk1;
+  S.npk = npk;
   S.lw = lw;
   S.lws = lws;
   S.sidx = sidx;
@@ -751,6 +761,7 @@ __global__ void __launch_bounds__(kTpsThreads, HKV_TPS_MINB) k_meta_tps(TableDev
                                                             const SegRec* __restrict__ recs, int64_t cap, int64_t n,
                                                             uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
                                                             int32_t* __restrict__ rsrc, int* __restrict__ lwtab) {
+  griddep_wait();
   extern __shared__ uint4 tps_smem[];
   __shared__ BlockCtrs bc;
   if (a.sc->err) return;
@@ -778,16 +789,48 @@ __global__ void __launch_bounds__(kTpsThreads, HKV_TPS_MINB) k_meta_tps(TableDev
   cp_async_commit();
   if (j + stride < nall) tps_fetch(t, tps_buf(tps_smem, 1), rb.b);
   cp_async_commit();
+  // keys of the head op's first two digest candidates of the segment after
+  // the current one, loaded into registers while the current one runs
+  uint64_t pk0 = 0, pk1 = 0;
+  int npk = 0;
+  auto prefetch_keys = [&](const SegRec& r, const uint4* L) {
+    npk = 0;
+    if (!t.digest_filter) return;
+    const uint32_t* O = reinterpret_cast<const uint32_t*>(L + 8);
+    const uint32_t d = r.flags >> 8;
+    int s0 = -1, s1 = -1;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      uint32_t m = (match16(L[2 * q], d) | (match16(L[2 * q + 1], d) << 16)) & O[q];
+      while (m && s1 < 0) {
+        const int x = 32 * q + __ffs(m) - 1;
+        m &= m - 1;
+        if (s0 < 0) s0 = x; else s1 = x;
+      }
+    }
+    const uint64_t* kr = t.keys + (uint64_t)r.b * kSlots;
+    if (s0 >= 0) { pk0 = kr[s0]; npk = 1; }
+    if (s1 >= 0) { pk1 = kr[s1]; npk = 2; }
+  };
+  if (j < nall) {
+    cp_async_wait<1>();
+    prefetch_keys(ra, tps_buf(tps_smem, 0));
+  }
   for (int stage = 0; j < nall; j += stride, stage ^= 1) {
     const SegRec rn = rec_at(j + 2 * stride);  // in flight while segment j is processed
     cp_async_wait<1>();
     uint4* buf = tps_buf(tps_smem, stage);
     tps_segment<OP, COLLECT, false>(t, a, ra, buf, sb, sidx, run_end, skeys, n, vrow, rrow, rsrc, clock0, fel_open, spec,
-                             lfu_like, runs, ctr, sd, fe_min, lwtab + gtid, stride);
+                             lfu_like, runs, ctr, sd, fe_min, lwtab + gtid, stride, nullptr, nullptr, 0, pk0, pk1,
+                             npk);
     ra = rb;
     rb = rn;
     if (j + 2 * stride < nall) tps_fetch(t, buf, rb.b);
     cp_async_commit();
+    if (j + stride < nall) {  // the next segment's line landed one segment ago
+      cp_async_wait<1>();
+      prefetch_keys(ra, tps_buf(tps_smem, stage ^ 1));
+    }
   }
   cp_async_wait<0>();
   if (fel_open) {
@@ -814,6 +857,7 @@ __global__ void __launch_bounds__(kLongThreads) k_meta_long(TableDev t, OpArgs a
                                                            const SegRec* __restrict__ lrecs, int64_t n,
                                                            uint32_t* __restrict__ vrow, uint32_t* __restrict__ rrow,
                                                            int32_t* __restrict__ rsrc) {
+  griddep_wait();
   extern __shared__ uint4 long_smem[];
   __shared__ BlockCtrs bc;
   if (a.sc->err) return;
@@ -866,6 +910,7 @@ template <int VEC, int KPT>
 __global__ void __launch_bounds__(256) k_values_write(TableDev t, const float* __restrict__ values,
                                                       const uint32_t* __restrict__ vrow, int64_t n,
                                                       const Scalars* sc) {
+  griddep_wait();
   if (sc->err) return;
   using V = typename std::conditional<VEC == 4, uint4, typename std::conditional<VEC == 2, float2, float>::type>::type;
   const Tile8 tile;
@@ -917,6 +962,7 @@ __global__ void __launch_bounds__(256) k_values_read(TableDev t, float* __restri
                                                      const long long* n_list, const uint64_t* __restrict__ ek_tmp,
                                                      const uint64_t* __restrict__ es_tmp, uint64_t* ek, uint64_t* es,
                                                      float* ev, int64_t n, const Scalars* sc) {
+  griddep_wait();
   if (sc->err) return;
   using V = typename std::conditional<VEC == 4, uint4, typename std::conditional<VEC == 2, float2, float>::type>::type;
   const Tile8 tile;
@@ -979,6 +1025,7 @@ __global__ void __launch_bounds__(256) k_values_read(TableDev t, float* __restri
 constexpr int kFinBlocks = 32;
 __global__ void __launch_bounds__(1024) k_finalize(TableDev t, Scalars* sc, const uint8_t* __restrict__ outcomes,
                                                    int64_t n, unsigned long long clock_advance, int add_found) {
+  griddep_wait();
   if (sc->err) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(t.err, sc->err);
     return;
@@ -1015,6 +1062,7 @@ __global__ void k_evict_gather(const Scalars* sc, const uint32_t* __restrict__ l
                                const uint64_t* __restrict__ ek_tmp, const uint64_t* __restrict__ es_tmp,
                                const float* __restrict__ ev_tmp, uint64_t* ek, uint64_t* es, float* ev,
                                int dim, int64_t n) {
+  griddep_wait();
   const Tile8 tile;
   const int r = tile.thread_rank();
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG;
@@ -1031,6 +1079,7 @@ __global__ void k_evict_gather(const Scalars* sc, const uint32_t* __restrict__ l
 }
 
 __global__ void k_zero_count(const Scalars* sc, long long* n_ev) {
+  griddep_wait();
   if (sc->err) *n_ev = 0;
 }
 
@@ -1040,6 +1089,7 @@ __global__ void k_zero_count(const Scalars* sc, long long* n_ev) {
 __global__ void __launch_bounds__(256) k_assign_find(TableDev t, const uint64_t* __restrict__ keys, int64_t n,
                                                      uint32_t* __restrict__ rows, uint8_t* __restrict__ outcomes,
                                                      Scalars* sc) {
+  griddep_wait();
   // thread per key (the find path's probe: one digest line per thread, the
   // candidate keys in slot order; counters as table.py:243-268)
   if (sc->err) return;
@@ -1079,6 +1129,7 @@ __global__ void __launch_bounds__(256) k_assign_apply(TableDev t, const float* _
                                                       const uint32_t* __restrict__ sb,
                                                       const uint32_t* __restrict__ sidx, int64_t n,
                                                       Scalars* sc) {
+  griddep_wait();
   if (sc->err) return;
   const Tile8 tile;
   const int r = tile.thread_rank();
@@ -1132,6 +1183,7 @@ struct IsUpdated {
 };
 
 __global__ void k_assign_count(Scalars* sc, const uint32_t* ranks, const uint8_t* outcomes, int64_t n) {
+  griddep_wait();
   if (sc->err || n <= 0) return;
   sc->nfound = (unsigned long long)ranks[n - 1] + (outcomes[n - 1] == kUpdated ? 1ull : 0ull);
 }
@@ -1152,6 +1204,7 @@ __device__ __forceinline__ uint32_t agg_hash(uint32_t row) {
 __global__ void k_assign_agg(const uint32_t* __restrict__ rows, int64_t n, uint32_t* __restrict__ akey,
                              uint32_t* __restrict__ alast, uint32_t* __restrict__ acnt, uint32_t amask,
                              uint32_t* __restrict__ aslot, const Scalars* sc, int count) {
+  griddep_wait();
   if (sc->err) return;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -1178,6 +1231,7 @@ __global__ void __launch_bounds__(256) k_assign_apply_agg(TableDev t, const floa
                                                           const uint32_t* __restrict__ acnt,
                                                           const uint32_t* __restrict__ aslot, int64_t n,
                                                           const Scalars* sc) {
+  griddep_wait();
   if (sc->err) return;
   const Tile8 tile;
   const int r = tile.thread_rank();
@@ -1329,6 +1383,7 @@ constexpr int kRunThreads = 1024, kRunPer = 4, kRunTile = kRunThreads * kRunPer;
 __global__ void __launch_bounds__(kRunThreads) k_run_ends_tile(const uint32_t* __restrict__ brk, int64_t n,
                                                                uint32_t* __restrict__ run_end,
                                                                uint32_t* __restrict__ tile_first, const Scalars* sc) {
+  griddep_wait();
   if (!sc->has_runs || sc->err) return;
   typedef cub::BlockScan<uint32_t, kRunThreads> BS;
   __shared__ typename BS::TempStorage tmp;
@@ -1354,6 +1409,7 @@ __global__ void __launch_bounds__(kRunThreads) k_run_ends_tile(const uint32_t* _
 
 __global__ void k_run_ends_fix(int64_t n, uint32_t* __restrict__ run_end, const uint32_t* __restrict__ tile_first,
                                int64_t ntiles, const Scalars* sc) {
+  griddep_wait();
   if (!sc->has_runs || sc->err) return;
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n || run_end[p] != 0xFFFFFFFFu) return;
@@ -1365,8 +1421,8 @@ __global__ void k_run_ends_fix(int64_t n, uint32_t* __restrict__ run_end, const 
 static cudaError_t run_ends(Workspace& ws, int64_t n, cudaStream_t s) {
   // tile_first lives in ws.rrow: the metadata pass that fills rrow runs after both kernels
   const int64_t ntiles = (n + kRunTile - 1) / kRunTile;
-  k_run_ends_tile<<<(unsigned)ntiles, kRunThreads, 0, s>>>(ws.aux2, n, ws.seg, ws.rrow, ws.sc);
-  k_run_ends_fix<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, ws.seg, ws.rrow, ntiles, ws.sc);
+  launch_pdl(k_run_ends_tile, dim3((unsigned)ntiles), dim3(kRunThreads), 0, s, ws.aux2, n, ws.seg, ws.rrow, ws.sc);
+  launch_pdl(k_run_ends_fix, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, n, ws.seg, ws.rrow, ntiles, ws.sc);
   g_launches += 2;
   return cudaGetLastError();
 }
@@ -1392,7 +1448,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
   if ((e = cudaMemsetAsync(ws.sc, 0, sizeof(Scalars), s))) return e;
   if (n > 0) {
     ktimer_begin("prep", s, 2);
-    k_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(t, a.keys, n, ws.bkt, ws.idx, t.dual ? ws.b2 : nullptr,
+    launch_pdl(k_prep, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, t, a.keys, n, ws.bkt, ws.idx, t.dual ? ws.b2 : nullptr,
                                                         ws.sc);
     ktimer_end("prep", s, 2);
     g_launches++;
@@ -1416,7 +1472,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       // segments are better overlapped with everything else inside k_meta_tps.
       const bool use_long = n >= kLongSeg && (n >> log2_buckets) >= 16;
       SegRec* lrecs = use_long ? reinterpret_cast<SegRec*>(ws.lrec) : nullptr;
-      k_segments<<<(unsigned)((n + 1023) / 1024), 1024, 0, s>>>(ws.sbkt, ws.sidx, a.keys, n, recs, n, lrecs, ws.sc, ws.aux2,
+      launch_pdl(k_segments, dim3((unsigned)((n + 1023) / 1024)), dim3(1024), 0, s, ws.sbkt, ws.sidx, a.keys, n, recs, n, lrecs, ws.sc, ws.aux2,
                                                                  a.outcomes, ws.vrow, fcode, ws.skeys);
       g_launches++;
       if ((e = run_ends(ws, n, s))) return e;
@@ -1441,7 +1497,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       const int64_t tcap = (int64_t)num_sms * HKV_TPS_MINB;  // one resident wave
       if (!ws.lwtab && (e = grow(ws.lwtab, tcap * kTpsThreads * kSlots))) return e;  // 128 entries per thread
       if (tb > tcap) tb = tcap;
-      fn<<<(unsigned)(tb < 1 ? 1 : tb), kTpsThreads, smem, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, recs, n, n,
+      launch_pdl(fn, dim3((unsigned)(tb < 1 ? 1 : tb)), dim3(kTpsThreads), smem, s, t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, recs, n, n,
                                                                ws.vrow, ws.rrow, ws.rsrc,
                                                                ws.lwtab);
       if (use_long) {
@@ -1455,7 +1511,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
             cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLongSmem);
           lattr.fetch_or(dbit);
         }
-        fl<<<(unsigned)num_sms, kLongThreads, kLongSmem, s>>>(t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, lrecs, n,
+        launch_pdl(fl, dim3((unsigned)num_sms), dim3(kLongThreads), kLongSmem, s, t, a, ws.sbkt, ws.sidx, ws.seg, ws.skeys, lrecs, n,
                                                               ws.vrow, ws.rrow, ws.rsrc);
         g_launches++;
       }
@@ -1472,7 +1528,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
   ktimer_begin("finalize", s, 2);
   // an empty batch never runs k_prep, which seeds first_ev: no outcomes, so
   // first_eviction_lambda cannot latch from the zeroed scratch
-  k_finalize<<<kFinBlocks, 1024, 0, s>>>(t, ws.sc, (a.op == kOpErase || n == 0) ? nullptr : a.outcomes, n,
+  launch_pdl(k_finalize, dim3(kFinBlocks), dim3(1024), 0, s, t, ws.sc, (a.op == kOpErase || n == 0) ? nullptr : a.outcomes, n,
                                          clock_advance, 0);
   ktimer_end("finalize", s, 2);
   g_launches++;
@@ -1496,13 +1552,13 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       if (rblocks > rcap) rblocks = rcap;
       if (rblocks < 1) rblocks = 1;
       if (vr == 4)
-        k_values_read<4, 4><<<(unsigned)rblocks, 256, 0, s>>>(t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
+        launch_pdl(k_values_read<4, 4>, dim3((unsigned)rblocks), dim3(256), 0, s, t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
                                                            ws.ek, ws.es, ek_out, es_out, ev_out, n, ws.sc);
       else if (vr == 2)
-        k_values_read<2, 4><<<(unsigned)rblocks, 256, 0, s>>>(t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
+        launch_pdl(k_values_read<2, 4>, dim3((unsigned)rblocks), dim3(256), 0, s, t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
                                                            ws.ek, ws.es, ek_out, es_out, ev_out, n, ws.sc);
       else
-        k_values_read<1, 4><<<(unsigned)rblocks, 256, 0, s>>>(t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
+        launch_pdl(k_values_read<1, 4>, dim3((unsigned)rblocks), dim3(256), 0, s, t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
                                                            ws.ek, ws.es, ek_out, es_out, ev_out, n, ws.sc);
       g_launches++;
     }
@@ -1510,9 +1566,9 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
     const int64_t wblocks = (((n + 3) / 4) * kG + 255) / 256;
     const int64_t wcap = (int64_t)num_sms * 8 * 4;
     const unsigned wb = (unsigned)(wblocks < wcap ? (wblocks < 1 ? 1 : wblocks) : wcap);
-    if (vr == 4) k_values_write<4, 4><<<wb, 256, 0, s>>>(t, a.values, ws.vrow, n, ws.sc);
-    else if (vr == 2) k_values_write<2, 4><<<wb, 256, 0, s>>>(t, a.values, ws.vrow, n, ws.sc);
-    else k_values_write<1, 4><<<wb, 256, 0, s>>>(t, a.values, ws.vrow, n, ws.sc);
+    if (vr == 4) launch_pdl(k_values_write<4, 4>, dim3(wb), dim3(256), 0, s, t, a.values, ws.vrow, n, ws.sc);
+    else if (vr == 2) launch_pdl(k_values_write<2, 4>, dim3(wb), dim3(256), 0, s, t, a.values, ws.vrow, n, ws.sc);
+    else launch_pdl(k_values_write<1, 4>, dim3(wb), dim3(256), 0, s, t, a.values, ws.vrow, n, ws.sc);
     ktimer_end("values_write", s);
     g_launches++;
   }
@@ -1520,18 +1576,18 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
     if (n > 0 && inplace) {
       const int vec = vec_of(t.dim, ev_out, ws.ev, nullptr, nullptr);
       if (vec == 4)
-        k_evict_gather<4><<<(unsigned)vblocks, 256, 0, s>>>(ws.sc, ws.aux, nev, ws.ek, ws.es, ws.ev, ek_out, es_out,
+        launch_pdl(k_evict_gather<4>, dim3((unsigned)vblocks), dim3(256), 0, s, ws.sc, ws.aux, nev, ws.ek, ws.es, ws.ev, ek_out, es_out,
                                                             ev_out, t.dim, n);
       else if (vec == 2)
-        k_evict_gather<2><<<(unsigned)vblocks, 256, 0, s>>>(ws.sc, ws.aux, nev, ws.ek, ws.es, ws.ev, ek_out, es_out,
+        launch_pdl(k_evict_gather<2>, dim3((unsigned)vblocks), dim3(256), 0, s, ws.sc, ws.aux, nev, ws.ek, ws.es, ws.ev, ek_out, es_out,
                                                             ev_out, t.dim, n);
       else
-        k_evict_gather<1><<<(unsigned)vblocks, 256, 0, s>>>(ws.sc, ws.aux, nev, ws.ek, ws.es, ws.ev, ek_out, es_out,
+        launch_pdl(k_evict_gather<1>, dim3((unsigned)vblocks), dim3(256), 0, s, ws.sc, ws.aux, nev, ws.ek, ws.es, ws.ev, ek_out, es_out,
                                                             ev_out, t.dim, n);
       g_launches++;
     }
     if (n > 0) {
-      k_zero_count<<<1, 1, 0, s>>>(ws.sc, nev);
+      launch_pdl(k_zero_count, dim3(1), dim3(1), 0, s, ws.sc, nev);
       g_launches++;
     } else if ((e = cudaMemsetAsync(n_evicted, 0, sizeof(int64_t), s))) {
       return e;
@@ -1551,7 +1607,7 @@ cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* val
     const int64_t blocks = tile_blocks(n, num_sms);
     int64_t fblocks = (n + 255) / 256;
     if (fblocks > (int64_t)num_sms * 8) fblocks = (int64_t)num_sms * 8;
-    k_assign_find<<<(unsigned)(fblocks < 1 ? 1 : fblocks), 256, 0, s>>>(t, keys, n, ws.aux, outcomes, ws.sc);
+    launch_pdl(k_assign_find, dim3((unsigned)(fblocks < 1 ? 1 : fblocks)), dim3(256), 0, s, t, keys, n, ws.aux, outcomes, ws.sc);
     g_launches++;
     if (need_ticks) {
       size_t bytes = ws.cub_bytes;
@@ -1560,7 +1616,7 @@ cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* val
                                                                                               IsUpdated{outcomes});
       if ((e = cub::DeviceScan::ExclusiveSum(ws.cub_tmp, bytes, up, ws.aux2, (int)n, s))) return e;
       g_launches += 2;
-      k_assign_count<<<1, 1, 0, s>>>(ws.sc, ws.aux2, outcomes, n);
+      launch_pdl(k_assign_count, dim3(1), dim3(1), 0, s, ws.sc, ws.aux2, outcomes, n);
       g_launches++;
     }
     // Duplicate resolution.  Batches dense in duplicates (>= 16 ops per bucket,
@@ -1585,38 +1641,38 @@ cudaError_t run_assign(const TableDev& t, const uint64_t* keys, const float* val
       if ((e = cudaMemsetAsync(akey, 0xFF, (size_t)acap * 4, s)) ||
           (e = cudaMemsetAsync(alast, 0, (size_t)acap * (count ? 8 : 4), s)))
         return e;
-      k_assign_agg<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ws.aux, n, akey, alast, acnt, (uint32_t)(acap - 1),
+      launch_pdl(k_assign_agg, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, ws.aux, n, akey, alast, acnt, (uint32_t)(acap - 1),
                                                               ws.vrow, ws.sc, count);
       g_launches++;
       ktimer_begin("assign_apply", s);
       if (vec == 4)
-        k_assign_apply_agg<4><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2,
+        launch_pdl(k_assign_apply_agg<4>, dim3((unsigned)blocks), dim3(256), 0, s, t, values, scores, refresh, epoch, ws.aux, ws.aux2,
                                                                ticks, alast, acnt, ws.vrow, n, ws.sc);
       else if (vec == 2)
-        k_assign_apply_agg<2><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2,
+        launch_pdl(k_assign_apply_agg<2>, dim3((unsigned)blocks), dim3(256), 0, s, t, values, scores, refresh, epoch, ws.aux, ws.aux2,
                                                                ticks, alast, acnt, ws.vrow, n, ws.sc);
       else
-        k_assign_apply_agg<1><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2,
+        launch_pdl(k_assign_apply_agg<1>, dim3((unsigned)blocks), dim3(256), 0, s, t, values, scores, refresh, epoch, ws.aux, ws.aux2,
                                                                ticks, alast, acnt, ws.vrow, n, ws.sc);
     } else {
-      k_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(t, keys, n, ws.bkt, ws.idx, nullptr, ws.sc);
+      launch_pdl(k_prep, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, t, keys, n, ws.bkt, ws.idx, nullptr, ws.sc);
       g_launches++;
       if ((e = sort_segments(ws, n, log2_buckets, s))) return e;
       ktimer_begin("assign_apply", s);
       if (vec == 4)
-        k_assign_apply<4><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks,
+        launch_pdl(k_assign_apply<4>, dim3((unsigned)blocks), dim3(256), 0, s, t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks,
                                                            ws.sbkt, ws.sidx, n, ws.sc);
       else if (vec == 2)
-        k_assign_apply<2><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks,
+        launch_pdl(k_assign_apply<2>, dim3((unsigned)blocks), dim3(256), 0, s, t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks,
                                                            ws.sbkt, ws.sidx, n, ws.sc);
       else
-        k_assign_apply<1><<<(unsigned)blocks, 256, 0, s>>>(t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks,
+        launch_pdl(k_assign_apply<1>, dim3((unsigned)blocks), dim3(256), 0, s, t, values, scores, refresh, epoch, ws.aux, ws.aux2, ticks,
                                                            ws.sbkt, ws.sidx, n, ws.sc);
     }
     ktimer_end("assign_apply", s);
     g_launches++;
   }
-  k_finalize<<<kFinBlocks, 1024, 0, s>>>(t, ws.sc, nullptr, n, (refresh && !scores && ticks) ? clock_advance : 0,
+  launch_pdl(k_finalize, dim3(kFinBlocks), dim3(1024), 0, s, t, ws.sc, nullptr, n, (refresh && !scores && ticks) ? clock_advance : 0,
                                 need_ticks ? 1 : 0);
   g_launches++;
   return cudaGetLastError();
