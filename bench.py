@@ -67,7 +67,11 @@ def parse():
     p.add_argument("--lambdas", default="0.5,0.75,1.0")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-extras", action="store_true",
+                   help="skip the per-config extras (insert_and_evict, CAS engine, dual mode, C1, C3, C4)")
     p.add_argument("--quick", action="store_true", help="2^24 slots, for profiling runs")
+    p.add_argument("--c4-capacity", type=int, default=2**26,
+                   help="C4 extra: slots of the dim-128 host-tiered table (2^26 = 32 GiB pinned host memory)")
     p.add_argument("--routed-find", action="store_true",
                    help="sharded runs: route finds through two all-to-alls instead of reading the owner shard "
                         "over NVLink peer memory (hkv_find_peer, the default)")
@@ -298,6 +302,153 @@ def fill_table(t, lam, capacity, dim, batch, torch, W, seed=0):
         off += n
     return off
 
+
+
+# ---------------------------------------------------------------------------
+# extras: every other SURVEY.md 8(d) row timed by the driver's own run
+# ---------------------------------------------------------------------------
+def _timed(torch, fn, reps, after=None):
+    """median device ms of fn(r) over reps (CUDA events on the current stream,
+    the op enqueued behind a 0.2 ms spin; after() untimed between reps)."""
+    st = torch.cuda.current_stream()
+    ms, out = [], None
+    for r in range(reps + 1):
+        torch.cuda.synchronize()
+        torch.cuda._sleep(SPIN_CYCLES)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        out = fn(r)
+        b.record(st)
+        torch.cuda.synchronize()
+        if r > 0:
+            ms.append(a.elapsed_time(b))
+        if after is not None:
+            after()
+    return statistics.median(ms), out
+
+
+def _mix(torch, o):
+    c = torch.bincount(o.to(torch.int64), minlength=7).cpu().tolist()
+    return {n: v for n, v in zip(["inserted", "updated", "rejected", "evicted", "found", "not_found", "erased"], c)
+            if v}
+
+
+def _rec(ms, n, extra=None):
+    d = {"ms": round(ms, 4), "bkvs": round(n / ms / 1e6, 4)}
+    if extra:
+        d.update(extra)
+    return d
+
+
+def _fill(t, lam, cap, dim, batch, torch, W, seed=0):
+    return fill_table(t, lam, cap, dim, batch, torch, W, seed)
+
+
+def run_extras(a, tables, torch, hkv, W):
+    """Per-config device timings on the headline tables and on fresh ones:
+    insert_and_evict and the CAS engine (workers > 1) at each lambda; dual
+    mode (serial dataflow and CAS engine) at 0.5 / 1.0; C1; C3 zipf
+    insert_and_evict (kLfu, kCustomized); C4 tiered find / assign."""
+    B, dim, cap, reps = a.batch, a.dim, a.capacity, 3
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    vals = torch.randn((B, dim), device="cuda", generator=gen)
+    fresh = [W.uniform_distinct_keys_torch(B, 0, stream_offset=2**45 + r * B) for r in range(reps + 1)]
+    ex = {}
+    # --- C2 tables: insert_and_evict, CAS engine ---
+    for lam, t in tables.items():
+        key = f"c2_{lam:.2f}"
+        ms, o = _timed(torch, lambda r: t.insert_and_evict(fresh[r], vals)[0], reps, after=t.restore)
+        ex[f"{key}_insert_and_evict"] = _rec(ms, B, {"outcomes": _mix(torch, o)})
+        t.set_workers(8)
+        ms, o = _timed(torch, lambda r: t.insert_or_assign(fresh[r], vals), reps, after=t.restore)
+        ex[f"{key}_cas_insert_or_assign"] = _rec(ms, B, {"outcomes": _mix(torch, o)})
+        res = torch.from_numpy(t.occupied_keys().view(np.int64)).cuda()
+        hits = res[torch.randint(0, res.numel(), (B,), device="cuda", generator=gen)]
+        del res
+        ms, o = _timed(torch, lambda r: t.insert_or_assign(hits, vals), reps, after=t.restore)
+        ex[f"{key}_cas_update_hits"] = _rec(ms, B, {"outcomes": _mix(torch, o)})
+        t.set_workers(1)
+        ms, o = _timed(torch, lambda r: t.insert_or_assign(hits, vals), reps, after=t.restore)
+        ex[f"{key}_update_hits"] = _rec(ms, B, {"outcomes": _mix(torch, o)})
+        ms, o = _timed(torch, lambda r: t.assign(hits, vals), reps)
+        ex[f"{key}_assign"] = _rec(ms, B)
+        ms, o = _timed(torch, lambda r: t.contains(hits), reps)
+        ex[f"{key}_contains"] = _rec(ms, B)
+        ms, o = _timed(torch, lambda r: t.find_ptr(hits), reps)
+        ex[f"{key}_find_ptr"] = _rec(ms, B)
+        miss = fresh[0]
+        ms, o = _timed(torch, lambda r: t.find(miss), reps)
+        ex[f"{key}_find_miss"] = _rec(ms, B)
+    tables.clear()
+    torch.cuda.empty_cache()
+    # --- dual mode (C2 shape) ---
+    for lam in (0.5, 1.0):
+        t = hkv.CacheTable(hkv.TableConfig(capacity=cap, value_dim=dim, mode="dual", workers=8))
+        t.validate_keys = False
+        _fill(t, lam, cap, dim, B, torch, W)
+        t.snapshot()
+        key = f"dual_{lam:.2f}"
+        ex[f"{key}_lambda_actual"] = round(t.load_factor(), 4)
+        ms, o = _timed(torch, lambda r: t.insert_or_assign(fresh[r], vals), reps, after=t.restore)
+        ex[f"{key}_cas_insert_or_assign"] = _rec(ms, B, {"outcomes": _mix(torch, o)})
+        t.set_workers(1)
+        ms, o = _timed(torch, lambda r: t.insert_or_assign(fresh[r], vals), reps, after=t.restore)
+        ex[f"{key}_insert_or_assign"] = _rec(ms, B, {"outcomes": _mix(torch, o)})
+        res = torch.from_numpy(t.occupied_keys().view(np.int64)).cuda()
+        hits = res[torch.randint(0, res.numel(), (B,), device="cuda", generator=gen)]
+        del res
+        ms, o = _timed(torch, lambda r: t.find(hits), reps)
+        ex[f"{key}_find"] = _rec(ms, B)
+        del t
+        torch.cuda.empty_cache()
+    # --- C1: 2^20 slots, dim 8, prefill 0.5, 1M insert_and_evict + 1M mixed find ---
+    t = hkv.CacheTable(hkv.TableConfig(capacity=2**20, value_dim=8))
+    t.validate_keys = False
+    v8 = torch.randn((B, 8), device="cuda", generator=gen)
+    t.insert_or_assign(W.uniform_distinct_keys_torch(2**19, 0), v8[: 2**19])
+    t.snapshot()
+    k1 = W.uniform_distinct_keys_torch(B, 0, stream_offset=2**41)
+    ms, o = _timed(torch, lambda r: t.insert_and_evict(k1, v8)[0], reps, after=t.restore)
+    ex["c1_insert_and_evict"] = _rec(ms, B, {"outcomes": _mix(torch, o)})
+    t.insert_and_evict(k1, v8)
+    ms, o = _timed(torch, lambda r: t.find(k1), reps)
+    ex["c1_find"] = _rec(ms, B)
+    del t
+    # --- C3: zipf alpha 0.99 insert_and_evict at lambda 1 (kLfu, kCustomized) ---
+    for pol in ("kLfu", "kCustomized"):
+        t = hkv.CacheTable(hkv.TableConfig(capacity=cap, value_dim=dim, score_policy=pol))
+        t.validate_keys = False
+        j = 0
+        while t.size() < cap and j < 4 * cap // B:
+            k = W.uniform_distinct_keys_torch(B, 0, stream_offset=j * B)
+            sc = (torch.arange(B, device="cuda", dtype=torch.int64) + j * B) if pol == "kCustomized" else None
+            t.insert_or_assign(k, vals, sc)
+            j += 1
+        t.snapshot()
+        zk = [torch.from_numpy(W.zipf_keys(B, 4 * cap, 0.99, seed=r).view(np.int64)).cuda() for r in range(reps + 1)]
+        zs = torch.arange(B, device="cuda", dtype=torch.int64) + j * B if pol == "kCustomized" else None
+        ms, o = _timed(torch, lambda r: t.insert_and_evict(zk[r], vals, zs)[0], reps, after=t.restore)
+        ex[f"c3_{pol}_insert_and_evict"] = _rec(ms, B, {"outcomes": _mix(torch, o)})
+        del t, zk
+        torch.cuda.empty_cache()
+    # --- C4: dim 128, every value row in mapped pinned host memory ---
+    c4cap = a.c4_capacity
+    t = hkv.CacheTable(hkv.TableConfig(capacity=c4cap, value_dim=128, fast_tier_budget=0))
+    t.validate_keys = False
+    v128 = torch.randn((B, 128), device="cuda", generator=gen)
+    _fill(t, 0.5, c4cap, 128, B, torch, W)
+    res = torch.from_numpy(t.occupied_keys().view(np.int64)).cuda()
+    hits = res[torch.randint(0, res.numel(), (B,), device="cuda", generator=gen)]
+    del res
+    ms, o = _timed(torch, lambda r: t.find(hits), reps)
+    ex["c4_find"] = _rec(ms, B, {"gbs_pcie": round(B * 512 / ms / 1e6, 1), "capacity": c4cap})
+    ms, o = _timed(torch, lambda r: t.find_ptr(hits), reps)
+    ex["c4_find_ptr"] = _rec(ms, B)
+    ms, o = _timed(torch, lambda r: t.assign(hits, v128), reps)
+    ex["c4_assign"] = _rec(ms, B, {"gbs_pcie": round(B * 512 / ms / 1e6, 1)})
+    del t
+    torch.cuda.empty_cache()
+    return ex
 
 def run_single(a):
     import torch
@@ -532,6 +683,11 @@ def run_single(a):
         e2e = {"value": keys_total / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d // a.steps,
                "d2h_bytes_per_step": d2h // a.steps}
 
+    extras = None
+    if not a.no_extras:
+        t = None  # drop the loop's reference: run_extras frees the headline tables
+        extras = run_extras(a, tables, torch, hkv, W)
+
     cpu_base = None
     if not a.no_cpu_baseline:
         # the reference package itself at this configuration, bounded to one
@@ -571,6 +727,7 @@ def run_single(a):
         "host_issue_us_per_op": round(host_s[0] * 1e6 / (a.steps * len(a.lambdas) * 2), 1),
         "fill_s": round(fill_s, 1),
         "clocks": clk, "gpu_launches": int(launches), "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu_base,
+        "extras": extras,
     }
     print(json.dumps(line), flush=True)
 

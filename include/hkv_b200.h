@@ -85,6 +85,9 @@ const char *hkv_version(void);
 /* CacheTable.__init__ (table.py:139-160) + TieredValueStore (store.py:41-79). */
 int hkv_create(const hkv_config *cfg, hkv_table **out);
 int hkv_destroy(hkv_table *t);
+/* Switch the upsert engine of a live table (hkv_config.workers semantics):
+ * 1 = serial batch order, > 1 = concurrent slot CAS.  Takes the inserter role. */
+int hkv_set_workers(hkv_table *t, int32_t workers);
 
 /* ---- triple-group role gate (gate.py:60-157) ----
  * Readers run with readers, updaters with updaters, an inserter alone;

@@ -42,6 +42,7 @@ SIGNATURES = {
     "hkv_launch_count": (_i64, []),
     "hkv_create": (C.c_int, [C.POINTER(HkvConfig), C.POINTER(_vp)]),
     "hkv_destroy": (C.c_int, [_vp]),
+    "hkv_set_workers": (C.c_int, [_vp, _i32]),
     "hkv_find": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _i32, _vp]),
     "hkv_contains": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "hkv_find_ptr": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),

@@ -427,6 +427,25 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
   return HKV_OK;
 }
 
+int hkv_set_workers(hkv_table* t, int32_t workers) {
+  if (!t) return fail(HKV_EINVAL, "null table");
+  if (workers < 1) return fail(HKV_EINVAL, "workers must be >= 1");
+  DeviceGuard _g(t->cfg.device);
+  // an engine switch is a structural event: no batch of either engine may be in flight
+  GateScope _gs(t->gate, HKV_ROLE_INSERTER, (cudaStream_t)0);
+  if (_gs.rc) return gate_fail(_gs.rc);
+  cudaError_t e = cudaSuccess;
+  if (workers > 1 && !t->locks) {
+    if ((e = cudaMalloc((void**)&t->locks, (size_t)t->buckets * 4)) ||
+        (e = cudaMemset(t->locks, 0, (size_t)t->buckets * 4)) || (e = cudaDeviceSynchronize()))
+      return fail(HKV_ENOMEM, "bucket lock allocation failed");
+  }
+  t->cfg.workers = workers;
+  t->dev.cas = workers > 1;
+  t->dev.locks = t->locks;
+  return HKV_OK;
+}
+
 int hkv_table_gate(hkv_table* t, hkv_gate** out) {
   if (!t || !out) return fail(HKV_EINVAL, "null argument");
   *out = t->gate;

@@ -691,6 +691,14 @@ class CacheTable:
     def load_factor(self) -> float:
         return self.size() / self.config.capacity
 
+    def set_workers(self, workers: int) -> None:
+        """Switch the upsert engine (TableConfig.workers semantics): 1 =
+        serial batch order, > 1 = concurrent slot CAS (hkv_set_workers)."""
+        if workers < 1:
+            raise ValueError("workers must be >= 1")
+        _lib.check(self._lib.hkv_set_workers(self._h, int(workers)))
+        self.config.workers = int(workers)
+
     def set_epoch(self, epoch: int) -> None:
         self.epoch.advance_to(epoch)
         _lib.check(self._lib.hkv_set_epoch(self._h, int(epoch)))
