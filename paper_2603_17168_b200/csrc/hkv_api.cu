@@ -752,7 +752,7 @@ int hkv_find_peer(hkv_table* t, const uint64_t* keys, int64_t n, float* out, uin
 // ---- single-key API -------------------------------------------------------
 static int one_ready(hkv_table* t) {
   cudaError_t e = cudaSuccess;
-  if (!t->one) e = cudaMalloc((void**)&t->one, sizeof(OneResult));
+  if (!t->one && !(e = cudaMalloc((void**)&t->one, sizeof(OneResult)))) e = cudaMemset(t->one, 0, sizeof(OneResult));
   if (!e && !t->one_val) e = cudaMalloc((void**)&t->one_val, (size_t)t->cfg.value_dim * 4);
   return e ? cuda_fail(e, "single-key staging") : HKV_OK;
 }
