@@ -747,6 +747,25 @@ def _paper_context(breakdown, dim):
                                            "ratio_to_best": round(b["insert_or_assign_bkvs"] / 2.13, 2)}}
 
 
+def _c5_model(world, dim, peer, find_ms, B):
+    """sharded find is bounded per GPU by min(HBM, NVLink).
+    HBM: 145 + 8 dim bytes per find hit (8(d)) at the measured copy peak.
+    NVLink (900 GB/s per direction): the (G-1)/G share of keys owned
+    elsewhere moves, per key, key + row + found flag when routed (8 + 4 dim +
+    1), or digest line + key sector + row when read over peer memory (128 +
+    32 + 4 dim)."""
+    peak, _ = load_peak()
+    hbm = peak * 1e9 / bytes_find_hit(dim) / 1e9
+    per_key = (128 + 32 + 4 * dim) if peer else (8 + 4 * dim + 1)
+    remote = (world - 1) / world
+    nvl = float("inf") if remote == 0 else 900e9 / (remote * per_key) / 1e9
+    model = world * min(hbm, nvl)
+    achieved = world * B / (find_ms / 1e3) / 1e9
+    return {"per_gpu_hbm_bkvs": round(hbm, 3), "per_gpu_nvlink_bkvs": None if nvl == float("inf") else round(nvl, 3),
+            "aggregate_model_bkvs": round(model, 3), "frac_of_model": round(achieved / model, 4),
+            "nvlink_bytes_per_remote_key": per_key}
+
+
 def run_sharded(a, rank, world):
     import torch
     import torch.distributed as dist
@@ -876,6 +895,7 @@ def run_sharded(a, rank, world):
                            "timing": "CUDA events per op on each rank (host-synchronising split exchange "
                                      "included), mean over steps, max over ranks"},
                 "find_bkvs_aggregate": round(world * B / (find_ms.item() / 1e3) / 1e9, 4),
+                "find_model": _c5_model(world, dim, peer, find_ms.item(), B),
                 "clocks": clk, "gpu_launches": int(launches), "e2e": e2e}
         print(json.dumps(line), flush=True)
 

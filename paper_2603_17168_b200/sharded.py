@@ -12,10 +12,12 @@ the CPU oracle at the global capacity checks it bit-exactly.
 
 Global batch order is rank-major (rank 0's batch, then rank 1's, ...).  Each
 op travels to its owner in one all-to-all (keys + values + scores + explicit
-LRU ticks = clock + global index + 1); a shard receives the segments in source
-rank order, each in source batch order, so applying them in received order is
-the global serial order restricted to the shard.  Results return in a second
-all-to-all and are scattered back through the inverse routing permutation.
+LRU ticks = clock + global index + 1, packed into one int32 row per op); a
+shard receives the segments in source rank order, each in source batch order,
+so applying them in received order is the global serial order restricted to
+the shard.  Results return in a second all-to-all and are scattered back
+through the inverse routing permutation.  The split sizes and every rank's
+batch size travel in one all_gather: one host synchronisation per op.
 Every rank advances its clock by the global batch size, so all shards share
 one logical clock.  size() is an all-reduce.
 
@@ -73,8 +75,53 @@ class ShardedCacheTable:
         self.local = (local_factory or CacheTable)(local_cfg)
         self.router = router or cuda_router
         self.clock = 0  # the global logical clock; every rank holds the same value
+        self._fence_t = None
 
     # ----- exchange plumbing ----------------------------------------------------
+    # One host synchronisation per op: the routing counts of every rank and
+    # every rank's batch size travel in ONE all_gather (the all-to-all split
+    # sizes must be host integers); the op's columns (key, tick, score, value
+    # row ...) travel packed as int32 words in ONE all_to_all each way.
+    def _plan(self, keys: torch.Tensor):
+        """-> perm (routed order), send splits, recv splits, batch sizes of every rank."""
+        perm, counts = self.router(keys, self.global_buckets, self.world)
+        meta = torch.cat([counts.to(torch.int64),
+                          torch.tensor([keys.numel()], dtype=torch.int64, device=counts.device)])
+        allm = torch.empty(self.world * (self.world + 1), dtype=torch.int64, device=meta.device)
+        dist.all_gather_into_tensor(allm, meta, group=self.group)
+        m = allm.view(self.world, self.world + 1).tolist()  # the op's one host sync
+        send = m[self.rank][: self.world]
+        recv = [m[q][self.rank] for q in range(self.world)]
+        sizes = [m[q][self.world] for q in range(self.world)]
+        return perm, send, recv, sizes
+
+    @staticmethod
+    def _words(x: torch.Tensor) -> torch.Tensor:
+        """(n, k) int32 view of a 1-D 64-bit / 8-bit-bool / 2-D 32-bit column."""
+        n = x.shape[0]
+        if x.numel() == 0:
+            per = x.element_size() // 4 if x.element_size() >= 4 else 1
+            k = per * (x.shape[1] if x.dim() == 2 else 1)
+            return torch.empty((n, k), dtype=torch.int32, device=x.device)
+        if x.dtype in (torch.int64, torch.uint64, torch.float64):
+            return x.contiguous().view(torch.int32).view(n, -1)
+        if x.dtype in (torch.bool, torch.uint8):
+            return x.to(torch.int32).view(n, 1)
+        return x.contiguous().view(torch.int32).view(n, -1)
+
+    def _a2a_packed(self, cols, send, recv):
+        """Pack columns into (n, W) int32 rows, exchange them in one
+        all_to_all, return the received (m, W) block."""
+        x = torch.cat([self._words(c) for c in cols], dim=1) if len(cols) > 1 else self._words(cols[0])
+        w = x.shape[1]
+        out = torch.empty((sum(recv), w), dtype=torch.int32, device=x.device)
+        dist.all_to_all_single(out, x.contiguous(), recv, send, group=self.group)
+        return out
+
+    @staticmethod
+    def _col64(block, a):
+        return block[:, a:a + 2].contiguous().view(torch.int64).view(-1)
+
     def _splits(self, counts: torch.Tensor):
         recv = torch.empty_like(counts)
         dist.all_to_all_single(recv, counts, group=self.group)
@@ -85,26 +132,22 @@ class ShardedCacheTable:
         dist.all_to_all_single(out, x.contiguous(), recv_splits, send_splits, group=self.group)
         return out
 
-    def _route(self, keys: torch.Tensor):
-        perm, counts = self.router(keys, self.global_buckets, self.world)
-        send, recv = self._splits(counts)
-        return perm, send, recv
-
     def _unpermute(self, routed_back: torch.Tensor, perm: torch.Tensor):
         out = torch.empty_like(routed_back)
         out[perm] = routed_back
         return out
 
-    def _global_offsets(self, n: int, device):
-        t = torch.tensor([n], dtype=torch.int64, device=device)
-        allv = [torch.empty_like(t) for _ in range(self.world)]
-        dist.all_gather(allv, t, group=self.group)
-        sizes = [int(x.item()) for x in allv]
-        return sum(sizes[: self.rank]), sum(sizes)
-
     @staticmethod
     def _u8(x: torch.Tensor):
         return x.to(torch.uint8) if x.dtype == torch.bool else x
+
+    def _fence(self):
+        """Stream-ordered barrier: a one-element all_reduce on the compute
+        stream.  No rank's kernels after it start before every rank's kernels
+        before it finished (no host synchronisation with NCCL)."""
+        if self._fence_t is None or self._fence_t.device != self.local.device:
+            self._fence_t = torch.zeros(1, dtype=torch.int32, device=getattr(self.local, "device", "cpu"))
+        dist.all_reduce(self._fence_t, group=self.group)
 
     # ----- reader ops -----------------------------------------------------------
     def enable_peer_find(self):
@@ -126,20 +169,24 @@ class ShardedCacheTable:
 
     def find(self, keys: torch.Tensor):
         if getattr(self, "_peer", False):
-            # every rank is in the find phase (no shard mutates while peers read it)
-            dist.barrier(group=self.group)
+            # every shard's previous mutations are complete before any rank
+            # reads it, and no rank mutates its shard before every peer read
+            # finished: two stream-ordered fences, no host barrier
+            self._fence()
             f, v = self.local._find_peer(keys)
-            dist.barrier(group=self.group)
+            self._fence()
             return f, v
-        perm, send, recv = self._route(keys)
+        perm, send, recv, _ = self._plan(keys)
         rk = self._a2a(keys[perm], send, recv)
         f, v = self.local.find(rk)
-        fb = self._a2a(self._u8(f), recv, send)
-        vb = self._a2a(v, recv, send)
-        return self._unpermute(fb, perm).bool(), self._unpermute(vb, perm)
+        back = self._a2a_packed([v, f], recv, send)  # value rows + found flag, one exchange
+        d = self.config.value_dim
+        vb = back[:, :d].contiguous().view(torch.float32)
+        fb = back[:, d] != 0
+        return self._unpermute(fb, perm), self._unpermute(vb, perm)
 
     def contains(self, keys: torch.Tensor):
-        perm, send, recv = self._route(keys)
+        perm, send, recv, _ = self._plan(keys)
         rk = self._a2a(keys[perm], send, recv)
         f = self.local.contains(rk)
         return self._unpermute(self._a2a(self._u8(f), recv, send), perm).bool()
@@ -154,40 +201,41 @@ class ShardedCacheTable:
         return self.size() / self.config.capacity
 
     # ----- inserter ops ---------------------------------------------------------
-    def _ticks(self, n: int, device):
-        off, total = self._global_offsets(n, device)
-        ticks = torch.arange(n, dtype=torch.int64, device=device) + (self.clock + off + 1)
-        return ticks, total
-
     def _upsert(self, op: str, keys, values, scores):
         n = keys.numel()
-        ticks, total = self._ticks(n, keys.device)
-        perm, send, recv = self._route(keys)
-        rk = self._a2a(keys[perm], send, recv)
-        rv = self._a2a(values[perm], send, recv)
-        rs = None if scores is None else self._a2a(scores[perm], send, recv)
-        rt = self._a2a(ticks[perm], send, recv)
+        perm, send, recv, sizes = self._plan(keys)
+        off, total = sum(sizes[: self.rank]), sum(sizes)
+        ticks = torch.arange(n, dtype=torch.int64, device=keys.device) + (self.clock + off + 1)
+        d = self.config.value_dim
+        cols = [keys[perm].view(torch.int64), ticks[perm], values[perm]]
+        if scores is not None:
+            cols.append(scores[perm].view(torch.int64))
+        blk = self._a2a_packed(cols, send, recv)
+        rk = self._col64(blk, 0)
+        rt = self._col64(blk, 2)
+        rv = blk[:, 4:4 + d].contiguous().view(torch.float32)
+        rs = self._col64(blk, 4 + d) if scores is not None else None
         res = None
         if op == "insert_or_assign":
             o = self.local.insert_or_assign(rk, rv, rs, ticks=rt, clock_advance=total)
+            ob = self._a2a(o, recv, send)
         elif op == "find_or_insert":
             o = self.local.find_or_insert(rk, rv, rs, ticks=rt, clock_advance=total)
-            vb = self._a2a(rv, recv, send)
-            values[perm] = vb
+            back = self._a2a_packed([rv, o], recv, send)  # rows read back + outcomes, one exchange
+            values[perm] = back[:, :d].contiguous().view(torch.float32)
+            ob = back[:, d].to(torch.uint8)
         else:  # insert_and_evict
             o, ek, ev, es = self.local.insert_and_evict(rk, rv, rs, ticks=rt, clock_advance=total)
+            ob = self._a2a(o, recv, send)
             # evicted tuples per source rank, in received (= source batch) order
             is_ev = (o == _EVICTED)
             seg = torch.repeat_interleave(torch.arange(self.world, device=o.device),
                                           torch.tensor(recv, device=o.device), output_size=o.numel())
             ev_send = torch.bincount(seg[is_ev], minlength=self.world).to(torch.int64)
             es_split, er_split = self._splits(ev_send)
-            bk = self._a2a(ek.view(torch.int64), es_split, er_split)
-            bv = self._a2a(ev, es_split, er_split)
-            bs = self._a2a(es.view(torch.int64), es_split, er_split)
-            res = (bk, bv, bs)
+            back = self._a2a_packed([ek.view(torch.int64), es.view(torch.int64), ev], es_split, er_split)
+            res = (self._col64(back, 0), back[:, 4:].contiguous().view(torch.float32), self._col64(back, 2))
         self.clock += total
-        ob = self._a2a(o, recv, send)
         outcomes = self._unpermute(ob, perm)
         if res is None:
             return outcomes
@@ -207,26 +255,26 @@ class ShardedCacheTable:
         return self._upsert("find_or_insert", keys, values_inout, scores)
 
     def erase(self, keys):
-        perm, send, recv = self._route(keys)
+        perm, send, recv, _ = self._plan(keys)
         rk = self._a2a(keys[perm], send, recv)
         o = self.local.erase(rk)
         return self._unpermute(self._a2a(o, recv, send), perm)
 
     # ----- updater ops ----------------------------------------------------------
     def assign(self, keys, values):
-        perm, send, recv = self._route(keys)
-        rk = self._a2a(keys[perm], send, recv)
-        rv = self._a2a(values[perm], send, recv)
-        o = self.local.assign(rk, rv)
+        perm, send, recv, _ = self._plan(keys)
+        d = self.config.value_dim
+        blk = self._a2a_packed([keys[perm].view(torch.int64), values[perm]], send, recv)
+        o = self.local.assign(self._col64(blk, 0), blk[:, 2:2 + d].contiguous().view(torch.float32))
         return self._unpermute(self._a2a(o, recv, send), perm)
 
     def assign_scores(self, keys, scores=None):
-        perm, send, recv = self._route(keys)
-        rk = self._a2a(keys[perm], send, recv)
+        perm, send, recv, _ = self._plan(keys)
         if scores is not None:
-            rs = self._a2a(scores[perm], send, recv)
-            o = self.local.assign_scores(rk, rs)
+            blk = self._a2a_packed([keys[perm].view(torch.int64), scores[perm].view(torch.int64)], send, recv)
+            o = self.local.assign_scores(self._col64(blk, 0), self._col64(blk, 2))
             return self._unpermute(self._a2a(o, recv, send), perm)
+        rk = self._a2a(keys[perm], send, recv)
         # refresh: ticks follow the GLOBAL found order (table.py:481-483)
         f = self._unpermute(self._a2a(self._u8(self.local.contains(rk)), recv, send), perm).bool()
         nf = int(f.sum().item())
@@ -237,6 +285,13 @@ class ShardedCacheTable:
         o = self.local.assign_scores(rk, None, ticks=rt, clock_advance=total)
         self.clock += total
         return self._unpermute(self._a2a(o, recv, send), perm)
+
+    def _global_offsets(self, n: int, device):
+        t = torch.tensor([n], dtype=torch.int64, device=device)
+        allv = torch.empty(self.world, dtype=torch.int64, device=device)
+        dist.all_gather_into_tensor(allv, t, group=self.group)
+        sizes = allv.tolist()
+        return sum(sizes[: self.rank]), sum(sizes)
 
     # ----- export (global rows are rank-major) ----------------------------------
     def export_batch_if(self, min_score, cursor, max_count: int):
