@@ -296,6 +296,19 @@ int hkv_check_consistency(hkv_table *t, int32_t *ok, hkv_stream stream);
 int hkv_route(const uint64_t *keys, int64_t n, int64_t global_buckets, int32_t world,
               int32_t *perm, int64_t *counts, hkv_stream stream);
 
+/* Routed exchange helpers of the sharded table (device pointers, async on
+ * `stream`; 0 ok, 1 bad arguments, 2 CUDA error):
+ *   hkv_route_gather  for routed position j (source op i = perm[j]):
+ *                     meta[j] = {key, tick_base + i + 1[, score]} (3 words
+ *                     when scores != NULL) and out_values row j = values row i
+ *   hkv_scatter_rows  dst[perm[j]] = src[j] for rows of row_bytes (1, or a
+ *                     multiple of 4): results back into batch order */
+int hkv_route_gather(const int32_t *perm, int64_t n, const uint64_t *keys, const uint64_t *scores,
+                     const float *values, int64_t dim, uint64_t tick_base, uint64_t *meta, float *out_values,
+                     hkv_stream stream);
+int hkv_scatter_rows(const int32_t *perm, int64_t n, const void *src, void *dst, int64_t row_bytes,
+                     hkv_stream stream);
+
 /* Launch-count instrumentation: number of kernels this library has launched. */
 int64_t hkv_launch_count(void);
 

@@ -77,6 +77,8 @@ SIGNATURES = {
     "hkv_restore": (C.c_int, [_vp, _vp]),
     "hkv_check_consistency": (C.c_int, [_vp, C.POINTER(_i32), _vp]),
     "hkv_route": (C.c_int, [_vp, _i64, _i64, _i32, _vp, _vp, _vp]),
+    "hkv_route_gather": (C.c_int, [_vp, _i64, _vp, _vp, _vp, _i64, _u64, _vp, _vp, _vp]),
+    "hkv_scatter_rows": (C.c_int, [_vp, _i64, _vp, _vp, _i64, _vp]),
     "hkv_set_kernel_timing": (C.c_int, [_i32]),
     "hkv_gate_create": (C.c_int, [C.POINTER(_vp)]),
     "hkv_gate_destroy": (C.c_int, [_vp]),

@@ -213,3 +213,91 @@ cudaError_t run_route(const uint64_t* keys, int64_t n, int64_t global_buckets, i
 }
 
 }  // namespace hkv
+
+namespace hkv {
+
+// ---- routed exchange helpers of the sharded table (sharded.py) -----------
+// k_route_gather: the routed order's send columns in one pass -- per op j
+// (source index i = perm[j]): meta[j] = (key, tick = tick_base + i + 1
+// [, score]) and the value row; rows are moved by 8-lane tiles with 16-B
+// vectors (coalesced writes, one random row read per op).
+template <int VEC>
+__global__ void __launch_bounds__(256) k_route_gather(const int32_t* __restrict__ perm, int64_t n,
+                                                      const uint64_t* __restrict__ keys,
+                                                      const uint64_t* __restrict__ scores,
+                                                      const float* __restrict__ values, int dim,
+                                                      uint64_t tick_base, int meta_w, uint64_t* __restrict__ meta,
+                                                      float* __restrict__ out_values) {
+  const int r = threadIdx.x & 7;
+  const int64_t tiles = (int64_t)gridDim.x * (blockDim.x / 8);
+  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x / 8) + threadIdx.x / 8; j < n; j += tiles) {
+    const int64_t i = perm[j];
+    if (r == 0) {
+      meta[j * meta_w] = keys[i];
+      meta[j * meta_w + 1] = tick_base + (uint64_t)i + 1;
+      if (meta_w > 2) meta[j * meta_w + 2] = scores[i];
+    }
+    if (values) copy_row<8, VEC>(out_values + (uint64_t)j * dim, values + (uint64_t)i * dim, dim, r);
+  }
+}
+
+// k_scatter_rows: dst[perm[j]] = src[j] for rows of `row_bytes` (a multiple
+// of 4): the inverse routing permutation of returned results.
+__global__ void __launch_bounds__(256) k_scatter_rows(const int32_t* __restrict__ perm, int64_t n,
+                                                      const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                                                      int words) {
+  const int64_t total = n * words;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = x / words;
+    const int w = (int)(x - j * words);
+    dst[(int64_t)perm[j] * words + w] = src[x];
+  }
+}
+__global__ void __launch_bounds__(256) k_scatter_bytes(const int32_t* __restrict__ perm, int64_t n,
+                                                       const uint8_t* __restrict__ src, uint8_t* __restrict__ dst) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    dst[perm[j]] = src[j];
+}
+
+}  // namespace hkv
+
+extern "C" int hkv_route_gather(const int32_t* perm, int64_t n, const uint64_t* keys, const uint64_t* scores,
+                                const float* values, int64_t dim, uint64_t tick_base, uint64_t* meta,
+                                float* out_values, void* stream) {
+  using namespace hkv;
+  if (n < 0 || dim < 1) return 1;
+  if (n == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int meta_w = scores ? 3 : 2;
+  const bool v4 = dim % 4 == 0 && ((uintptr_t)values % 16 == 0) && ((uintptr_t)out_values % 16 == 0);
+  int64_t blocks = (n * 8 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (v4)
+    k_route_gather<4><<<(unsigned)blocks, 256, 0, s>>>(perm, n, keys, scores, values, (int)dim, tick_base, meta_w,
+                                                       meta, out_values);
+  else
+    k_route_gather<1><<<(unsigned)blocks, 256, 0, s>>>(perm, n, keys, scores, values, (int)dim, tick_base, meta_w,
+                                                       meta, out_values);
+  g_launches++;
+  return cudaGetLastError() ? 2 : 0;
+}
+
+extern "C" int hkv_scatter_rows(const int32_t* perm, int64_t n, const void* src, void* dst, int64_t row_bytes,
+                                void* stream) {
+  using namespace hkv;
+  if (n < 0 || row_bytes < 1 || (row_bytes != 1 && row_bytes % 4)) return 1;
+  if (n == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (row_bytes == 1) {
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_scatter_bytes<<<(unsigned)blocks, 256, 0, s>>>(perm, n, (const uint8_t*)src, (uint8_t*)dst);
+  } else {
+    const int words = (int)(row_bytes / 4);
+    int64_t blocks = (n * words + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    k_scatter_rows<<<(unsigned)blocks, 256, 0, s>>>(perm, n, (const uint32_t*)src, (uint32_t*)dst, words);
+  }
+  g_launches++;
+  return cudaGetLastError() ? 2 : 0;
+}

@@ -52,7 +52,7 @@ def cuda_router(keys: torch.Tensor, global_buckets: int, world: int):
     _lib.check(lib.hkv_route(C.c_void_p(keys.data_ptr()), n, global_buckets, world, C.c_void_p(perm.data_ptr()),
                              C.c_void_p(counts.data_ptr()),
                              C.c_void_p(torch.cuda.current_stream(keys.device).cuda_stream)))
-    return perm.long(), counts
+    return perm, counts
 
 
 class ShardedCacheTable:
@@ -122,6 +122,52 @@ class ShardedCacheTable:
     def _col64(block, a):
         return block[:, a:a + 2].contiguous().view(torch.int64).view(-1)
 
+    def _sp(self, t: torch.Tensor):
+        return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+    def _gather_send(self, perm, keys, values, scores, tick_base):
+        """Routed-order send columns in one pass: meta rows (key, tick
+        [, score]) as int64 and the value rows (hkv_route_gather on the
+        device; torch indexing for the CPU tensors of the host-logic tests)."""
+        n = keys.numel()
+        w = 3 if scores is not None else 2
+        d = self.config.value_dim
+        if keys.is_cuda:
+            from . import _lib
+
+            p32 = perm if perm.dtype == torch.int32 else perm.to(torch.int32)
+            meta = torch.empty((n, w), dtype=torch.int64, device=keys.device)
+            vrows = torch.empty((n, d), dtype=torch.float32, device=keys.device) if values is not None else None
+            rc = _lib.load().hkv_route_gather(
+                C.c_void_p(p32.data_ptr()), n, C.c_void_p(keys.data_ptr()),
+                None if scores is None else C.c_void_p(scores.contiguous().data_ptr()),
+                None if values is None else C.c_void_p(values.contiguous().data_ptr()), d,
+                int(tick_base) & 0xFFFFFFFFFFFFFFFF, C.c_void_p(meta.data_ptr()),
+                None if vrows is None else C.c_void_p(vrows.data_ptr()), self._sp(keys))
+            if rc:
+                raise RuntimeError("hkv_route_gather failed")
+            return meta, vrows
+        cols = [keys[perm].view(torch.int64), perm.to(torch.int64) + (tick_base + 1)]
+        if scores is not None:
+            cols.append(scores[perm].view(torch.int64))
+        return torch.stack(cols, dim=1), (values[perm] if values is not None else None)
+
+    def _scatter_back(self, routed: torch.Tensor, perm: torch.Tensor):
+        """out[perm[j]] = routed[j] (hkv_scatter_rows on the device)."""
+        if not routed.is_cuda:
+            return self._unpermute(routed, perm)
+        from . import _lib
+
+        out = torch.empty_like(routed)
+        n = routed.shape[0]
+        rb = routed.element_size() * (routed[0].numel() if n else 1)
+        p32 = perm if perm.dtype == torch.int32 else perm.to(torch.int32)
+        rc = _lib.load().hkv_scatter_rows(C.c_void_p(p32.data_ptr()), n, C.c_void_p(routed.contiguous().data_ptr()),
+                                          C.c_void_p(out.data_ptr()), rb, self._sp(routed))
+        if rc:
+            raise RuntimeError("hkv_scatter_rows failed")
+        return out
+
     def _splits(self, counts: torch.Tensor):
         recv = torch.empty_like(counts)
         dist.all_to_all_single(recv, counts, group=self.group)
@@ -176,16 +222,18 @@ class ShardedCacheTable:
             f, v = self.local._find_peer(keys)
             self._fence()
             return f, v
+        if self.world == 1:  # one shard: nothing to route
+            return self.local.find(keys)
         perm, send, recv, _ = self._plan(keys)
         rk = self._a2a(keys[perm], send, recv)
         f, v = self.local.find(rk)
-        back = self._a2a_packed([v, f], recv, send)  # value rows + found flag, one exchange
-        d = self.config.value_dim
-        vb = back[:, :d].contiguous().view(torch.float32)
-        fb = back[:, d] != 0
-        return self._unpermute(fb, perm), self._unpermute(vb, perm)
+        vb = self._a2a(v, recv, send)
+        fb = self._a2a(self._u8(f), recv, send)
+        return self._scatter_back(fb, perm).bool(), self._scatter_back(vb, perm)
 
     def contains(self, keys: torch.Tensor):
+        if self.world == 1:
+            return self.local.contains(keys)
         perm, send, recv, _ = self._plan(keys)
         rk = self._a2a(keys[perm], send, recv)
         f = self.local.contains(rk)
@@ -203,27 +251,32 @@ class ShardedCacheTable:
     # ----- inserter ops ---------------------------------------------------------
     def _upsert(self, op: str, keys, values, scores):
         n = keys.numel()
+        if self.world == 1:
+            # one shard holds every bucket: the local op with the global ticks
+            ticks = torch.arange(n, dtype=torch.int64, device=keys.device) + (self.clock + 1)
+            fn = getattr(self.local, op)
+            r = fn(keys, values, scores, ticks=ticks, clock_advance=n)
+            self.clock += n
+            return r
         perm, send, recv, sizes = self._plan(keys)
         off, total = sum(sizes[: self.rank]), sum(sizes)
-        ticks = torch.arange(n, dtype=torch.int64, device=keys.device) + (self.clock + off + 1)
         d = self.config.value_dim
-        cols = [keys[perm].view(torch.int64), ticks[perm], values[perm]]
-        if scores is not None:
-            cols.append(scores[perm].view(torch.int64))
-        blk = self._a2a_packed(cols, send, recv)
-        rk = self._col64(blk, 0)
-        rt = self._col64(blk, 2)
-        rv = blk[:, 4:4 + d].contiguous().view(torch.float32)
-        rs = self._col64(blk, 4 + d) if scores is not None else None
+        meta, vrows = self._gather_send(perm, keys.view(torch.int64), values,
+                                        None if scores is None else scores.view(torch.int64), self.clock + off)
+        # two exchanges: the packed (key, tick[, score]) rows and the value rows
+        rmeta = self._a2a(meta, send, recv)
+        rv = self._a2a(vrows, send, recv)
+        rk = rmeta[:, 0].contiguous()
+        rt = rmeta[:, 1].contiguous()
+        rs = rmeta[:, 2].contiguous() if scores is not None else None
         res = None
         if op == "insert_or_assign":
             o = self.local.insert_or_assign(rk, rv, rs, ticks=rt, clock_advance=total)
             ob = self._a2a(o, recv, send)
         elif op == "find_or_insert":
             o = self.local.find_or_insert(rk, rv, rs, ticks=rt, clock_advance=total)
-            back = self._a2a_packed([rv, o], recv, send)  # rows read back + outcomes, one exchange
-            values[perm] = back[:, :d].contiguous().view(torch.float32)
-            ob = back[:, d].to(torch.uint8)
+            ob = self._a2a(o, recv, send)
+            values.copy_(self._scatter_back(self._a2a(rv, recv, send), perm))
         else:  # insert_and_evict
             o, ek, ev, es = self.local.insert_and_evict(rk, rv, rs, ticks=rt, clock_advance=total)
             ob = self._a2a(o, recv, send)
@@ -236,7 +289,7 @@ class ShardedCacheTable:
             back = self._a2a_packed([ek.view(torch.int64), es.view(torch.int64), ev], es_split, er_split)
             res = (self._col64(back, 0), back[:, 4:].contiguous().view(torch.float32), self._col64(back, 2))
         self.clock += total
-        outcomes = self._unpermute(ob, perm)
+        outcomes = self._scatter_back(ob, perm)
         if res is None:
             return outcomes
         # entries arrive grouped by shard in routed order; restore batch order
@@ -255,6 +308,8 @@ class ShardedCacheTable:
         return self._upsert("find_or_insert", keys, values_inout, scores)
 
     def erase(self, keys):
+        if self.world == 1:
+            return self.local.erase(keys)
         perm, send, recv, _ = self._plan(keys)
         rk = self._a2a(keys[perm], send, recv)
         o = self.local.erase(rk)
@@ -262,13 +317,21 @@ class ShardedCacheTable:
 
     # ----- updater ops ----------------------------------------------------------
     def assign(self, keys, values):
+        if self.world == 1:
+            return self.local.assign(keys, values)
         perm, send, recv, _ = self._plan(keys)
-        d = self.config.value_dim
-        blk = self._a2a_packed([keys[perm].view(torch.int64), values[perm]], send, recv)
-        o = self.local.assign(self._col64(blk, 0), blk[:, 2:2 + d].contiguous().view(torch.float32))
-        return self._unpermute(self._a2a(o, recv, send), perm)
+        meta, vrows = self._gather_send(perm, keys.view(torch.int64), values, None, 0)
+        rk = self._a2a(meta, send, recv)[:, 0].contiguous()
+        o = self.local.assign(rk, self._a2a(vrows, send, recv))
+        return self._scatter_back(self._a2a(o, recv, send), perm)
 
     def assign_scores(self, keys, scores=None):
+        if self.world == 1:
+            if scores is not None:
+                return self.local.assign_scores(keys, scores)
+            o = self.local.assign_scores(keys)
+            self.clock += int((o == _UPDATED).sum().item())
+            return o
         perm, send, recv, _ = self._plan(keys)
         if scores is not None:
             blk = self._a2a_packed([keys[perm].view(torch.int64), scores[perm].view(torch.int64)], send, recv)

@@ -158,3 +158,34 @@ def test_peer_find_ipc_two_processes():
         p.join(300)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert list(ret) == [1, 1]
+
+
+@pytest.mark.parametrize("dim,custom", [(64, False), (7, True), (128, True)])
+def test_route_gather_and_scatter_kernels(dim, custom):
+    """hkv_route_gather / hkv_scatter_rows (the routed exchange's device
+    passes) equal torch indexing."""
+    import types
+
+    from paper_2603_17168_b200.sharded import ShardedCacheTable
+
+    torch.cuda.set_device(0)
+    n = 100_003
+    g = torch.Generator(device="cuda").manual_seed(1)
+    keys = torch.randint(1, 2**62, (n,), device="cuda", generator=g)
+    vals = torch.randn((n, dim), device="cuda", generator=g)
+    sc = torch.randint(0, 2**40, (n,), device="cuda", generator=g) if custom else None
+    perm = torch.randperm(n, device="cuda", generator=g).to(torch.int32)
+    fake = types.SimpleNamespace(config=types.SimpleNamespace(value_dim=dim))
+    fake._sp = lambda t: ShardedCacheTable._sp(fake, t)
+    meta, rows = ShardedCacheTable._gather_send(fake, perm, keys, vals, sc, 1000)
+    p = perm.long()
+    assert torch.equal(meta[:, 0], keys[p]) and torch.equal(meta[:, 1], p + 1001)
+    if custom:
+        assert torch.equal(meta[:, 2], sc[p])
+    assert torch.equal(rows, vals[p])
+    fake._unpermute = ShardedCacheTable._unpermute
+    back = ShardedCacheTable._scatter_back(fake, rows, perm)
+    assert torch.equal(back, vals)
+    flags = (torch.arange(n, device="cuda") % 3 == 0).to(torch.uint8)
+    fb = ShardedCacheTable._scatter_back(fake, flags[p], perm)
+    assert torch.equal(fb, flags)
