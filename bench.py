@@ -448,6 +448,17 @@ def run_extras(a, tables, torch, hkv, W):
     ex["c4_assign"] = _rec(ms, B, {"gbs_pcie": round(B * 512 / ms / 1e6, 1)})
     del t
     torch.cuda.empty_cache()
+    # the paper's hybrid point is dim 64: same table shape, 256-B rows
+    t = hkv.CacheTable(hkv.TableConfig(capacity=c4cap, value_dim=64, fast_tier_budget=0))
+    t.validate_keys = False
+    _fill(t, 0.5, c4cap, 64, B, torch, W)
+    res = torch.from_numpy(t.occupied_keys().view(np.int64)).cuda()
+    hits = res[torch.randint(0, res.numel(), (B,), device="cuda", generator=gen)]
+    del res
+    ms, o = _timed(torch, lambda r: t.find(hits), reps)
+    ex["c4_dim64_find"] = _rec(ms, B, {"gbs_pcie": round(B * 256 / ms / 1e6, 1), "paper_h100_nvl_bkvs": 0.172})
+    del t
+    torch.cuda.empty_cache()
     return ex
 
 def run_single(a):

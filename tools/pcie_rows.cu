@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
+#include <cstring>
+#include <sys/mman.h>
 
 constexpr int kRowBytes = 512;
 constexpr int kRowsPerWarp = 8;  // bulk path: rows in flight per warp
@@ -72,11 +74,25 @@ __global__ void k_bulk(const uint4* __restrict__ src, const uint32_t* __restrict
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
   const int64_t nrows_tab = (int64_t)1 << 26;  // 32 GiB of 512-B rows
   const int64_t n = 1 << 20;
   void* host = nullptr;
-  if (cudaHostAlloc(&host, nrows_tab * kRowBytes, cudaHostAllocMapped)) { printf("alloc failed\n"); return 1; }
+  // argv[1] == "thp": anonymous mmap backed by 2-MB transparent huge pages,
+  // registered mapped (cudaHostRegister) instead of cudaHostAlloc's 4-KB pages
+  const bool thp = argc > 1 && !strcmp(argv[1], "thp");
+  if (thp) {
+    const size_t bytes = (size_t)nrows_tab * kRowBytes;
+    host = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (host == MAP_FAILED) { printf("mmap failed\n"); return 1; }
+    int rc = madvise(host, bytes, MADV_HUGEPAGE);
+    memset(host, 0, bytes);
+    cudaError_t e = cudaHostRegister(host, bytes, cudaHostRegisterMapped);
+    printf("thp arena: madvise rc %d, cudaHostRegister %s\n", rc, cudaGetErrorString(e));
+  } else if (cudaHostAlloc(&host, nrows_tab * kRowBytes, cudaHostAllocMapped)) {
+    printf("alloc failed\n");
+    return 1;
+  }
   uint4* dsrc;
   cudaHostGetDevicePointer((void**)&dsrc, host, 0);
   uint32_t* hrows = (uint32_t*)malloc(n * 4);
