@@ -21,8 +21,15 @@ batch size travel in one all_gather: one host synchronisation per op.
 Every rank advances its clock by the global batch size, so all shards share
 one logical clock.  size() is an all-reduce.
 
-Dual mode is not sharded (a key's two buckets may live on different ranks):
-run dual-mode tables as per-GPU replicas.
+Dual mode: keys route by the owner of their FIRST
+bucket, and each shard is a dual-mode table of capacity / G whose second
+bucket is drawn inside the shard (second_hash(h) & (B_local - 1)).  The
+sharded dual table is therefore exactly G independent reference dual tables,
+each fed its routed sub-batch in global order (checked shard by shard
+against the oracle); it differs from ONE global dual table only in where a
+key's second candidate may live -- a global second bucket on another GPU
+would need a cross-GPU two-bucket critical section per op.  Dual shards use
+the routed find (the peer find probes single-mode shards).
 """
 
 from __future__ import annotations
@@ -58,8 +65,6 @@ def cuda_router(keys: torch.Tensor, global_buckets: int, world: int):
 class ShardedCacheTable:
     def __init__(self, config: TableConfig, group=None, local_factory: Optional[Callable] = None,
                  router: Optional[Callable] = None):
-        if config.mode is not Mode.single:
-            raise ValueError("sharded tables support single mode only (dual mode: per-GPU replicas)")
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)

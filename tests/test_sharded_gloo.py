@@ -26,7 +26,8 @@ class OracleShard:
 
     def __init__(self, cfg):
         self.config = cfg
-        self.t = OracleTable(cfg.capacity, cfg.value_dim, "single", cfg.score_policy.value, cfg.fast_tier_budget)
+        self.t = OracleTable(cfg.capacity, cfg.value_dim, cfg.mode.value, cfg.score_policy.value,
+                             cfg.fast_tier_budget)
         self.device = torch.device("cpu")
 
     @staticmethod
@@ -198,6 +199,71 @@ def test_sharded_table_equals_global_table(policy):
     results = mgr.dict()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, port, policy, results)) for r in range(WORLD)]
+    [p.start() for p in procs]
+    [p.join(240) for p in procs]
+    for p in procs:
+        if p.is_alive():
+            p.kill()
+    for r in range(WORLD):
+        assert results.get(r) == "ok", results.get(r)
+
+
+def _dual_worker(rank, port, policy, results):
+    """Dual-mode sharding: every shard equals an oracle DUAL table of
+    capacity / world fed the rank-major global batch restricted to the keys
+    whose first bucket it owns, with the global ticks."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        import paper_2603_17168_b200 as hkv
+        from paper_2603_17168_b200.sharded import ShardedCacheTable
+
+        cfg = hkv.TableConfig(capacity=CAP, value_dim=DIM, score_policy=policy, mode="dual")
+        st = ShardedCacheTable(cfg, local_factory=OracleShard, router=numpy_router)
+        ref = OracleTable(CAP // WORLD, DIM, "dual", policy)  # this shard's reference
+        bl = (CAP // 128) // WORLD
+        clock = 0
+        for step in range(10):
+            bs = _batches(step, policy)
+            gk = np.concatenate([b[0] for b in bs])
+            gv = np.concatenate([b[1] for b in bs])
+            gs = None if policy != "kCustomized" else np.concatenate([b[2] for b in bs])
+            owner = ((fmix64_array(gk) & np.uint64(bl * WORLD - 1)) // np.uint64(bl)).astype(np.int64)
+            mine = np.flatnonzero(owner == rank)
+            ticks = (clock + 1 + mine).astype(np.uint64)
+            k, v, s = bs[rank]
+            kt = torch.from_numpy(k.view(np.int64))
+            vt = torch.from_numpy(v.copy())
+            stt = None if s is None else torch.from_numpy(s.view(np.int64))
+            st.insert_or_assign(kt, vt, stt)
+            ref.insert_or_assign(gk[mine], gv[mine], None if gs is None else gs[mine], ticks=ticks,
+                                 clock_advance=len(gk))
+            clock += len(gk)
+            f, vv = st.find(kt)
+            off = sum(len(b[0]) for b in bs[:rank])
+            assert f.numpy().sum() > 0 or step == 0
+        loc = st.local.t
+        assert loc.keys.tobytes() == ref.keys.tobytes()
+        assert loc.scores.tobytes() == ref.scores.tobytes()
+        assert loc.values.tobytes() == ref.values.tobytes()
+        assert loc.clock == ref.clock == st.clock
+        results[rank] = "ok"
+    except Exception:
+        import traceback
+
+        results[rank] = traceback.format_exc()
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("policy", ["kLru", "kCustomized"])
+def test_sharded_dual_mode_equals_per_shard_dual_tables(policy):
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    results = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_dual_worker, args=(r, port, policy, results)) for r in range(WORLD)]
     [p.start() for p in procs]
     [p.join(240) for p in procs]
     for p in procs:
