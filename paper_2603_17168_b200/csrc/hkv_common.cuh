@@ -157,6 +157,39 @@ __device__ __forceinline__ uint32_t any16(uint4 w, uint32_t dd) {
          ((e - 0x01010101u) & ~e);
 }
 
+// L2 eviction priority for the small per-op plan arrays (outcomes, value
+// rows, read provenance) that the metadata pass writes at random batch
+// indices while it streams hundreds of MB of bucket lines through L2: with
+// evict_last they stay resident until the value pass reads them, instead of
+// costing a DRAM sector fill and write-back per op.
+#ifndef HKV_L2HINT
+#define HKV_L2HINT 1
+#endif
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t p = 0;
+#if HKV_L2HINT
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#endif
+  return p;
+}
+__device__ __forceinline__ void st_keep(uint32_t* a, uint32_t v, uint64_t pol) {
+#if HKV_L2HINT
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+#else
+  *a = v;
+#endif
+}
+__device__ __forceinline__ void st_keep(int32_t* a, int32_t v, uint64_t pol) {
+  st_keep(reinterpret_cast<uint32_t*>(a), (uint32_t)v, pol);
+}
+__device__ __forceinline__ void st_keep(uint8_t* a, uint8_t v, uint64_t pol) {
+#if HKV_L2HINT
+  asm volatile("st.global.L2::cache_hint.b8 [%0], %1, %2;" ::"l"(a), "r"((uint32_t)v), "l"(pol) : "memory");
+#else
+  *a = v;
+#endif
+}
+
 // Streaming loads/stores for data touched once.
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 r;

@@ -11,8 +11,13 @@ namespace hkv {
 // Per-batch device scalars (zeroed by the launcher before each batch).
 struct Scalars {
   int err;                       // sentinel key seen in this batch
-  unsigned nseg;                 // single-op bucket segments
-  unsigned nmulti;               // multi-op bucket segments
+  union {  // the collector's k_alloc reserves both with one packed 64-bit atomic per block
+    struct {
+      unsigned nseg;             // single-op bucket segments
+      unsigned nmulti;           // multi-op bucket segments
+    };
+    unsigned long long seg_pack;
+  };
   unsigned first_ev;             // lowest batch index with an Evicted outcome
   unsigned npend[2];             // dual-mode pending list sizes (per round parity)
   unsigned has_runs;             // single mode: some op is followed by the same key in its bucket segment
@@ -22,6 +27,16 @@ struct Scalars {
   long long n_sel;               // DeviceSelect count
   unsigned long long fel_cnt;    // k_finalize: inserts before the first eviction (summed over blocks)
   unsigned fel_done;             // k_finalize: blocks finished
+  // collector (hkv_collect.cu): k_alloc hands out both with one packed
+  // 64-bit atomic per block
+  union {
+    struct {
+      unsigned nsegd;            // segment descriptors (touched buckets)
+      unsigned npos;             // sorted positions handed out
+    };
+    unsigned long long alloc_pack;
+  };
+  unsigned nbig;                 // segments of more than 16 ops (both groupings; skew hint)
 };
 
 // Per-stream scratch, grown on demand.
@@ -64,6 +79,11 @@ struct Workspace {
   size_t cub_bytes = 0;
   int64_t cub_for_n = -1;
   Scalars* sc = nullptr;
+  uint32_t* col = nullptr;   // collector: per-bucket op counters / range cursors (zero between calls)
+  uint32_t* segd = nullptr;  // collector: segment descriptors (4 u32 per touched bucket)
+  volatile unsigned* skew_host = nullptr;  // mapped pinned word: segments of > 16 ops in the last batch
+  unsigned* skew_dev = nullptr;            //   (written by k_finalize; read by the next call's path choice)
+  int64_t col_buckets = 0;
 };
 
 struct OpArgs {
@@ -124,6 +144,11 @@ cudaError_t run_route(const uint64_t* keys, int64_t n, int64_t global_buckets, i
 // Live timing of dominant kernels (hkv_set_kernel_timing).
 void ktimer_begin(const char* name, cudaStream_t s, int level = 1);
 void ktimer_end(const char* name, cudaStream_t s, int level = 1);
+
+// sort-free grouping of sparse single-mode batches (hkv_collect.cu)
+bool collect_eligible(int64_t n, int log2_buckets, unsigned last_big_segments);
+cudaError_t run_collect(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, Workspace& ws, cudaStream_t s,
+                        int num_sms, uint8_t fcode);
 
 cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual);
 cudaError_t ws_reserve_dual(Workspace& ws, int64_t n, int log2_buckets);

@@ -1,6 +1,6 @@
 """Warm per-stage device times of the single-mode mutation pipeline on C2.
 
-    python tools/stage_times.py [log2_capacity] [lambdas, e.g. 0.5,1.0] [single|dual]
+    python tools/stage_times.py [log2_capacity] [lambdas, e.g. 0.5,1.0] [single|dual] [ops, e.g. insert_or_assign,find]
 
 Fills a dim-64 table to lambda 0.5 and 1.0, then runs insert_or_assign of
 1M fresh keys (snapshot restored after each), assign of 1M resident keys and
@@ -18,7 +18,7 @@ import paper_2603_17168_b200 as hkv  # noqa: E402
 from paper_2603_17168_b200 import _lib  # noqa: E402
 from paper_2603_17168_b200 import workloads as W  # noqa: E402
 
-STAGES = ["prep", "sort", "segments", "apply", "finalize", "values_write", "assign_apply", "find", "find_gather",
+STAGES = ["prep", "sort", "segments", "count", "alloc", "scatter", "segfin", "big", "apply", "finalize", "values_write", "assign_apply", "find", "find_gather",
           "dual_ranks", "dual_flow"]
 lg = int(sys.argv[1]) if len(sys.argv) > 1 else 27
 cap, dim, B = 2**lg, 64, 2**20
@@ -53,7 +53,8 @@ for lam in [float(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else 
     t.snapshot()
     q = W.uniform_distinct_keys_torch(B, 0, stream_offset=0)
     torch.cuda.synchronize()
-    for op in ("insert_or_assign", "assign", "find"):
+    ops = sys.argv[4].split(",") if len(sys.argv) > 4 else ["insert_or_assign", "assign", "find"]
+    for op in ops:
         for warm in (True, False):
             lib.hkv_set_kernel_timing(0 if warm else 2)
             tot = 0.0
