@@ -173,9 +173,8 @@ struct hkv_table {
   uint64_t epoch = 0;
   unsigned long long dual_epoch = 0;  // dual-mode turn-counter tag (hkv_dual.cu)
   TableDev dev{};
-  uint64_t* keys = nullptr;
+  uint64_t* ks = nullptr;       // [capacity] x {key, score} (hkv_common.cuh)
   uint8_t* digests = nullptr;
-  uint64_t* scores = nullptr;
   uint32_t* bits = nullptr;
   uint64_t* smin = nullptr;     // [B][8] per-16-slot-group score minima (eviction summary)
   uint32_t* svalid = nullptr;   // [B] bit g: smin[b][g] is exact
@@ -190,9 +189,8 @@ struct hkv_table {
   hkv_gate* gate = nullptr;
   unsigned long long* lead = nullptr;
   // metadata snapshot
-  uint64_t* snap_keys = nullptr;
+  uint64_t* snap_ks = nullptr;
   uint8_t* snap_digests = nullptr;
-  uint64_t* snap_scores = nullptr;
   uint32_t* snap_bits = nullptr;
   uint64_t* snap_smin = nullptr;
   uint32_t* snap_svalid = nullptr;
@@ -257,8 +255,8 @@ void free_table(hkv_table* t) {
   if (t->one) cudaFree(t->one);
   if (t->locks) cudaFree(t->locks);
   if (t->one_val) cudaFree(t->one_val);
-  void* dptrs[] = {t->keys, t->digests, t->scores, t->bits, t->smin, t->svalid, t->vfast, t->sc, t->role_word, t->lead,
-                   t->snap_keys, t->snap_digests, t->snap_scores, t->snap_bits, t->snap_smin, t->snap_svalid,
+  void* dptrs[] = {t->ks, t->digests, t->bits, t->smin, t->svalid, t->vfast, t->sc, t->role_word, t->lead,
+                   t->snap_ks, t->snap_digests, t->snap_bits, t->snap_smin, t->snap_svalid,
                    t->snap_sc};
   for (void* p : dptrs)
     if (p) cudaFree(p);
@@ -348,8 +346,8 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
   const uint64_t dim = (uint64_t)c.value_dim;
   const uint64_t over_rows = cap - t->fast_rows;
   cudaError_t e;
-  if ((e = cudaMalloc((void**)&t->keys, cap * 8)) || (e = cudaMalloc((void**)&t->digests, cap)) ||
-      (e = cudaMalloc((void**)&t->scores, cap * 8)) || (e = cudaMalloc((void**)&t->bits, (size_t)bc * 16)) ||
+  if ((e = cudaMalloc((void**)&t->ks, cap * 16)) || (e = cudaMalloc((void**)&t->digests, cap)) ||
+      (e = cudaMalloc((void**)&t->bits, (size_t)bc * 16)) ||
       (e = cudaMalloc((void**)&t->smin, (size_t)bc * 64)) || (e = cudaMalloc((void**)&t->svalid, (size_t)bc * 4)) ||
       (e = cudaMalloc((void**)&t->sc, sizeof(TableScalars))) || (e = cudaMalloc((void**)&t->role_word, 4))) {
     free_table(t);
@@ -382,8 +380,9 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
     return fail(HKV_ENOMEM, "lead array allocation failed");
   }
   // initial state, table.py:143-149 / store.py:36-37
-  if ((e = cudaMemset(t->keys, 0xFF, cap * 8)) || (e = cudaMemset(t->digests, 0, cap)) ||
-      (e = cudaMemset(t->scores, 0, cap * 8)) || (e = cudaMemset(t->bits, 0, (size_t)bc * 16)) ||
+  // keys EMPTY, scores 0: the two halves of every 16-B pair
+  if ((e = cudaMemset2D(t->ks, 16, 0xFF, 8, cap)) || (e = cudaMemset2D(t->ks + 1, 16, 0, 8, cap)) ||
+      (e = cudaMemset(t->digests, 0, cap)) || (e = cudaMemset(t->bits, 0, (size_t)bc * 16)) ||
       (e = cudaMemset(t->smin, 0, (size_t)bc * 64)) || (e = cudaMemset(t->svalid, 0, (size_t)bc * 4)) ||
       (e = cudaMemset(t->sc, 0, sizeof(TableScalars))) || (e = cudaMemset(t->role_word, 0, 4)) ||
       (t->vfast && (e = cudaMemset(t->vfast, 0, t->fast_rows * dim * 4))) ||
@@ -397,9 +396,8 @@ int hkv_create(const hkv_config* cfg, hkv_table** out) {
     return cuda_fail(e, "hkv_create sync");
   }
   TableDev& d = t->dev;
-  d.keys = t->keys;
+  d.ks = t->ks;
   d.digests = t->digests;
-  d.scores = t->scores;
   d.bits = t->bits;
   d.smin = t->smin;
   d.svalid = t->svalid;
@@ -686,7 +684,7 @@ int hkv_ipc_handles(hkv_table* t, void* out, int64_t out_bytes) {
   DeviceGuard _g(t->cfg.device);
   cudaIpcMemHandle_t* h = reinterpret_cast<cudaIpcMemHandle_t*>(out);
   cudaError_t e;
-  if ((e = cudaIpcGetMemHandle(&h[0], t->keys)) || (e = cudaIpcGetMemHandle(&h[1], t->digests)) ||
+  if ((e = cudaIpcGetMemHandle(&h[0], t->ks)) || (e = cudaIpcGetMemHandle(&h[1], t->digests)) ||
       (e = cudaIpcGetMemHandle(&h[2], t->vfast)))
     return cuda_fail(e, "hkv_ipc_handles");
   return HKV_OK;
@@ -701,7 +699,7 @@ int hkv_set_peers(hkv_table* t, int32_t world, int32_t rank, const void* handles
   std::vector<PeerView> v((size_t)world);
   for (int r = 0; r < world; r++) {
     if (r == rank) {
-      v[r] = PeerView{t->keys, t->digests, t->vfast};
+      v[r] = PeerView{t->ks, t->digests, t->vfast};
       continue;
     }
     void* p[3];
@@ -730,7 +728,7 @@ int hkv_set_peers_local(hkv_table* t, int32_t world, hkv_table* const* shards) {
       if (e && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "hkv_set_peers_local: peer access");
       cudaGetLastError();
     }
-    v[r] = PeerView{o->keys, o->digests, o->vfast};
+    v[r] = PeerView{o->ks, o->digests, o->vfast};
   }
   return install_peers(t, world, v);
 }
@@ -970,9 +968,9 @@ int hkv_import_state(hkv_table* t, const uint64_t* keys, const uint8_t* digests,
   if (_gs.rc) return gate_fail(_gs.rc);
   const uint64_t cap = (uint64_t)t->cfg.capacity, dim = (uint64_t)t->cfg.value_dim;
   cudaError_t e;
-  if ((e = cudaMemcpy(t->keys, keys, cap * 8, cudaMemcpyHostToDevice)) ||
+  if ((e = cudaMemcpy2D(t->ks, 16, keys, 8, 8, cap, cudaMemcpyHostToDevice)) ||
       (e = cudaMemcpy(t->digests, digests, cap, cudaMemcpyHostToDevice)) ||
-      (e = cudaMemcpy(t->scores, scores, cap * 8, cudaMemcpyHostToDevice)))
+      (e = cudaMemcpy2D(t->ks + 1, 16, scores, 8, 8, cap, cudaMemcpyHostToDevice)))
     return cuda_fail(e, "import metadata");
   if (t->fast_rows && (e = cudaMemcpy(t->vfast, values, t->fast_rows * dim * 4, cudaMemcpyHostToDevice)))
     return cuda_fail(e, "import values");
@@ -1000,9 +998,9 @@ int hkv_export_state(hkv_table* t, uint64_t* keys, uint8_t* digests, uint64_t* s
   const uint64_t cap = (uint64_t)t->cfg.capacity, dim = (uint64_t)t->cfg.value_dim;
   cudaError_t e = cudaDeviceSynchronize();
   if (e) return cuda_fail(e, "export sync");
-  if (keys && (e = cudaMemcpy(keys, t->keys, cap * 8, cudaMemcpyDeviceToHost))) return cuda_fail(e, "export keys");
+  if (keys && (e = cudaMemcpy2D(keys, 8, t->ks, 16, 8, cap, cudaMemcpyDeviceToHost))) return cuda_fail(e, "export keys");
   if (digests && (e = cudaMemcpy(digests, t->digests, cap, cudaMemcpyDeviceToHost))) return cuda_fail(e, "export");
-  if (scores && (e = cudaMemcpy(scores, t->scores, cap * 8, cudaMemcpyDeviceToHost))) return cuda_fail(e, "export");
+  if (scores && (e = cudaMemcpy2D(scores, 8, t->ks + 1, 16, 8, cap, cudaMemcpyDeviceToHost))) return cuda_fail(e, "export");
   if (values) {
     if (t->fast_rows && (e = cudaMemcpy(values, t->vfast, t->fast_rows * dim * 4, cudaMemcpyDeviceToHost)))
       return cuda_fail(e, "export values");
@@ -1033,8 +1031,9 @@ int hkv_read_rows(hkv_table* t, int64_t row0, int64_t nrows, uint64_t* keys, uin
   if (_gs.rc) return gate_fail(_gs.rc);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
-  if (keys && nrows) e = cudaMemcpyAsync(keys, t->keys + row0, (size_t)nrows * 8, cudaMemcpyDefault, s);
-  if (!e && scores && nrows) e = cudaMemcpyAsync(scores, t->scores + row0, (size_t)nrows * 8, cudaMemcpyDefault, s);
+  if (keys && nrows) e = cudaMemcpy2DAsync(keys, 8, t->ks + 2 * row0, 16, 8, (size_t)nrows, cudaMemcpyDefault, s);
+  if (!e && scores && nrows)
+    e = cudaMemcpy2DAsync(scores, 8, t->ks + 2 * row0 + 1, 16, 8, (size_t)nrows, cudaMemcpyDefault, s);
   if (!e) e = cudaStreamSynchronize(s);
   return e ? cuda_fail(e, "hkv_read_rows") : HKV_OK;
 }
@@ -1066,9 +1065,8 @@ int hkv_snapshot(hkv_table* t, hkv_stream stream) {
   if (_gs.rc) return gate_fail(_gs.rc);
   const uint64_t cap = (uint64_t)t->cfg.capacity;
   cudaError_t e;
-  if (!t->snap_keys) {
-    if ((e = cudaMalloc((void**)&t->snap_keys, cap * 8)) || (e = cudaMalloc((void**)&t->snap_digests, cap)) ||
-        (e = cudaMalloc((void**)&t->snap_scores, cap * 8)) ||
+  if (!t->snap_ks) {
+    if ((e = cudaMalloc((void**)&t->snap_ks, cap * 16)) || (e = cudaMalloc((void**)&t->snap_digests, cap)) ||
         (e = cudaMalloc((void**)&t->snap_bits, (size_t)t->buckets * 16)) ||
         (e = cudaMalloc((void**)&t->snap_smin, (size_t)t->buckets * 64)) ||
         (e = cudaMalloc((void**)&t->snap_svalid, (size_t)t->buckets * 4)) ||
@@ -1076,9 +1074,8 @@ int hkv_snapshot(hkv_table* t, hkv_stream stream) {
       return fail(HKV_ENOMEM, std::string("snapshot allocation failed: ") + cudaGetErrorString(e));
   }
   cudaStream_t s = (cudaStream_t)stream;
-  if ((e = cudaMemcpyAsync(t->snap_keys, t->keys, cap * 8, cudaMemcpyDeviceToDevice, s)) ||
+  if ((e = cudaMemcpyAsync(t->snap_ks, t->ks, cap * 16, cudaMemcpyDeviceToDevice, s)) ||
       (e = cudaMemcpyAsync(t->snap_digests, t->digests, cap, cudaMemcpyDeviceToDevice, s)) ||
-      (e = cudaMemcpyAsync(t->snap_scores, t->scores, cap * 8, cudaMemcpyDeviceToDevice, s)) ||
       (e = cudaMemcpyAsync(t->snap_bits, t->bits, (size_t)t->buckets * 16, cudaMemcpyDeviceToDevice, s)) ||
       (e = cudaMemcpyAsync(t->snap_smin, t->smin, (size_t)t->buckets * 64, cudaMemcpyDeviceToDevice, s)) ||
       (e = cudaMemcpyAsync(t->snap_svalid, t->svalid, (size_t)t->buckets * 4, cudaMemcpyDeviceToDevice, s)) ||
@@ -1089,16 +1086,15 @@ int hkv_snapshot(hkv_table* t, hkv_stream stream) {
 
 int hkv_restore(hkv_table* t, hkv_stream stream) {
   if (!t) return fail(HKV_EINVAL, "null table");
-  if (!t->snap_keys) return fail(HKV_EINVAL, "no snapshot taken");
+  if (!t->snap_ks) return fail(HKV_EINVAL, "no snapshot taken");
   DeviceGuard _g(t->cfg.device);
   GateScope _gs(t->gate, HKV_ROLE_INSERTER, (cudaStream_t)stream);
   if (_gs.rc) return gate_fail(_gs.rc);
   const uint64_t cap = (uint64_t)t->cfg.capacity;
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
-  if ((e = cudaMemcpyAsync(t->keys, t->snap_keys, cap * 8, cudaMemcpyDeviceToDevice, s)) ||
+  if ((e = cudaMemcpyAsync(t->ks, t->snap_ks, cap * 16, cudaMemcpyDeviceToDevice, s)) ||
       (e = cudaMemcpyAsync(t->digests, t->snap_digests, cap, cudaMemcpyDeviceToDevice, s)) ||
-      (e = cudaMemcpyAsync(t->scores, t->snap_scores, cap * 8, cudaMemcpyDeviceToDevice, s)) ||
       (e = cudaMemcpyAsync(t->bits, t->snap_bits, (size_t)t->buckets * 16, cudaMemcpyDeviceToDevice, s)) ||
       (e = cudaMemcpyAsync(t->smin, t->snap_smin, (size_t)t->buckets * 64, cudaMemcpyDeviceToDevice, s)) ||
       (e = cudaMemcpyAsync(t->svalid, t->snap_svalid, (size_t)t->buckets * 4, cudaMemcpyDeviceToDevice, s)) ||

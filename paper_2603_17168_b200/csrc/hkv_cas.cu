@@ -60,13 +60,13 @@ __device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
 }
 __device__ __forceinline__ uint64_t ld_key(const TableDev& t, uint64_t row) {
 #ifdef HKV_CAS_KEYLDCG
-  return __ldcg(t.keys + row);
+  return __ldcg(kptr(t, row));
 #else
-  return *(volatile const uint64_t*)(t.keys + row);
+  return *(volatile const uint64_t*)kptr(t, row);
 #endif
 }
 __device__ __forceinline__ bool cas_key(const TableDev& t, uint64_t row, uint64_t expect) {
-  return atomicCAS((unsigned long long*)(t.keys + row), (unsigned long long)expect,
+  return atomicCAS((unsigned long long*)kptr(t, row), (unsigned long long)expect,
                    (unsigned long long)kLockedKey) == (unsigned long long)expect;
 }
 
@@ -145,13 +145,13 @@ constexpr int kScanBatch = HKV_CAS_SCANB;  // full-bucket scans per warp pass
 // first-index minimum (np.argmin, table.py:1080) of bucket b's 128 scores,
 // read by the whole warp (lane j: slots 4j..4j+3, 1 KB coalesced)
 __device__ __forceinline__ void warp_min(const TableDev& t, uint64_t b, int lane, uint64_t& minv, int& mslot) {
-  const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(t.scores + b * kSlots + 4 * lane);
-  const ulonglong2 x = __ldcg(sp), y = __ldcg(sp + 1);
-  uint64_t v = x.x;
+  const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(kptr(t, b * kSlots + 4 * lane));
+  const uint64_t s0 = __ldcg(sp).y, s1 = __ldcg(sp + 1).y, s2 = __ldcg(sp + 2).y, s3 = __ldcg(sp + 3).y;
+  uint64_t v = s0;
   int m = 4 * lane;
-  if (x.y < v) { v = x.y; m = 4 * lane + 1; }
-  if (y.x < v) { v = y.x; m = 4 * lane + 2; }
-  if (y.y < v) { v = y.y; m = 4 * lane + 3; }
+  if (s1 < v) { v = s1; m = 4 * lane + 1; }
+  if (s2 < v) { v = s2; m = 4 * lane + 2; }
+  if (s3 < v) { v = s3; m = 4 * lane + 3; }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const uint64_t ov = __shfl_xor_sync(kFullMask, v, o);
@@ -308,8 +308,8 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
           // hit (table.py:749-772): hold the slot
           row = hb * kSlots + slot;
           if (cas_key(t, row, key)) {
-            const uint64_t old = hit_needs_old(t.policy) ? __ldcg(t.scores + row) : 0;
-            t.scores[row] = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
+            const uint64_t old = hit_needs_old(t.policy) ? __ldcg(sptr(t, row)) : 0;
+            *sptr(t, row) = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
             summ_invalidate(t, hb, slot);
             task = a.op == kOpFindOrInsert ? kTaskRead : kTaskHit;
           } else {
@@ -332,11 +332,11 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
             slot = 32 * q + __ffs(~ws[q]) - 1;  // the lowest EMPTY slot
             row = tb * kSlots + slot;
             // EMPTY -> LOCKED; under the bucket lock nothing else claims it
-            atomicCAS((unsigned long long*)(t.keys + row), (unsigned long long)kEmptyKey,
+            atomicCAS((unsigned long long*)kptr(t, row), (unsigned long long)kEmptyKey,
                       (unsigned long long)kLockedKey);
             t.bits[tb * 4 + q] = ws[q] | (1u << (slot & 31));
             t.digests[row] = (uint8_t)d;
-            t.scores[row] = s_in;
+            *sptr(t, row) = s_in;
             t.svalid[tb] = 0u;
             task = kTaskInsert;
           } else {
@@ -361,13 +361,13 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
 #pragma unroll
         for (int k = 0; k < kScanBatch; k++) {
           if (ls[k] < 0) continue;
-          const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(t.scores + p1[k] * kSlots + 4 * lane);
-          x1[k] = __ldcg(sp);
-          y1[k] = __ldcg(sp + 1);
+          const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(kptr(t, p1[k] * kSlots + 4 * lane));
+          x1[k] = make_ulonglong2(__ldcg(sp).y, __ldcg(sp + 1).y);
+          y1[k] = make_ulonglong2(__ldcg(sp + 2).y, __ldcg(sp + 3).y);
           if (t.dual) {
-            const ulonglong2* sq = reinterpret_cast<const ulonglong2*>(t.scores + p2[k] * kSlots + 4 * lane);
-            x2[k] = __ldcg(sq);
-            y2[k] = __ldcg(sq + 1);
+            const ulonglong2* sq = reinterpret_cast<const ulonglong2*>(kptr(t, p2[k] * kSlots + 4 * lane));
+            x2[k] = make_ulonglong2(__ldcg(sq).y, __ldcg(sq + 1).y);
+            y2[k] = make_ulonglong2(__ldcg(sq + 2).y, __ldcg(sq + 3).y);
           }
         }
 #pragma unroll
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
               a.es[i] = minv;
             }
             t.digests[row] = (uint8_t)d;
-            t.scores[row] = s_in;
+            *sptr(t, row) = s_in;
             t.svalid[tb] = 0u;
             task = kTaskEvict;
           }
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
       __syncwarp();
       fence_rel();  // rows (every lane's stores) before the keys
       __syncwarp();
-      if (task != kTaskNone) st_release_u64(t.keys + row, key);
+      if (task != kTaskNone) st_release_u64(kptr(t, row), key);
       if (!__any_sync(kFullMask, task != kTaskNone) && !__all_sync(kFullMask, done)) {
         if (++idle_rounds > 2) __nanosleep(64);
       } else {

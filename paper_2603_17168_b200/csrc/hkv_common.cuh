@@ -7,8 +7,9 @@
 //   bits    [B][4]   u32  128-bit occupancy bitmap (bit s <=> keys[b][s] is a
 //                         user key); replaces the reference's occupancy
 //                         counter + argmax(keys==EMPTY) scan (table.py:1171)
-//   keys    [B][128] u64  8 lines per bucket
-//   scores  [B][128] u64  8 lines per bucket (read only on full-bucket decisions)
+//   ks      [B][128] {u64 key, u64 score}  one 16-B pair per slot (16 lines per
+//                         bucket): an insert's key and score writes land in one
+//                         32-B sector instead of two in separate arrays
 //   smin    [B][8]   u64  eviction summary: min score of each 16-slot group, so
 //   svalid  [B]      u32  a full-bucket argmin reads 64 B + one group's 128 B
 //                         instead of the 1-KB score row (bit g: group g exact;
@@ -40,9 +41,8 @@ enum Ctr : int { kLoads = 0, kCompares = 1, kScans = 2, kRetries = 3, kVFast = 4
 
 // Table metadata handed to kernels by value.
 struct TableDev {
-  uint64_t* keys;
+  uint64_t* ks;       // [capacity] x {key, score} (kptr / sptr)
   uint8_t* digests;
-  uint64_t* scores;
   uint32_t* bits;
   uint64_t* smin;     // [B][8] min score of each 16-slot group (exact where svalid says so)
   uint32_t* svalid;   // [B] bit g set <=> smin[b][g] == min(scores[b][16g .. 16g+15])
@@ -124,6 +124,10 @@ __device__ __forceinline__ uint64_t hit_score(int policy, uint64_t old, uint64_t
 __device__ __forceinline__ bool hit_needs_old(int policy) {
   return policy == kLfu || policy == kEpochLfu || policy == kCustom;
 }
+
+// slot row's key and score in the interleaved pair array
+__device__ __forceinline__ uint64_t* kptr(const TableDev& t, uint64_t row) { return t.ks + 2 * row; }
+__device__ __forceinline__ uint64_t* sptr(const TableDev& t, uint64_t row) { return t.ks + 2 * row + 1; }
 
 // store.py:84-94 / 115-131: position-addressed value row.
 __device__ __forceinline__ float* value_row(const TableDev& t, uint64_t row) {

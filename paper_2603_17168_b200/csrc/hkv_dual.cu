@@ -71,13 +71,13 @@ __device__ __forceinline__ int probe_loaded(const TableDev& t, const Tile8& tile
                                             uint32_t d, uint4 dw, uint32_t occ, ctr_t& n_compares) {
   const int r = tile.thread_rank();
   uint32_t cand = (t.digest_filter ? match16(dw, d) : 0xFFFFu) & occ;
-  const uint64_t* kp = t.keys + b * kSlots + r * kSPL;
+  const uint64_t* kp = kptr(t, b * kSlots + r * kSPL);
   int hit = -1, ncmp = 0, ncmp_all = 0;
   while (cand) {
     const int j = __ffs(cand) - 1;
     cand &= cand - 1;
     ncmp_all++;
-    if (kp[j] == key) {
+    if (kp[2 * j] == key) {
       hit = r * kSPL + j;
       ncmp = ncmp_all;
       break;
@@ -129,7 +129,7 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
     if (slot >= 0) {
       if (slot / kSPL == r) {
         const uint64_t row = hb * kSlots + slot;
-        t.keys[row] = kEmptyKey;
+        *kptr(t, row) = kEmptyKey;
         const uint32_t o = (hb == b1) ? occ1 : occ2;
         store_occ(t, hb, r, o & ~(1u << (slot % kSPL)));
       }
@@ -148,8 +148,8 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
     // hit: table.py:1045-1062
     const uint64_t row = hb * kSlots + slot;
     if (slot / kSPL == r) {
-      const uint64_t old = hit_needs_old(t.policy) ? t.scores[row] : 0;
-      t.scores[row] = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
+      const uint64_t old = hit_needs_old(t.policy) ? *sptr(t, row) : 0;
+      *sptr(t, row) = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
       summ_invalidate(t, hb, slot);
     }
     float* vr = value_row(t, row);
@@ -209,9 +209,9 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
       const int j = __ffs(~occ & 0xFFFFu) - 1;
       s = r * kSPL + j;
       const uint64_t row = tb * kSlots + s;
-      t.keys[row] = key;
+      *kptr(t, row) = key;
       t.digests[row] = (uint8_t)d;
-      t.scores[row] = s_in;
+      *sptr(t, row) = s_in;
       summ_invalidate(t, tb, s);
       store_occ(t, tb, r, occ | (1u << j));
     }
@@ -229,16 +229,16 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
     float* vr = value_row(t, row);
     if (a.collect) {
       if (r == ol) {
-        a.ek[i] = t.keys[row];
+        a.ek[i] = *kptr(t, row);
         a.es[i] = minv;
       }
       copy_row<kG, VEC>(a.ev + (uint64_t)i * dim, vr, dim, r);
       ctr[row < t.fast_rows ? kVFast : kVOver]++;
     }
     if (r == ol) {
-      t.keys[row] = key;
+      *kptr(t, row) = key;
       t.digests[row] = (uint8_t)d;
-      t.scores[row] = s_in;
+      *sptr(t, row) = s_in;
       summ_invalidate(t, tb, m);
     }
     write_row<VEC>(vr, vin, pre, dim, r);

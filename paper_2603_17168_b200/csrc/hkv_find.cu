@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(256) k_find_peer(const PeerView* __restrict__ 
         while (m) {
           const int j = __ffs(m) - 1;
           m &= m - 1;
-          const uint64_t k2 = v.keys[rowbase + 32 * q + j];
+          const uint64_t k2 = v.ks[2 * (rowbase + 32 * q + j)];
           if (k2 == key) {
             hit = 32 * q + j;
             m = 0;

@@ -108,7 +108,7 @@ enum { kOpUpsert = 0, kOpFindOrInsert = 1, kOpErase = 2 };
 // One shard of a hash-sharded table as seen by another rank (peer memory:
 // CUDA IPC over NVLink, or a table of the same process).
 struct PeerView {
-  const uint64_t* keys;
+  const uint64_t* ks;   // (key, score) pairs
   const uint8_t* digests;
   const float* values;  // fast tier: every row of the shard (peer find needs fast_tier_budget == buckets)
 };

@@ -14,8 +14,7 @@ namespace hkv {
 // [cursor, capacity) keeping user keys (key < LOCKED) that pass the predicate.
 // ---------------------------------------------------------------------------
 struct ExportFlag {
-  const uint64_t* keys;
-  const uint64_t* scores;
+  const uint64_t* ks;  // (key, score) pairs
   const uint8_t* mask;
   int64_t base;  // first row of this chunk
   int64_t mask_base;
@@ -23,8 +22,8 @@ struct ExportFlag {
   uint64_t min_score;
   __host__ __device__ bool operator()(const int64_t& j) const {
     const int64_t r = base + j;
-    if (keys[r] >= kLockedKey) return false;
-    if (has_min && scores[r] < min_score) return false;
+    if (ks[2 * r] >= kLockedKey) return false;
+    if (has_min && ks[2 * r + 1] < min_score) return false;
     if (mask && !mask[r - mask_base]) return false;
     return true;
   }
@@ -41,8 +40,8 @@ __global__ void k_export_gather(TableDev t, const uint32_t* __restrict__ list, i
   for (int64_t j = gid; j < take; j += ngroups) {
     const uint64_t row = (uint64_t)(base + list[j]);
     if (r == 0) {
-      ok[j] = t.keys[row];
-      os[j] = t.scores[row];
+      ok[j] = *kptr(t, row);
+      os[j] = *sptr(t, row);
       ctr[row < t.fast_rows ? kVFast : kVOver]++;
     }
     copy_row<kG, VEC>(ov + j * (int64_t)t.dim, value_row(t, row), t.dim, r);
@@ -64,7 +63,7 @@ cudaError_t run_export(const TableDev& t, int64_t cursor, int64_t max_count, int
   while (pos < end && taken < max_count) {
     const int64_t len = (end - pos) < kChunk ? (end - pos) : kChunk;
     thrust::counting_iterator<int64_t> cnt(0);
-    ExportFlag f{t.keys, t.scores, mask, pos, cursor, has_min, min_score};
+    ExportFlag f{t.ks, mask, pos, cursor, has_min, min_score};
     thrust::transform_iterator<ExportFlag, thrust::counting_iterator<int64_t>, bool> fl(cnt, f);
     size_t bytes = ws.cub_bytes;
     if ((e = cub::DeviceSelect::Flagged(ws.cub_tmp, bytes, cnt, fl, ws.aux, nsel, (int)len, s))) return e;
@@ -110,10 +109,10 @@ __global__ void k_bits_from_keys(TableDev t, int64_t buckets) {
   const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / kG;
   long long cnt = 0;
   for (int64_t b = gid; b < buckets; b += ngroups) {
-    const uint64_t* kp = t.keys + b * kSlots + r * kSPL;
+    const uint64_t* kp = kptr(t, b * kSlots + r * kSPL);
     uint32_t occ = 0;
 #pragma unroll
-    for (int j = 0; j < kSPL; j++) occ |= (kp[j] < kLockedKey ? 1u : 0u) << j;
+    for (int j = 0; j < kSPL; j++) occ |= (kp[2 * j] < kLockedKey ? 1u : 0u) << j;
     store_occ(t, b, r, occ);
     cnt += __popc(occ);
   }
@@ -140,11 +139,11 @@ __global__ void k_consistency(TableDev t, int64_t buckets, int* ok_dev, unsigned
   long long cnt = 0;
   int bad = 0;
   for (int64_t b = gid; b < buckets; b += ngroups) {
-    const uint64_t* kp = t.keys + b * kSlots + r * kSPL;
+    const uint64_t* kp = kptr(t, b * kSlots + r * kSPL);
     const uint8_t* dp = t.digests + b * kSlots + r * kSPL;
     uint32_t occ = 0;
     for (int j = 0; j < kSPL; j++) {
-      const uint64_t k = kp[j];
+      const uint64_t k = kp[2 * j];
       if (k < kLockedKey) {
         occ |= 1u << j;
         if (digest_of(fmix64(k)) != dp[j]) bad = 1;

@@ -190,9 +190,9 @@ __global__ void __launch_bounds__(kTpsThreads, HKV_TPS_MINB) k_meta_tps(TableDev
         if (s0 < 0) s0 = x; else s1 = x;
       }
     }
-    const uint64_t* kr = t.keys + (uint64_t)r.b * kSlots;
-    if (s0 >= 0) { k0 = kr[s0]; nk = 1; }
-    if (s1 >= 0) { k1 = kr[s1]; nk = 2; }
+    const uint64_t* kr = kptr(t, (uint64_t)r.b * kSlots);
+    if (s0 >= 0) { k0 = kr[2 * s0]; nk = 1; }
+    if (s1 >= 0) { k1 = kr[2 * s1]; nk = 2; }
   };
 #if HKV_TPS_STAGES == 3
   // Three line buffers: segment j+2's line is issued while j runs, and the
@@ -313,15 +313,12 @@ __global__ void __launch_bounds__(kLongThreads) k_meta_long(TableDev t, OpArgs a
 #pragma unroll
     for (int k = 0; k < 8; k++) stage[k] = dp[k];
     stage[8] = reinterpret_cast<const uint4*>(t.bits)[rec.b];
-    const ulonglong2* kp = reinterpret_cast<const ulonglong2*>(t.keys + rowbase);
-    const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(t.scores + rowbase);
+    const ulonglong2* kp = reinterpret_cast<const ulonglong2*>(kptr(t, rowbase));
 #pragma unroll 8
-    for (int s2 = 0; s2 < kSlots / 2; s2++) {
-      const ulonglong2 kk = kp[s2], ss = sp[s2];
-      K[(2 * s2) * kLongThreads + threadIdx.x] = kk.x;
-      K[(2 * s2 + 1) * kLongThreads + threadIdx.x] = kk.y;
-      Sc[(2 * s2) * kLongThreads + threadIdx.x] = ss.x;
-      Sc[(2 * s2 + 1) * kLongThreads + threadIdx.x] = ss.y;
+    for (int s = 0; s < kSlots; s++) {
+      const ulonglong2 ks = kp[s];  // (key, score)
+      K[s * kLongThreads + threadIdx.x] = ks.x;
+      Sc[s * kLongThreads + threadIdx.x] = ks.y;
     }
     tps_segment<OP, COLLECT, true>(t, a, rec, stage, sb, sidx, run_end, skeys, n, vrow, rrow, rsrc, clock0,
                                    fel_open, false, lfu_like, runs, ctr, sd, fe_min, LW + threadIdx.x,
@@ -592,11 +589,11 @@ __global__ void __launch_bounds__(256) k_assign_apply(TableDev t, const float* _
         }
         if (r == 0) {
           if (scores) {
-            t.scores[row] = scores[i];
+            *sptr(t, row) = scores[i];
             summ_invalidate(t, row / kSlots, (int)(row % kSlots));
           } else if (refresh) {
             const uint64_t tick = ticks ? ticks[i] : clock0 + (uint64_t)ranks[i] + 1;
-            t.scores[row] = hit_score(t.policy, t.scores[row], epoch, tick, false, 0);
+            *sptr(t, row) = hit_score(t.policy, *sptr(t, row), epoch, tick, false, 0);
             summ_invalidate(t, row / kSlots, (int)(row % kSlots));
           }
         }
@@ -683,11 +680,11 @@ __global__ void __launch_bounds__(256) k_assign_apply_agg(TableDev t, const floa
     if (values) copy_row<kG, VEC>(value_row(t, row), values + (uint64_t)i * t.dim, t.dim, r);
     if (r == 0) {
       if (scores) {
-        t.scores[row] = scores[i];
+        *sptr(t, row) = scores[i];
         summ_invalidate(t, row / kSlots, (int)(row % kSlots));
       } else if (refresh) {
         const uint64_t tick = ticks ? ticks[i] : clock0 + (uint64_t)ranks[i] + 1;
-        t.scores[row] = run_hit_score(t.policy, t.scores[row], epoch, tick, false, 0, acnt[h]);
+        *sptr(t, row) = run_hit_score(t.policy, *sptr(t, row), epoch, tick, false, 0, acnt[h]);
         summ_invalidate(t, row / kSlots, (int)(row % kSlots));
       }
     }

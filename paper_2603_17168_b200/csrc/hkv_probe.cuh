@@ -19,10 +19,10 @@ constexpr int kSPL = kSlots / kG;     // slots per lane (16)
 __device__ __forceinline__ void bucket_min(const TableDev& t, const Tile8& tile,
                                            uint64_t b, uint64_t& minv, int& mslot) {
   const int r = tile.thread_rank();
-  const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(t.scores + b * kSlots + r * kSPL);
+  const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(kptr(t, b * kSlots + r * kSPL));
   ulonglong2 s[kSPL / 2];
 #pragma unroll
-  for (int k = 0; k < kSPL / 2; k++) s[k] = sp[k];
+  for (int k = 0; k < kSPL / 2; k++) s[k] = make_ulonglong2(sp[2 * k].y, sp[2 * k + 1].y);
   uint64_t v = s[0].x;
   int m = r * kSPL;
 #pragma unroll
@@ -85,7 +85,7 @@ __device__ __forceinline__ int probe_line_thread(const TableDev& t, uint64_t b, 
     while (m) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
-      const uint64_t k = __ldg(t.keys + rowbase + 32 * q + j);
+      const uint64_t k = __ldg(kptr(t, rowbase + 32 * q + j));
       if (k == kEmptyKey) continue;  // candidates exclude EMPTY slots (table.py:243-247)
       ncmp++;
       if (k == key) {

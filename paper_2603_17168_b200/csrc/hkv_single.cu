@@ -21,10 +21,10 @@ namespace hkv {
 __device__ int probe_serial(const TableDev& t, uint64_t b, uint64_t key, uint32_t d, unsigned long long* ctr) {
   ctr[kLoads]++;
   const uint8_t* dl = t.digests + b * kSlots;
-  const uint64_t* kr = t.keys + b * kSlots;
+  const uint64_t* kr = kptr(t, b * kSlots);
   for (int s = 0; s < kSlots; s++) {
     if (t.digest_filter && dl[s] != d) continue;
-    const uint64_t k = kr[s];
+    const uint64_t k = kr[2 * s];
     if (k == kEmptyKey) continue;
     ctr[kCompares]++;
     if (k == key) return s;
@@ -33,12 +33,12 @@ __device__ int probe_serial(const TableDev& t, uint64_t b, uint64_t key, uint32_
 }
 
 __device__ void min_slot_serial(const TableDev& t, uint64_t b, int& m, uint64_t& mn) {
-  const uint64_t* sr = t.scores + b * kSlots;
+  const uint64_t* sr = sptr(t, b * kSlots);
   m = 0;
   mn = sr[0];
   for (int s = 1; s < kSlots; s++)
-    if (sr[s] < mn) {  // np.argmin: the first index on ties
-      mn = sr[s];
+    if (sr[2 * s] < mn) {  // np.argmin: the first index on ties
+      mn = sr[2 * s];
       m = s;
     }
 }
@@ -71,9 +71,9 @@ __device__ void write_row(const TableDev& t, uint64_t b, int s, const float* v, 
 __device__ void publish(const TableDev& t, uint64_t b, int s, uint64_t key, uint32_t d, uint64_t score,
                         const float* v, unsigned long long* c) {
   t.digests[b * kSlots + s] = (uint8_t)d;
-  t.scores[b * kSlots + s] = score;
+  *sptr(t, b * kSlots + s) = score;
   write_row(t, b, s, v, c);
-  t.keys[b * kSlots + s] = key;
+  *kptr(t, b * kSlots + s) = key;
   t.svalid[b] = 0;
 }
 
@@ -115,7 +115,7 @@ __global__ void k_upsert_one(TableDev t, uint64_t key, const float* v, int dual,
   }
   const bool custom = t.policy == kCustom;
   if (s >= 0) {  // _scalar_hit (table.py:749-772)
-    uint64_t& sc = t.scores[b * kSlots + s];
+    uint64_t& sc = *sptr(t, b * kSlots + s);
     uint64_t ns;
     if (custom) {
       ns = has_score ? score : sc;
@@ -201,7 +201,7 @@ __global__ void k_upsert_one(TableDev t, uint64_t key, const float* v, int dual,
     *t.fel = (double)(long long)*t.size / (double)t.capacity;
     *t.fel_set = 1;
   }
-  r->evicted_key = t.keys[tb * kSlots + m];
+  r->evicted_key = *kptr(t, tb * kSlots + m);
   r->evicted_score = mn;
   publish(t, tb, m, key, d, s_in, v, c);
   r->kind = kEvicted;

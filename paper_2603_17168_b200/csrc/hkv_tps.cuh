@@ -154,19 +154,19 @@ __device__ __forceinline__ void put8(uint64_t (&a)[8], int g, uint64_t v) {
 // itself).
 template <bool C>
 __device__ __forceinline__ uint64_t bkey(const TableDev& t, const TpsState& S, int j) {
-  if constexpr (C) return S.K[j * S.cs]; else return t.keys[S.rowbase + j];
+  if constexpr (C) return S.K[j * S.cs]; else return *kptr(t, S.rowbase + j);
 }
 template <bool C>
 __device__ __forceinline__ void set_bkey(const TableDev& t, const TpsState& S, int j, uint64_t v) {
-  if constexpr (C) S.K[j * S.cs] = v; else t.keys[S.rowbase + j] = v;
+  if constexpr (C) S.K[j * S.cs] = v; else *kptr(t, S.rowbase + j) = v;
 }
 template <bool C>
 __device__ __forceinline__ uint64_t bscore(const TableDev& t, const TpsState& S, int j) {
-  if constexpr (C) return S.Sc[j * S.cs]; else return t.scores[S.rowbase + j];
+  if constexpr (C) return S.Sc[j * S.cs]; else return *sptr(t, S.rowbase + j);
 }
 template <bool C>
 __device__ __forceinline__ void set_bscore(const TableDev& t, const TpsState& S, int j, uint64_t v) {
-  if constexpr (C) S.Sc[j * S.cs] = v; else t.scores[S.rowbase + j] = v;
+  if constexpr (C) S.Sc[j * S.cs] = v; else *sptr(t, S.rowbase + j) = v;
 }
 template <bool C>
 __device__ __forceinline__ void set_bdigest(const TableDev& t, const TpsState& S, int j, uint32_t d) {
@@ -208,13 +208,10 @@ __device__ __forceinline__ void tps_group_scan(const TableDev& t, const TpsState
 #pragma unroll
     for (int k = 0; k < 16; k++) v[k] = S.Sc[(16 * g + k) * S.cs];
   } else {
-    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(t.scores + S.rowbase + 16 * g);
+    // 16 (key, score) pairs: two 128-B lines
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(kptr(t, S.rowbase + 16 * g));
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-      const ulonglong2 x = p[k];
-      v[2 * k] = x.x;
-      v[2 * k + 1] = x.y;
-    }
+    for (int k = 0; k < 16; k++) v[k] = p[k].y;
   }
   mn = v[0];
   ms = 0;
@@ -362,9 +359,13 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
 #pragma unroll
       for (int w = 3; w >= 0; w--)
         if (oc[w] != 0xFFFFFFFFu) s = 32 * w + __ffs(~oc[w]) - 1;
+#ifndef HKV_EXP_NOKEY
       set_bkey<C>(t, S, s, key);
+#endif
       set_bdigest<C>(t, S, s, d);
+#ifndef HKV_EXP_NOSCORE
       set_bscore<C>(t, S, s, s_in);
+#endif
       const uint32_t o = S.O[s >> 5] | (1u << (s & 31));
       S.O[s >> 5] = o;
       set_bocc<C>(t, S, b, s >> 5, o);
@@ -617,13 +618,9 @@ __device__ __forceinline__ void tps_segment(const TableDev& t, const OpArgs& a, 
   }
   if (S.svdirty || S.smdirty) t.svalid[b] = S.sv;
   if constexpr (C) {  // write the bucket back once
-    ulonglong2* kd = reinterpret_cast<ulonglong2*>(t.keys + S.rowbase);
-    ulonglong2* sd2 = reinterpret_cast<ulonglong2*>(t.scores + S.rowbase);
+    ulonglong2* kd = reinterpret_cast<ulonglong2*>(kptr(t, S.rowbase));
 #pragma unroll 8
-    for (int j = 0; j < kSlots / 2; j++) {
-      kd[j] = make_ulonglong2(S.K[(2 * j) * cs], S.K[(2 * j + 1) * cs]);
-      sd2[j] = make_ulonglong2(S.Sc[(2 * j) * cs], S.Sc[(2 * j + 1) * cs]);
-    }
+    for (int j = 0; j < kSlots; j++) kd[j] = make_ulonglong2(S.K[j * cs], S.Sc[j * cs]);
     uint4* dd = reinterpret_cast<uint4*>(t.digests + S.rowbase);
 #pragma unroll
     for (int k = 0; k < 8; k++) dd[k] = S.L[k];
