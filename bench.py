@@ -563,6 +563,15 @@ def run_single(a):
         prof = cProfile.Profile()
     wall = 0.0
     launches = 0
+    import ctypes as C
+
+    def ktime(name):
+        ms, n = C.c_double(), C.c_int64()
+        lib.hkv_kernel_times(name.encode(), C.byref(ms), C.byref(n))
+        return ms.value, n.value
+
+    knames = ("find", "find_gather", "apply", "values_write")
+    ktimes = {}  # lambda -> name -> (ms, launches): the live kernel timers, read per lambda
     for li, lam in enumerate(a.lambdas):
         for s in range(a.warmup):
             one_op(lam, s, False)
@@ -582,6 +591,7 @@ def run_single(a):
         torch.cuda.nvtx.range_pop()
         lib.hkv_set_kernel_timing(0)
         launches += lib.hkv_launch_count() - launches0
+        ktimes[lam] = {nm: ktime(nm) for nm in knames}
     if prof is not None:
         import pstats
 
@@ -589,17 +599,13 @@ def run_single(a):
     clk = clocks.stop()
     lib.hkv_set_kernel_timing(0)
 
-    import ctypes as C
+    def ksum(name):
+        return sum(k[name][0] for k in ktimes.values()), sum(k[name][1] for k in ktimes.values())
 
-    def ktime(name):
-        ms, n = C.c_double(), C.c_int64()
-        lib.hkv_kernel_times(name.encode(), C.byref(ms), C.byref(n))
-        return ms.value, n.value
-
-    find_ms, find_n = ktime("find")  # probe kernel
-    fg_ms, fg_n = ktime("find_gather")
-    apply_ms, apply_n = ktime("apply")
-    vw_ms, vw_n = ktime("values_write")
+    find_ms, find_n = ksum("find")  # probe kernel
+    fg_ms, fg_n = ksum("find_gather")
+    apply_ms, apply_n = ksum("apply")
+    vw_ms, vw_n = ksum("values_write")
     # device times
     per = {}
     tot_ms = 0.0
@@ -661,13 +667,38 @@ def run_single(a):
             traffic = json.load(open(tpath)).get(name)
         except Exception:
             traffic = None
+    # the same two kernels per lambda (the byte model depends on the outcome mix)
+    per_lambda = {}
+    for lam, kt in ktimes.items():
+        pc = per_lam_counts[lam]
+        v = 4 * dim
+        ent = {}
+        fms, fn = kt["find"][0] + kt["find_gather"][0], kt["find"][1]
+        if fn:
+            gbs = B * bytes_find_hit(dim) / (fms / fn / 1e3) / 1e9
+            ent["find"] = {"avg_ms": round(fms / fn, 5), "achieved_gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
+        ams, an = kt["apply"]
+        if an:
+            moved = int(pc[[0, 1, 3]].sum()) * 2 * v + int(pc[2]) * v
+            mb = (bytes_upsert(pc, dim) - moved) / an
+            gbs = mb / (ams / an / 1e3) / 1e9
+            ent["k_meta_tps"] = {"avg_ms": round(ams / an, 5), "algorithmic_bytes_per_launch": int(mb),
+                                 "achieved_gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
+            # the whole insert_or_assign against its full byte model (metadata + value rows)
+            im = breakdown[f"{lam:.2f}"]["insert_ms"]
+            ub = bytes_upsert(pc // a.steps, dim)
+            ent["insert_or_assign_op"] = {"ms": round(im, 5), "algorithmic_bytes": int(ub),
+                                          "achieved_gbs": round(ub / (im / 1e3) / 1e9, 1),
+                                          "frac": round(ub / (im / 1e3) / 1e9 / peak, 4)}
+        per_lambda[f"{lam:.2f}"] = ent
     roofline = {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": int(kbytes), "avg_launch_ms": round(avg_ms, 5),
                 "traffic": traffic,
                 "other_kernels": {c[0]: {"avg_ms": round(c[1] / c[2], 5),
                                          "achieved_gbs": round(c[3] / (c[1] / c[2] / 1e3) / 1e9, 1),
-                                         "share_of_step": round(c[1] / tot_ms, 4)} for c in cand}}
+                                         "share_of_step": round(c[1] / tot_ms, 4)} for c in cand},
+                "per_lambda": per_lambda}
 
     # e2e through the public API with pinned host buffers
     e2e = None

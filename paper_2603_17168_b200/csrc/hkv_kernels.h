@@ -63,8 +63,8 @@ struct Workspace {
   int* lwtab = nullptr;      // single mode: per-thread last-writer tables of the metadata pass
   uint32_t* b2 = nullptr;    // dual: second bucket
   uint32_t* pend = nullptr;  // dual: second pending list
-  uint64_t* ek = nullptr;
-  uint64_t* es = nullptr;
+  uint64_t* ek = nullptr;  // per-op victim (key, score) pairs: ek[2i], ek[2i + 1] (= es[2i])
+  uint64_t* es = nullptr;  // ek + 1 (not a separate allocation)
   float* ev = nullptr;
   // dual mode: 2n (bucket, op) pairs and per-op ranks (hkv_dual.cu)
   int64_t dcap = 0;
@@ -92,7 +92,7 @@ struct OpArgs {
   const uint64_t* scores;
   const uint64_t* ticks;
   uint8_t* outcomes;
-  uint64_t* ek;  // per-op evicted key scratch (collect)
+  uint64_t* ek;  // per-op evicted (key, score) scratch (collect): ek[2i], es[2i] with es = ek + 1
   uint64_t* es;
   float* ev;
   int op;        // 0 insert_or_assign, 1 find_or_insert, 2 erase

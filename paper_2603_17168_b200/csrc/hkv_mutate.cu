@@ -414,8 +414,8 @@ __global__ void __launch_bounds__(256) k_values_read(TableDev t, float* __restri
         i = list[j];
         dst[u] = reinterpret_cast<V*>(ev + j * (int64_t)dim);
         if (r == 0) {
-          ek[j] = ek_tmp[i];
-          es[j] = es_tmp[i];
+          ek[j] = ek_tmp[2 * i];
+          es[j] = es_tmp[2 * i];
         }
       } else {
         i = (uint32_t)j;
@@ -503,8 +503,8 @@ __global__ void k_evict_gather(const Scalars* sc, const uint32_t* __restrict__ l
   for (int64_t j = gid; j < ne; j += ngroups) {
     const uint32_t i = list[j];
     if (r == 0) {
-      ek[j] = ek_tmp[i];
-      es[j] = es_tmp[i];
+      ek[j] = ek_tmp[2 * i];
+      es[j] = es_tmp[2 * i];
     }
     copy_row<kG, VEC>(ev + j * dim, ev_tmp + (uint64_t)i * dim, dim, r);
   }
@@ -733,7 +733,9 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual
   }
   // ev_mode: 1 = per-op victim key/score scratch, 2 = also victim value rows (dual mode)
   if (ev_mode >= 1 && ws.cap_ek < n) {
-    if ((e = grow(ws.ek, ws.cap_n)) || (e = grow(ws.es, ws.cap_n))) return e;
+    // victim (key, score) of op i at ek[2i], ek[2i + 1]: one sector per eviction
+    if ((e = grow(ws.ek, 2 * ws.cap_n))) return e;
+    ws.es = ws.ek + 1;
     ws.cap_ek = ws.cap_n;
   }
   if (ev_mode >= 2 && (ws.cap_ev < n || ws.dim != dim)) {
@@ -777,7 +779,7 @@ void ws_free(Workspace& ws) {
                   ws.lwtab,
                   ws.rsrc,
                   ws.b2, ws.pend,
-                  ws.ek, ws.es, ws.ev, ws.cub_tmp, ws.sc, ws.col, ws.segd};
+                  ws.ek, ws.ev, ws.cub_tmp, ws.sc, ws.col, ws.segd};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ws.skew_host) cudaFreeHost((void*)ws.skew_host);
@@ -983,10 +985,12 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
   g_launches++;
   long long* nev = reinterpret_cast<long long*>(n_evicted);
   if (collect && n > 0) {
+    ktimer_begin("evict_select", s, 2);
     size_t bytes = ws.cub_bytes;
     thrust::counting_iterator<int64_t> cnt(0);
     thrust::transform_iterator<IsEvicted, thrust::counting_iterator<int64_t>, bool> fl(cnt, IsEvicted{a.outcomes});
     if ((e = cub::DeviceSelect::Flagged(ws.cub_tmp, bytes, cnt, fl, ws.aux, nev, (int)n, s))) return e;
+    ktimer_end("evict_select", s, 2);
     g_launches += 2;
   }
   const int64_t vblocks = tile_blocks(n, num_sms);
@@ -996,6 +1000,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
     const int vr = vec_of(t.dim, a.values, t.vfast, t.vover, collect ? ev_out : nullptr);
     if (collect || a.op == kOpFindOrInsert) {
       const uint32_t* list = collect ? ws.aux : nullptr;
+      ktimer_begin("values_read", s, 2);
       int64_t rblocks = (((n + 3) / 4) * kG + 255) / 256;
       const int64_t rcap = (int64_t)num_sms * 8 * 4;
       if (rblocks > rcap) rblocks = rcap;
@@ -1009,6 +1014,7 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       else
         launch_pdl(k_values_read<1, 4>, dim3((unsigned)rblocks), dim3(256), 0, s, t, a.values, a.outcomes, ws.rrow, ws.rsrc, list, nev,
                                                            ws.ek, ws.es, ek_out, es_out, ev_out, n, ws.sc);
+      ktimer_end("values_read", s, 2);
       g_launches++;
     }
     ktimer_begin("values_write", s);

@@ -415,8 +415,8 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
       if (s_in >= gmin) {  // the single-bucket path admits ties (table.py:1083)
         const int m = 16 * gi + ms;
         if constexpr (COLLECT) {
-          a.ek[i] = bkey<C>(t, S, m);
-          a.es[i] = gmin;
+          a.ek[2 * i] = bkey<C>(t, S, m);
+          a.es[2 * i] = gmin;
         }
         set_bkey<C>(t, S, m, key);
         set_bdigest<C>(t, S, m, d);

@@ -14,11 +14,12 @@ import sys
 import torch
 
 sys.path.insert(0, ".")
+import bench  # noqa: E402
 import paper_2603_17168_b200 as hkv  # noqa: E402
 from paper_2603_17168_b200 import _lib  # noqa: E402
 from paper_2603_17168_b200 import workloads as W  # noqa: E402
 
-STAGES = ["prep", "sort", "segments", "count", "alloc", "scatter", "segfin", "big", "apply", "finalize", "values_write", "assign_apply", "find", "find_gather",
+STAGES = ["prep", "sort", "segments", "count", "alloc", "scatter", "segfin", "big", "apply", "finalize", "evict_select", "values_read", "values_write", "assign_apply", "find", "find_gather",
           "dual_ranks", "dual_flow"]
 lg = int(sys.argv[1]) if len(sys.argv) > 1 else 27
 cap, dim, B = 2**lg, 64, 2**20
@@ -44,12 +45,7 @@ off = 0
 reps = 10
 ins = [W.uniform_distinct_keys_torch(B, 0, stream_offset=2**44 + i * B) for i in range(reps)]
 for lam in [float(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else ['0.5', '1.0'])]:
-    while t.size() < int(cap * lam):
-        n = min(B, int(cap * lam) - t.size())
-        t.insert_or_assign(W.uniform_distinct_keys_torch(n, 0, stream_offset=off), vals[:n])
-        off += n
-        if lam == 1.0 and off > 4 * cap:
-            break
+    bench.fill_table(t, lam, cap, dim, B, torch, W)
     t.snapshot()
     q = W.uniform_distinct_keys_torch(B, 0, stream_offset=0)
     torch.cuda.synchronize()
@@ -64,12 +60,14 @@ for lam in [float(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else 
                 e0.record(st)
                 if op == "insert_or_assign":
                     t.insert_or_assign(ins[i], vals)
+                elif op == "insert_and_evict":
+                    t.insert_and_evict(ins[i], vals)
                 elif op == "assign":
                     t.assign(q, vals)
                 else:
                     t.find(q)
                 e1.record(st)
-                if op == "insert_or_assign":
+                if op.startswith("insert"):
                     t.restore()
                 torch.cuda.synchronize()
                 tot += e0.elapsed_time(e1)
