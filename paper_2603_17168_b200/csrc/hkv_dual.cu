@@ -168,7 +168,7 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
   const uint64_t s_in = insert_score(t.policy, a.epoch, tick, cs);
   uint64_t tb = b1;
   int m = 0;
-  uint64_t minv = 0;
+  uint64_t minv = 0, rest = kMaxScore;  // rest: the victim group's other 15 scores' minimum (its lane)
   bool admit = false;
   bool free_insert = false;
   if (!t.dual) {
@@ -176,7 +176,7 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
     if (occ_total < kSlots) {
       free_insert = true;  // _bulk_insert_free, table.py:1072-1076
     } else {
-      bucket_min(t, tile, b1, minv, m);  // table.py:1079-1083
+      bucket_min_summ(t, tile, b1, minv, m, rest);  // table.py:1079-1083
       ctr[kScans]++;
       admit = s_in >= minv;  // single-bucket path admits ties
     }
@@ -187,15 +187,16 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
       tb = o1 <= o2 ? b1 : b2;  // D1, table.py:1089-1095
       free_insert = true;
     } else {
-      uint64_t min1, min2;  // D2, table.py:1096-1119
+      uint64_t min1, min2, rest1, rest2;  // D2, table.py:1096-1119
       int m1, m2;
-      bucket_min(t, tile, b1, min1, m1);
-      bucket_min(t, tile, b2, min2, m2);
+      bucket_min_summ(t, tile, b1, min1, m1, rest1);
+      bucket_min_summ(t, tile, b2, min2, m2, rest2);
       ctr[kScans] += 2;
       const bool use2 = min2 < min1;
       tb = use2 ? b2 : b1;
       m = use2 ? m2 : m1;
       minv = use2 ? min2 : min1;
+      rest = use2 ? rest2 : rest1;
       admit = t.admit_unified ? s_in >= minv : s_in > minv;
     }
   }
@@ -239,7 +240,7 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
       *kptr(t, row) = key;
       t.digests[row] = (uint8_t)d;
       *sptr(t, row) = s_in;
-      summ_invalidate(t, tb, m);
+      t.smin[tb * 8 + ol] = s_in < rest ? s_in : rest;  // the group stays exact
     }
     write_row<VEC>(vr, vin, pre, dim, r);
     ctr[row < t.fast_rows ? kVFast : kVOver]++;

@@ -53,6 +53,58 @@ __device__ __forceinline__ void summ_invalidate(const TableDev& t, uint64_t b, i
   atomicAnd(t.svalid + b, ~(1u << (slot >> 4)));
 }
 
+// bucket_min through the eviction summary (the caller owns bucket b): lane r
+// of the tile owns group r (its kSPL = 16 slots).  A lane whose group minimum
+// is exact reads it from smin (the 64-B summary line); the others rescan their
+// 16 (key, score) pairs and make it exact.  The winning group (lowest minimum,
+// lowest group on ties) then finds its first slot holding the minimum, so the
+// answer is np.argmin's first index, as bucket_min.  In the winning lane,
+// `rest` = the group's minimum over its other 15 slots, for the caller to keep
+// the summary exact after replacing the victim's score.
+__device__ __forceinline__ void bucket_min_summ(const TableDev& t, const Tile8& tile, uint64_t b, uint64_t& minv,
+                                                int& mslot, uint64_t& rest) {
+  const int r = tile.thread_rank();
+  const uint32_t sv = t.svalid[b];
+  const bool exact = (sv >> r) & 1u;
+  const ulonglong2* gp = reinterpret_cast<const ulonglong2*>(kptr(t, b * kSlots + r * kSPL));
+  uint64_t gm;
+  if (exact) {
+    gm = t.smin[b * 8 + r];
+  } else {
+    gm = kMaxScore;
+#pragma unroll
+    for (int k = 0; k < kSPL; k++) {
+      const uint64_t x = gp[k].y;
+      gm = x < gm ? x : gm;
+    }
+    t.smin[b * 8 + r] = gm;
+  }
+  const unsigned fixed = tile.ballot(!exact);
+  if (fixed && r == 0) atomicOr(t.svalid + b, fixed);
+  uint64_t v = gm;
+  int g = r;
+#pragma unroll
+  for (int o = kG / 2; o > 0; o >>= 1) {
+    const uint64_t ov = tile.shfl_xor(v, o);
+    const int og = tile.shfl_xor(g, o);
+    if (ov < v || (ov == v && og < g)) { v = ov; g = og; }
+  }
+  int slot = 0;
+  rest = kMaxScore;
+  if (r == g) {
+    int first = -1;
+#pragma unroll
+    for (int k = 0; k < kSPL; k++) {
+      const uint64_t x = gp[k].y;
+      if (first < 0 && x == v) first = k;
+      else rest = x < rest ? x : rest;
+    }
+    slot = r * kSPL + first;
+  }
+  minv = v;
+  mslot = tile.shfl(slot, g);
+}
+
 // Thread-per-key probe (the default): one thread reads its key's whole
 // 128-B digest line (8 x 16 B, all in flight together), matches the 128
 // digests with __vcmpeq4, then checks candidate keys in slot order.  No
