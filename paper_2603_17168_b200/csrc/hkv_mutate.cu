@@ -150,28 +150,36 @@ __global__ void __launch_bounds__(kTpsThreads, HKV_TPS_MINB) k_meta_tps(TableDev
                                                             int32_t* __restrict__ rsrc, int* __restrict__ lwtab,
                                                             const unsigned* nbound) {
   griddep_wait();
-  if (nbound) n = *nbound;  // collector pipeline: sorted positions in use (device count)
   extern __shared__ uint4 tps_smem[];
   __shared__ BlockCtrs bc;
-  if (a.sc->err) return;
   block_ctrs_init(bc);
+  // every scalar the pass needs, and the thread's first two records from the
+  // singleton list (the common case), loaded together: the prologue is one
+  // round trip, not a chain of them
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int err = a.sc->err;
+  const int64_t nseg = (int64_t)a.sc->nseg;
+  const int64_t nmul = (int64_t)a.sc->nmulti;
+  const bool runs = a.sc->has_runs != 0;
+  const long long size0 = a.sc->size_before;
+  if (nbound) n = *nbound;  // collector pipeline: sorted positions in use (device count)
   const uint64_t clock0 = *t.clock;
   const bool fel_open = !*t.fel_set;
+  const SegRec g0 = gtid < cap ? recs[gtid] : SegRec{0, 0, 0, 0, 0};
+  const SegRec g1 = gtid + stride < cap ? recs[gtid + stride] : SegRec{0, 0, 0, 0, 0};
+  if (err) return;
   // at lambda > 0.97 a full bucket is the rule: fetch the summary with the first op
-  const bool spec = *t.size * 100ull > t.capacity * 97ull;
+  const bool spec = (unsigned long long)size0 * 100ull > t.capacity * 97ull;
   const bool lfu_like = t.policy == kLfu || t.policy == kEpochLfu;
-  const bool runs = a.sc->has_runs != 0;
   ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
   int sd = 0;
   uint32_t fe_min = 0xFFFFFFFFu;
-  const int64_t nseg = (int64_t)a.sc->nseg;
-  const int64_t nall = nseg + (int64_t)a.sc->nmulti;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nall = nseg + nmul;
   auto rec_at = [&](int64_t j) -> SegRec {
     if (j >= nall) return SegRec{0, 0, 0, 0, 0};
     return j < nseg ? recs[j] : recs[cap - 1 - (j - nseg)];
   };
-  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t j = gtid;
   // keys of the head op's first two digest candidates, loaded into registers
   // ahead of the segment that compares them
@@ -196,9 +204,9 @@ __global__ void __launch_bounds__(kTpsThreads, HKV_TPS_MINB) k_meta_tps(TableDev
   };
 #if HKV_TPS_STAGES == 3
   // Three line buffers: segment j+2's line is issued while j runs, and the
-  // candidate keys of j+1 were issued at the end of j-1 — a whole segment of
+  // candidate keys of j+1 were issued at the end of j-1 -- a whole segment of
   // slack for both dependent loads.
-  SegRec r0 = rec_at(j), r1 = rec_at(j + stride), r2 = rec_at(j + 2 * stride);
+  SegRec r0 = j < nseg ? g0 : rec_at(j), r1 = j + stride < nseg ? g1 : rec_at(j + stride), r2 = rec_at(j + 2 * stride);
   if (j < nall) tps_fetch(t, tps_buf(tps_smem, 0), r0.b);
   cp_async_commit();
   if (j + stride < nall) tps_fetch(t, tps_buf(tps_smem, 1), r1.b);
@@ -235,7 +243,7 @@ __global__ void __launch_bounds__(kTpsThreads, HKV_TPS_MINB) k_meta_tps(TableDev
     r2 = r3;
   }
 #else
-  SegRec ra = rec_at(j), rb = rec_at(j + stride);
+  SegRec ra = j < nseg ? g0 : rec_at(j), rb = j + stride < nseg ? g1 : rec_at(j + stride);
   if (j < nall) tps_fetch(t, tps_buf(tps_smem, 0), ra.b);
   cp_async_commit();
   if (j + stride < nall) tps_fetch(t, tps_buf(tps_smem, 1), rb.b);

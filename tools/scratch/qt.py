@@ -1,5 +1,5 @@
 """quick C2 insert timing: python tools/scratch/qt.py lambdas [ops] (env HKV_LIB selects a build)"""
-import sys, time
+import os, sys, time
 import torch
 sys.path.insert(0, ".")
 import bench
@@ -14,7 +14,9 @@ if os.environ.get("FETCH"):
 lams = [float(x) for x in sys.argv[1].split(",")]
 ops = sys.argv[2].split(",") if len(sys.argv) > 2 else ["insert_or_assign", "find"]
 cap, dim, B = 2**27, 64, 2**20
-t = hkv.CacheTable(hkv.TableConfig(capacity=cap, value_dim=dim))
+mode = os.environ.get("MODE", "single")
+workers = int(os.environ.get("WORKERS", "1"))
+t = hkv.CacheTable(hkv.TableConfig(capacity=cap, value_dim=dim, mode=mode, workers=workers))
 t.validate_keys = False
 vals = torch.randn((B, dim), device="cuda")
 ins = [W.uniform_distinct_keys_torch(B, 0, stream_offset=2**44 + i * B) for i in range(6)]
