@@ -174,7 +174,13 @@ __device__ __forceinline__ void set_bdigest(const TableDev& t, const TpsState& S
 }
 template <bool C>
 __device__ __forceinline__ void set_bocc(const TableDev& t, const TpsState& S, uint64_t b, int w, uint32_t o) {
-  if constexpr (!C) t.bits[b * 4 + w] = o;  // cached: S.O holds it, flushed at the end
+  if constexpr (!C) {  // cached: S.O holds it, flushed at the end
+#if HKV_OCC_HINT
+    st_keep(t.bits + b * 4 + w, o, S.pol);
+#else
+    t.bits[b * 4 + w] = o;
+#endif
+  }
 }
 
 // candidates of digest d: digest-equal and occupied (table.py:243-247)
@@ -526,6 +532,25 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
+// the occupancy word with L2 evict_last priority: the 16-MB bitmap of a C2
+// table then stays in L2 across batches while the digest lines and pairs
+// stream through (HKV_OCC_HINT=0: plain)
+#ifndef HKV_LINE_HINT
+#define HKV_LINE_HINT 0
+#endif
+#ifndef HKV_OCC_HINT
+#define HKV_OCC_HINT 1
+#endif
+__device__ __forceinline__ void cp_async16_keep(void* smem, const void* gmem) {
+#if HKV_OCC_HINT
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "l"(pol) : "memory");
+#else
+  cp_async16(smem, gmem);
+#endif
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -539,8 +564,12 @@ __device__ __forceinline__ uint4* tps_buf(uint4* smem, int stage) {
 __device__ __forceinline__ void tps_fetch(const TableDev& t, uint4* buf, uint64_t b) {
   const uint4* dp = reinterpret_cast<const uint4*>(t.digests + b * kSlots);
 #pragma unroll
+#if HKV_LINE_HINT
+  for (int k = 0; k < 8; k++) cp_async16_keep(buf + k, dp + k);
+#else
   for (int k = 0; k < 8; k++) cp_async16(buf + k, dp + k);
-  cp_async16(buf + 8, reinterpret_cast<const uint4*>(t.bits) + b);
+#endif
+  cp_async16_keep(buf + 8, reinterpret_cast<const uint4*>(t.bits) + b);
 }
 
 template <int OP, bool COLLECT, bool C>
