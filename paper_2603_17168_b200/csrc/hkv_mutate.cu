@@ -153,9 +153,7 @@ __global__ void __launch_bounds__(kTpsThreads, HKV_TPS_MINB) k_meta_tps(TableDev
   extern __shared__ uint4 tps_smem[];
   __shared__ BlockCtrs bc;
   block_ctrs_init(bc);
-  // every scalar the pass needs, and the thread's first two records from the
-  // singleton list (the common case), loaded together: the prologue is one
-  // round trip, not a chain of them
+  // every scalar the pass needs, loaded together
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int err = a.sc->err;
@@ -166,9 +164,9 @@ __global__ void __launch_bounds__(kTpsThreads, HKV_TPS_MINB) k_meta_tps(TableDev
   if (nbound) n = *nbound;  // collector pipeline: sorted positions in use (device count)
   const uint64_t clock0 = *t.clock;
   const bool fel_open = !*t.fel_set;
-  const SegRec g0 = gtid < cap ? recs[gtid] : SegRec{0, 0, 0, 0, 0};
-  const SegRec g1 = gtid + stride < cap ? recs[gtid + stride] : SegRec{0, 0, 0, 0, 0};
   if (err) return;
+  const SegRec g0 = gtid < nseg ? recs[gtid] : SegRec{0, 0, 0, 0, 0};
+  const SegRec g1 = gtid + stride < nseg ? recs[gtid + stride] : SegRec{0, 0, 0, 0, 0};
   // at lambda > 0.97 a full bucket is the rule: fetch the summary with the first op
   const bool spec = (unsigned long long)size0 * 100ull > t.capacity * 97ull;
   const bool lfu_like = t.policy == kLfu || t.policy == kEpochLfu;
@@ -339,15 +337,57 @@ __global__ void __launch_bounds__(kLongThreads) k_meta_long(TableDev t, OpArgs a
   block_ctrs_flush(bc, t.counters, t.size, ctr, sd);
 }
 
+// Clock advance + first_eviction_lambda (table.py:986-991) + error latch +
+// the skew hint, run by every block of the batch's last kernel (k_finalize,
+// or k_values_write when the batch moves values: one launch fewer).  The
+// lambda needs the inserts that precede the first eviction: counted by every
+// block over a strided share, the last block to finish publishes it.
+// Returns false when the batch failed (nothing else may run).
+template <int NT>
+__device__ __forceinline__ bool finalize_batch(const TableDev& t, Scalars* sc, const uint8_t* __restrict__ outcomes,
+                                               unsigned long long clock_advance, int add_found,
+                                               volatile unsigned* skew_hint) {
+  // segments of more than 16 ops in this batch, for the next call's choice
+  // between the collector and the sorted grouping (a mapped host word)
+  if (skew_hint && blockIdx.x == 0 && threadIdx.x == 0) *skew_hint = sc->nbig;
+  if (sc->err) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(t.err, sc->err);
+    return false;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *t.clock += clock_advance + (add_found ? sc->nfound : 0ull);
+  const unsigned fe = sc->first_ev;
+  if (*t.fel_set || fe == 0xFFFFFFFFu || outcomes == nullptr) return true;
+  unsigned cnt = 0;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < (int64_t)fe;
+       j += (int64_t)gridDim.x * blockDim.x)
+    cnt += outcomes[j] == kInserted;
+  typedef cub::BlockReduce<unsigned, NT> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const unsigned tot = BR(tmp).Sum(cnt);
+  if (threadIdx.x == 0) {
+    if (tot) atomicAdd(&sc->fel_cnt, (unsigned long long)tot);
+    __threadfence();
+    if (atomicAdd(&sc->fel_done, 1u) == gridDim.x - 1) {
+      __threadfence();
+      const unsigned long long all = atomicAdd(&sc->fel_cnt, 0ull);
+      *t.fel = (double)(sc->size_before + (long long)all) / (double)t.capacity;
+      *t.fel_set = 1;
+    }
+  }
+  return true;
+}
+
 // Value rows for the final writers: table[vrow[i]] = values[i].  Inputs are
 // read sequentially (consecutive i), destination rows at random; KPT ops per
 // tile keep 2*KPT 16-B loads in flight per lane.
 template <int VEC, int KPT>
 __global__ void __launch_bounds__(256) k_values_write(TableDev t, const float* __restrict__ values,
-                                                      const uint32_t* __restrict__ vrow, int64_t n,
-                                                      const Scalars* sc) {
+                                                      const uint32_t* __restrict__ vrow, int64_t n, Scalars* sc,
+                                                      const uint8_t* __restrict__ fin_outcomes,
+                                                      unsigned long long clock_advance,
+                                                      volatile unsigned* skew_hint) {
   griddep_wait();
-  if (sc->err) return;
+  if (!finalize_batch<256>(t, sc, fin_outcomes, clock_advance, 0, skew_hint)) return;
   using V = typename std::conditional<VEC == 4, uint4, typename std::conditional<VEC == 2, float2, float>::type>::type;
   const Tile8 tile;
   const int r = tile.thread_rank();
@@ -455,41 +495,12 @@ __global__ void __launch_bounds__(256) k_values_read(TableDev t, float* __restri
   }
 }
 
-// Clock advance + first_eviction_lambda (table.py:986-991) + error latch.
-// The lambda needs the inserts that precede the first eviction: counted by
-// every block over a strided share, the last block to finish publishes it.
 constexpr int kFinBlocks = 32;
 __global__ void __launch_bounds__(1024) k_finalize(TableDev t, Scalars* sc, const uint8_t* __restrict__ outcomes,
                                                    int64_t n, unsigned long long clock_advance, int add_found,
                                                    volatile unsigned* skew_hint) {
   griddep_wait();
-  // segments of more than 16 ops in this batch, for the next call's choice
-  // between the collector and the sorted grouping (a mapped host word)
-  if (skew_hint && blockIdx.x == 0 && threadIdx.x == 0) *skew_hint = sc->nbig;
-  if (sc->err) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(t.err, sc->err);
-    return;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *t.clock += clock_advance + (add_found ? sc->nfound : 0ull);
-  const unsigned fe = sc->first_ev;
-  if (*t.fel_set || fe == 0xFFFFFFFFu || outcomes == nullptr) return;
-  unsigned cnt = 0;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < (int64_t)fe;
-       j += (int64_t)gridDim.x * blockDim.x)
-    cnt += outcomes[j] == kInserted;
-  typedef cub::BlockReduce<unsigned, 1024> BR;
-  __shared__ typename BR::TempStorage tmp;
-  const unsigned tot = BR(tmp).Sum(cnt);
-  if (threadIdx.x == 0) {
-    if (tot) atomicAdd(&sc->fel_cnt, (unsigned long long)tot);
-    __threadfence();
-    if (atomicAdd(&sc->fel_done, 1u) == gridDim.x - 1) {
-      __threadfence();
-      const unsigned long long all = atomicAdd(&sc->fel_cnt, 0ull);
-      *t.fel = (double)(sc->size_before + (long long)all) / (double)t.capacity;
-      *t.fel_set = 1;
-    }
-  }
+  finalize_batch<1024>(t, sc, outcomes, clock_advance, add_found, skew_hint);
 }
 
 struct IsEvicted {
@@ -984,13 +995,18 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
       ktimer_end("dual_flow", s);
     }
   }
-  ktimer_begin("finalize", s, 2);
   // an empty batch never runs k_prep, which seeds first_ev: no outcomes, so
   // first_eviction_lambda cannot latch from the zeroed scratch
-  launch_pdl(k_finalize, dim3(kFinBlocks), dim3(1024), 0, s, t, ws.sc, (a.op == kOpErase || n == 0) ? nullptr : a.outcomes, n,
-                                         clock_advance, 0, (!t.dual && !cas && n > 0) ? ws.skew_dev : nullptr);
-  ktimer_end("finalize", s, 2);
-  g_launches++;
+  const uint8_t* fin_outcomes = (a.op == kOpErase || n == 0) ? nullptr : a.outcomes;
+  volatile unsigned* skew_hint = (!t.dual && !cas && n > 0) ? ws.skew_dev : nullptr;
+  // a batch that moves values finalises in k_values_write (its last kernel)
+  const bool fin_in_values = !inplace && n > 0 && a.op != kOpErase;
+  if (!fin_in_values) {
+    ktimer_begin("finalize", s, 2);
+    launch_pdl(k_finalize, dim3(kFinBlocks), dim3(1024), 0, s, t, ws.sc, fin_outcomes, n, clock_advance, 0, skew_hint);
+    ktimer_end("finalize", s, 2);
+    g_launches++;
+  }
   long long* nev = reinterpret_cast<long long*>(n_evicted);
   if (collect && n > 0) {
     ktimer_begin("evict_select", s, 2);
@@ -1029,9 +1045,15 @@ cudaError_t run_mutation(const TableDev& t, OpArgs a, int64_t n, int log2_bucket
     const int64_t wblocks = (((n + 3) / 4) * kG + 255) / 256;
     const int64_t wcap = (int64_t)num_sms * 8 * 4;
     const unsigned wb = (unsigned)(wblocks < wcap ? (wblocks < 1 ? 1 : wblocks) : wcap);
-    if (vr == 4) launch_pdl(k_values_write<4, 4>, dim3(wb), dim3(256), 0, s, t, a.values, ws.vrow, n, ws.sc);
-    else if (vr == 2) launch_pdl(k_values_write<2, 4>, dim3(wb), dim3(256), 0, s, t, a.values, ws.vrow, n, ws.sc);
-    else launch_pdl(k_values_write<1, 4>, dim3(wb), dim3(256), 0, s, t, a.values, ws.vrow, n, ws.sc);
+    if (vr == 4)
+      launch_pdl(k_values_write<4, 4>, dim3(wb), dim3(256), 0, s, t, a.values, ws.vrow, n, ws.sc, fin_outcomes,
+                 (unsigned long long)clock_advance, skew_hint);
+    else if (vr == 2)
+      launch_pdl(k_values_write<2, 4>, dim3(wb), dim3(256), 0, s, t, a.values, ws.vrow, n, ws.sc, fin_outcomes,
+                 (unsigned long long)clock_advance, skew_hint);
+    else
+      launch_pdl(k_values_write<1, 4>, dim3(wb), dim3(256), 0, s, t, a.values, ws.vrow, n, ws.sc, fin_outcomes,
+                 (unsigned long long)clock_advance, skew_hint);
     ktimer_end("values_write", s);
     g_launches++;
   }
