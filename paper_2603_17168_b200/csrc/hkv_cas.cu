@@ -401,8 +401,8 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
             retry = true;  // an op holds the minimum slot: rescan next round
           } else {
             if (a.collect) {
-              a.ek[2 * i] = victim;
-              a.es[2 * i] = minv;
+              a.ek[kRecU64 * i] = victim;
+              a.es[kRecU64 * i] = minv;
             }
             t.digests[row] = (uint8_t)d;
             *sptr(t, row) = s_in;

@@ -230,8 +230,8 @@ __device__ __forceinline__ void process_op(const TableDev& t, const OpArgs& a,
     float* vr = value_row(t, row);
     if (a.collect) {
       if (r == ol) {
-        a.ek[2 * i] = *kptr(t, row);
-        a.es[2 * i] = minv;
+        a.ek[kRecU64 * i] = *kptr(t, row);
+        a.es[kRecU64 * i] = minv;
       }
       copy_row<kG, VEC>(a.ev + (uint64_t)i * dim, vr, dim, r);
       ctr[row < t.fast_rows ? kVFast : kVOver]++;

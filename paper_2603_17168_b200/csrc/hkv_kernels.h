@@ -8,6 +8,8 @@
 
 namespace hkv {
 
+constexpr int kRecU64 = 4, kRecU32 = 8;  // stride of the per-op read record (32 B)
+
 // Per-batch device scalars (zeroed by the launcher before each batch).
 struct Scalars {
   int err;                       // sentinel key seen in this batch
@@ -58,13 +60,17 @@ struct Workspace {
   int64_t agg_cap = 0;
   uint64_t* skeys = nullptr; // single mode: keys in sorted (bucket, batch index) order
   uint32_t* vrow = nullptr;  // single mode: destination row of final value writers
+  // Per-op value-read record, 32 B (one sector per op that reads a row):
+  // {victim key, victim score, row, provenance}.  ek / es / rrow / rsrc are
+  // strided views into it: ek[kRecU64 * i], rrow[kRecU32 * i], ...
+  uint64_t* rrec = nullptr;
   uint32_t* rrow = nullptr;  // single mode: row of a value read
   int32_t* rsrc = nullptr;   // single mode: provenance of a value read (-1 = pre-batch row)
   int* lwtab = nullptr;      // single mode: per-thread last-writer tables of the metadata pass
   uint32_t* b2 = nullptr;    // dual: second bucket
   uint32_t* pend = nullptr;  // dual: second pending list
-  uint64_t* ek = nullptr;  // per-op victim (key, score) pairs: ek[2i], ek[2i + 1] (= es[2i])
-  uint64_t* es = nullptr;  // ek + 1 (not a separate allocation)
+  uint64_t* ek = nullptr;  // victim key of op i at ek[kRecU64 * i] (view of rrec)
+  uint64_t* es = nullptr;  // victim score at es[kRecU64 * i] (view of rrec)
   float* ev = nullptr;
   // dual mode: 2n (bucket, op) pairs and per-op ranks (hkv_dual.cu)
   int64_t dcap = 0;
@@ -92,7 +98,7 @@ struct OpArgs {
   const uint64_t* scores;
   const uint64_t* ticks;
   uint8_t* outcomes;
-  uint64_t* ek;  // per-op evicted (key, score) scratch (collect): ek[2i], es[2i] with es = ek + 1
+  uint64_t* ek;  // per-op evicted (key, score) scratch (collect): ek[kRecU64 * i], es[kRecU64 * i]
   uint64_t* es;
   float* ev;
   int op;        // 0 insert_or_assign, 1 find_or_insert, 2 erase

@@ -462,16 +462,16 @@ __global__ void __launch_bounds__(256) k_values_read(TableDev t, float* __restri
         i = list[j];
         dst[u] = reinterpret_cast<V*>(ev + j * (int64_t)dim);
         if (r == 0) {
-          ek[j] = ek_tmp[2 * i];
-          es[j] = es_tmp[2 * i];
+          ek[j] = ek_tmp[kRecU64 * i];
+          es[j] = es_tmp[kRecU64 * i];
         }
       } else {
         i = (uint32_t)j;
         if (outcomes[i] != kFound) continue;
         dst[u] = reinterpret_cast<V*>(values + (uint64_t)i * dim);
       }
-      const int32_t src = rsrc[i];
-      from[u] = reinterpret_cast<const V*>(src < 0 ? value_row(t, rrow[i]) : values + (uint64_t)src * dim);
+      const int32_t src = rsrc[kRecU32 * i];
+      from[u] = reinterpret_cast<const V*>(src < 0 ? value_row(t, rrow[kRecU32 * i]) : values + (uint64_t)src * dim);
     }
     for (int e0 = r; e0 < nv; e0 += kG * 2) {
       V x[KPT][2];
@@ -522,8 +522,8 @@ __global__ void k_evict_gather(const Scalars* sc, const uint32_t* __restrict__ l
   for (int64_t j = gid; j < ne; j += ngroups) {
     const uint32_t i = list[j];
     if (r == 0) {
-      ek[j] = ek_tmp[2 * i];
-      es[j] = es_tmp[2 * i];
+      ek[j] = ek_tmp[kRecU64 * i];
+      es[j] = es_tmp[kRecU64 * i];
     }
     copy_row<kG, VEC>(ev + j * dim, ev_tmp + (uint64_t)i * dim, dim, r);
   }
@@ -741,8 +741,13 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual
     const int64_t c = n + n / 4 + 1024;
     if ((e = grow(ws.bkt, c)) || (e = grow(ws.idx, c)) || (e = grow(ws.sbkt, c)) || (e = grow(ws.sidx, c)) ||
         (e = grow(ws.seg, c)) || (e = grow(ws.aux, c)) || (e = grow(ws.aux2, c)) || (e = grow(ws.skey, 3 * c)) || (e = grow(ws.lrec, 3 * (c / kLongSeg + 1))) ||
-        (e = grow(ws.vrow, c)) || (e = grow(ws.rrow, c)) || (e = grow(ws.rsrc, c)) || (e = grow(ws.skeys, c)) || (e = grow(ws.segd, 4 * c)))
+        (e = grow(ws.vrow, c)) || (e = grow(ws.rrec, kRecU64 * c)) || (e = grow(ws.skeys, c)) || (e = grow(ws.segd, 4 * c)))
       return e;
+    // the op's value-read record: victim key, victim score, row, provenance
+    ws.ek = ws.rrec;
+    ws.es = ws.rrec + 1;
+    ws.rrow = reinterpret_cast<uint32_t*>(ws.rrec + 2);
+    ws.rsrc = reinterpret_cast<int32_t*>(ws.rrec + 2) + 1;
     if (ws.b2) { cudaFree(ws.b2); ws.b2 = nullptr; }
     if (ws.pend) { cudaFree(ws.pend); ws.pend = nullptr; }
     ws.cap_n = c;
@@ -751,12 +756,7 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual
     if ((e = grow(ws.b2, ws.cap_n)) || (e = grow(ws.pend, ws.cap_n))) return e;
   }
   // ev_mode: 1 = per-op victim key/score scratch, 2 = also victim value rows (dual mode)
-  if (ev_mode >= 1 && ws.cap_ek < n) {
-    // victim (key, score) of op i at ek[2i], ek[2i + 1]: one sector per eviction
-    if ((e = grow(ws.ek, 2 * ws.cap_n))) return e;
-    ws.es = ws.ek + 1;
-    ws.cap_ek = ws.cap_n;
-  }
+
   if (ev_mode >= 2 && (ws.cap_ev < n || ws.dim != dim)) {
     if ((e = grow(ws.ev, ws.cap_n * dim))) return e;
     ws.cap_ev = ws.cap_n;
@@ -794,11 +794,10 @@ cudaError_t ws_reserve(Workspace& ws, int64_t n, int dim, int ev_mode, bool dual
 
 void ws_free(Workspace& ws) {
   ws_free_dual(ws);
-  void* ptrs[] = {ws.bkt, ws.idx, ws.sbkt, ws.sidx, ws.seg, ws.aux, ws.aux2, ws.skey, ws.lrec, ws.agg, ws.skeys, ws.vrow, ws.rrow,
+  void* ptrs[] = {ws.bkt, ws.idx, ws.sbkt, ws.sidx, ws.seg, ws.aux, ws.aux2, ws.skey, ws.lrec, ws.agg, ws.skeys, ws.vrow, ws.rrec,
                   ws.lwtab,
-                  ws.rsrc,
                   ws.b2, ws.pend,
-                  ws.ek, ws.ev, ws.cub_tmp, ws.sc, ws.col, ws.segd};
+                  ws.ev, ws.cub_tmp, ws.sc, ws.col, ws.segd};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ws.skew_host) cudaFreeHost((void*)ws.skew_host);
@@ -878,10 +877,10 @@ __global__ void k_run_ends_fix(int64_t n, uint32_t* __restrict__ run_end, const 
 }
 
 static cudaError_t run_ends(Workspace& ws, int64_t n, cudaStream_t s) {
-  // tile_first lives in ws.rrow: the metadata pass that fills rrow runs after both kernels
+  // tile_first lives in ws.idx: the sort consumed it
   const int64_t ntiles = (n + kRunTile - 1) / kRunTile;
-  launch_pdl(k_run_ends_tile, dim3((unsigned)ntiles), dim3(kRunThreads), 0, s, ws.aux2, n, ws.seg, ws.rrow, ws.sc);
-  launch_pdl(k_run_ends_fix, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, n, ws.seg, ws.rrow, ntiles, ws.sc);
+  launch_pdl(k_run_ends_tile, dim3((unsigned)ntiles), dim3(kRunThreads), 0, s, ws.aux2, n, ws.seg, ws.idx, ws.sc);
+  launch_pdl(k_run_ends_fix, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, n, ws.seg, ws.idx, ntiles, ws.sc);
   g_launches += 2;
   return cudaGetLastError();
 }

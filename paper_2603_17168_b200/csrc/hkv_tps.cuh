@@ -16,7 +16,7 @@ namespace hkv {
 // stay bit-exact the pass records, per op:
 //   vrow[i]  destination row when op i is the LAST writer of that row in its
 //            segment (a later writer of the same slot retires the earlier one)
-//   rrow[i], rsrc[i]  for value reads (find_or_insert hits, insert_and_evict
+//   rrow[8i], rsrc[8i]  for value reads (find_or_insert hits, insert_and_evict
 //            victims): the row, and the op whose input currently sits in that
 //            row (-1 = the row's content before the batch)
 // The last writer of a slot comes from a short scan back through the
@@ -421,8 +421,8 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
       if (s_in >= gmin) {  // the single-bucket path admits ties (table.py:1083)
         const int m = 16 * gi + ms;
         if constexpr (COLLECT) {
-          a.ek[2 * i] = bkey<C>(t, S, m);
-          a.es[2 * i] = gmin;
+          a.ek[kRecU64 * i] = bkey<C>(t, S, m);
+          a.es[kRecU64 * i] = gmin;
         }
         set_bkey<C>(t, S, m, key);
         set_bdigest<C>(t, S, m, d);
@@ -447,8 +447,8 @@ __device__ __forceinline__ int tps_op(const TableDev& t, const OpArgs& a, TpsSta
   // value plan (provenance read BEFORE this op's own write is recorded)
   if (rslot >= 0) {
     ctr[rowbase + rslot < t.fast_rows ? kVFast : kVOver]++;
-    st_keep(rrow + i, (uint32_t)(rowbase + rslot), S.pol);
-    st_keep(rsrc + i, bit128(S.wm, rslot) ? lw_get(S, rslot, q - 1) : -1, S.pol);
+    st_keep(rrow + kRecU32 * i, (uint32_t)(rowbase + rslot), S.pol);
+    st_keep(rsrc + kRecU32 * i, bit128(S.wm, rslot) ? lw_get(S, rslot, q - 1) : -1, S.pol);
   }
   if (wslot >= 0) {
     ctr[rowbase + wslot < t.fast_rows ? kVFast : kVOver]++;
@@ -522,8 +522,8 @@ __device__ __forceinline__ void tps_run(const TableDev& t, const OpArgs& a, TpsS
     const int src = bit128(S.wm, res) ? lw_get(S, res, q) : -1;
     for (int64_t p = q + 1; p <= qe; p++) {
       const uint32_t j = sidx[p];
-      st_keep(rrow + j, (uint32_t)row, S.pol);
-      st_keep(rsrc + j, src, S.pol);
+      st_keep(rrow + kRecU32 * j, (uint32_t)row, S.pol);
+      st_keep(rsrc + kRecU32 * j, src, S.pol);
     }
   }
 }
