@@ -383,17 +383,21 @@ def run_extras(a, tables, torch, hkv, W):
     torch.cuda.empty_cache()
     # --- dual mode (C2 shape) ---
     for lam in (0.5, 1.0):
-        t = hkv.CacheTable(hkv.TableConfig(capacity=cap, value_dim=dim, mode="dual", workers=8))
+        # filled by the serial engine (it keeps the eviction summary exact, as
+        # a workers=1 table does in use); both engines then start from the
+        # same snapshot
+        t = hkv.CacheTable(hkv.TableConfig(capacity=cap, value_dim=dim, mode="dual", workers=1))
         t.validate_keys = False
         _fill(t, lam, cap, dim, B, torch, W)
         t.snapshot()
         key = f"dual_{lam:.2f}"
         ex[f"{key}_lambda_actual"] = round(t.load_factor(), 4)
         ms, o = _timed(torch, lambda r: t.insert_or_assign(fresh[r], vals), reps, after=t.restore)
+        ex[f"{key}_insert_or_assign"] = _rec(ms, B, {"outcomes": _mix(torch, o)})
+        t.set_workers(8)
+        ms, o = _timed(torch, lambda r: t.insert_or_assign(fresh[r], vals), reps, after=t.restore)
         ex[f"{key}_cas_insert_or_assign"] = _rec(ms, B, {"outcomes": _mix(torch, o)})
         t.set_workers(1)
-        ms, o = _timed(torch, lambda r: t.insert_or_assign(fresh[r], vals), reps, after=t.restore)
-        ex[f"{key}_insert_or_assign"] = _rec(ms, B, {"outcomes": _mix(torch, o)})
         res = torch.from_numpy(t.occupied_keys().view(np.int64)).cuda()
         hits = res[torch.randint(0, res.numel(), (B,), device="cuda", generator=gen)]
         del res
