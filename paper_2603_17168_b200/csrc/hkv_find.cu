@@ -118,6 +118,12 @@ __global__ void __launch_bounds__(256) k_find_tpk(TableDev t, const uint64_t* __
 // both sides).  Warps of a block are in different phases at any time, so
 // probe latency overlaps other warps' value traffic without a second pass
 // over the keys.
+#ifndef HKV_FIND_U
+#define HKV_FIND_U 8     // 16-B row vectors per lane in flight in the value gather
+#endif
+#ifndef HKV_FIND_BPS
+#define HKV_FIND_BPS 8   // resident blocks per SM of the fused find (persistent grid)
+#endif
 template <bool kZero, int U>
 __global__ void __launch_bounds__(256) k_find_fused(TableDev t, const uint64_t* __restrict__ keys, int64_t n,
                                                     uint8_t* __restrict__ found, float* __restrict__ out) {
@@ -294,11 +300,11 @@ void launch_find(const TableDev& t, const uint64_t* keys, int64_t n, float* out,
   } else if ((t.dim % 4) == 0 && (((uintptr_t)out & 15) == 0) && (((uintptr_t)t.vfast & 15) == 0) &&
              (((uintptr_t)t.vover & 15) == 0) && !(getenv("HKV_FIND") && std::string(getenv("HKV_FIND")) != "fused")) {
     int64_t blocks = (n + 255) / 256;
-    const int64_t max_blocks = (int64_t)num_sms * 8;
+    const int64_t max_blocks = (int64_t)num_sms * HKV_FIND_BPS;
     if (blocks > max_blocks) blocks = max_blocks;
     if (blocks < 1) blocks = 1;
-    if (mode == 3) k_find_fused<true, 8><<<(unsigned)blocks, 256, 0, s>>>(t, keys, n, found, out);
-    else k_find_fused<false, 8><<<(unsigned)blocks, 256, 0, s>>>(t, keys, n, found, out);
+    if (mode == 3) k_find_fused<true, HKV_FIND_U><<<(unsigned)blocks, 256, 0, s>>>(t, keys, n, found, out);
+    else k_find_fused<false, HKV_FIND_U><<<(unsigned)blocks, 256, 0, s>>>(t, keys, n, found, out);
     g_launches++;
   } else {
     launch_probe<4>(t, keys, n, found, nullptr, nullptr, rows, s, num_sms);
