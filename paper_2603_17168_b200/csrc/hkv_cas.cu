@@ -88,22 +88,31 @@ __device__ __forceinline__ void unlock_bucket(unsigned* locks, uint64_t b, unsig
   st_release_u32(locks + b, from + 2);
 }
 
+// A bucket's probe state: digest-candidate mask (digest equal, slot occupied)
+// and the occupancy words it was built from.
+struct Cand {
+  uint32_t c[4];
+  uint4 occ;
+};
+__device__ __forceinline__ Cand load_cand(const TableDev& t, uint64_t b, uint32_t d) {
+  Cand r;
+  const uint4* dp = reinterpret_cast<const uint4*>(t.digests + b * kSlots);
+  r.occ = __ldcg(reinterpret_cast<const uint4*>(t.bits + b * 4));
+  const uint32_t occ[4] = {r.occ.x, r.occ.y, r.occ.z, r.occ.w};
+  uint4 w[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) w[k] = __ldcg(dp + k);
+#pragma unroll
+  for (int q = 0; q < 4; q++)
+    r.c[q] = (t.digest_filter ? (match16(w[2 * q], d) | (match16(w[2 * q + 1], d) << 16)) : ~0u) & occ[q];
+  return r;
+}
+
 // Lock-free probe of bucket b by one thread: slot of `key`, -1 (absent), or
 // kBusy (a digest candidate is LOCKED: an op holds it mid-update).  Compares
 // counted as table.py:243-268 (candidates in slot order, up to the match).
-__device__ __forceinline__ int probe_cas(const TableDev& t, uint64_t b, uint64_t key, uint32_t d, ctr_t& ncmp) {
-  const uint4* dp = reinterpret_cast<const uint4*>(t.digests + b * kSlots);
-  const uint4 ow = __ldcg(reinterpret_cast<const uint4*>(t.bits + b * 4));
-  const uint32_t occ[4] = {ow.x, ow.y, ow.z, ow.w};
-  uint32_t c[4];
-  {
-    uint4 w[8];
-#pragma unroll
-    for (int k = 0; k < 8; k++) w[k] = __ldcg(dp + k);
-#pragma unroll
-    for (int q = 0; q < 4; q++)
-      c[q] = (t.digest_filter ? (match16(w[2 * q], d) | (match16(w[2 * q + 1], d) << 16)) : ~0u) & occ[q];
-  }
+__device__ __forceinline__ int probe_cand(const TableDev& t, uint64_t b, const Cand& cd, uint64_t key, ctr_t& ncmp) {
+  const uint32_t* c = cd.c;
   bool busy = false;
 #pragma unroll
   for (int q = 0; q < 4; q++) {
@@ -124,11 +133,79 @@ __device__ __forceinline__ int probe_cas(const TableDev& t, uint64_t b, uint64_t
   return busy ? kBusy : -1;
 }
 
+// An op's probe: both buckets' lines in flight at once; dual mode consults
+// (and counts) b2 only when b1 misses (_vec_lookup, table.py:284-300).
+// o1 / o2: the occupancy words the probe saw.
+__device__ __forceinline__ int probe_op(const TableDev& t, uint64_t b1, uint64_t b2, uint64_t key, uint32_t d,
+                                        ctr_t* ctr, uint64_t& hb, uint4& o1, uint4& o2) {
+  const Cand c1 = load_cand(t, b1, d);
+  Cand c2 = c1;
+  if (t.dual) c2 = load_cand(t, b2, d);
+  o1 = c1.occ;
+  o2 = c2.occ;
+  hb = b1;
+  int slot = probe_cand(t, b1, c1, key, ctr[kCompares]);
+  ctr[kLoads]++;
+  if (slot == -1 && t.dual) {
+    hb = b2;
+    slot = probe_cand(t, b2, c2, key, ctr[kCompares]);
+    ctr[kLoads]++;
+  }
+  return slot;
+}
+
+// A full bucket's minimum through the eviction summary, by one thread that
+// holds the bucket's lock: exact groups come from the 64-B summary line, the
+// others are rescanned (16 pairs each) and made exact.  gmin = the bucket's
+// minimum, gi = the lowest group holding it (groups are in slot order, so the
+// group's first slot holding gmin is np.argmin's first index, table.py:1080).
+//
+// svalid under this engine: bits 0-7 group valid, bits 8-31 a generation that
+// every hit's score write bumps (then clears its group's bit).  The rescans
+// are validated by a CAS from the word read before them, so a hit whose score
+// write the rescan may have missed either fails that CAS (its bump landed
+// first) or clears the bit after it -- a valid group never holds a minimum
+// above its true one.
+__device__ __forceinline__ void summ_min_thread(const TableDev& t, uint64_t b, uint64_t& gmin, int& gi) {
+  const uint32_t sv0 = ld_acquire_u32(t.svalid + b);
+  const uint32_t inv = ~sv0 & 0xFFu;
+  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(t.smin + b * 8);
+  uint64_t sm[8];
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const ulonglong2 x = __ldcg(p + k);
+    sm[2 * k] = x.x;
+    sm[2 * k + 1] = x.y;
+  }
+  if (inv) {
+#pragma unroll
+    for (int g = 0; g < 8; g++) {
+      if ((inv >> g) & 1u) {
+        const ulonglong2* gp = reinterpret_cast<const ulonglong2*>(kptr(t, b * kSlots + 16 * g));
+        uint64_t mn = kMaxScore;
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+          const uint64_t x = __ldcg(gp + k).y;
+          mn = x < mn ? x : mn;
+        }
+        sm[g] = mn;
+        t.smin[b * 8 + g] = mn;
+      }
+    }
+    atomicCAS(t.svalid + b, sv0, sv0 | inv);
+  }
+  gmin = sm[0];
+  gi = 0;
+#pragma unroll
+  for (int k = 1; k < 8; k++)
+    if (sm[k] < gmin) { gmin = sm[k]; gi = k; }
+}
+
 // ---------------------------------------------------------------------------
 // Warp-synchronous rounds.  A warp owns 32 ops (one per lane).  Each round,
 // every unfinished op makes one NON-BLOCKING attempt: probe; hit -> CAS the
-// slot; miss -> try the bucket lock(s), claim a free slot or (after a
-// warp-cooperative score scan) CAS the victim, write the slot's metadata and
+// slot; miss -> try the bucket lock(s), claim a free slot or (after the
+// full-bucket decision through the eviction summary) CAS the victim, write the slot's metadata and
 // drop the bucket lock(s) -- the slot itself stays LOCKED.  Then the warp
 // moves every claimed op's value row with coalesced copies, fences, and
 // publishes the keys.  An op that met a LOCKED candidate, a held lock or a
@@ -137,48 +214,6 @@ __device__ __forceinline__ int probe_cas(const TableDev& t, uint64_t b, uint64_t
 // ---------------------------------------------------------------------------
 enum : int { kTaskNone = 0, kTaskHit = 1, kTaskRead = 2, kTaskInsert = 3, kTaskEvict = 4 };
 constexpr unsigned kFullMask = 0xFFFFFFFFu;
-#ifndef HKV_CAS_SCANB
-#define HKV_CAS_SCANB 2
-#endif
-constexpr int kScanBatch = HKV_CAS_SCANB;  // full-bucket scans per warp pass
-
-// first-index minimum (np.argmin, table.py:1080) of bucket b's 128 scores,
-// read by the whole warp (lane j: slots 4j..4j+3, 1 KB coalesced)
-__device__ __forceinline__ void warp_min(const TableDev& t, uint64_t b, int lane, uint64_t& minv, int& mslot) {
-  const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(kptr(t, b * kSlots + 4 * lane));
-  const uint64_t s0 = __ldcg(sp).y, s1 = __ldcg(sp + 1).y, s2 = __ldcg(sp + 2).y, s3 = __ldcg(sp + 3).y;
-  uint64_t v = s0;
-  int m = 4 * lane;
-  if (s1 < v) { v = s1; m = 4 * lane + 1; }
-  if (s2 < v) { v = s2; m = 4 * lane + 2; }
-  if (s3 < v) { v = s3; m = 4 * lane + 3; }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t ov = __shfl_xor_sync(kFullMask, v, o);
-    const int om = __shfl_xor_sync(kFullMask, m, o);
-    if (ov < v || (ov == v && om < m)) { v = ov; m = om; }
-  }
-  minv = v;
-  mslot = m;
-}
-
-// first-index minimum over a bucket whose 128 scores the warp holds four
-// per lane (x, y = slots 4 lane .. 4 lane + 3)
-__device__ __forceinline__ void lane_min4(ulonglong2 x, ulonglong2 y, int lane, uint64_t& minv, int& mslot) {
-  uint64_t v = x.x;
-  int m = 4 * lane;
-  if (x.y < v) { v = x.y; m = 4 * lane + 1; }
-  if (y.x < v) { v = y.x; m = 4 * lane + 2; }
-  if (y.y < v) { v = y.y; m = 4 * lane + 3; }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t ov = __shfl_xor_sync(kFullMask, v, o);
-    const int om = __shfl_xor_sync(kFullMask, m, o);
-    if (ov < v || (ov == v && om < m)) { v = ov; m = om; }
-  }
-  minv = v;
-  mslot = m;
-}
 
 // the warp copies the rows of every lane in `mask`: dst/src per lane
 template <int VEC>
@@ -254,13 +289,8 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
         const unsigned seen_lo = ld_acquire_u32(locks + lo);
         const unsigned seen_hi = hi != lo ? ld_acquire_u32(locks + hi) : 0u;
         uint64_t hb = b1;
-        slot = probe_cas(t, b1, key, d, ctr[kCompares]);
-        ctr[kLoads]++;
-        if (slot == -1 && t.dual) {
-          hb = b2;
-          slot = probe_cas(t, b2, key, d, ctr[kCompares]);
-          ctr[kLoads]++;
-        }
+        uint4 w1, w2;
+        slot = probe_op(t, b1, b2, key, d, ctr, hb, w1, w2);
         if (slot == -1) {
           // try the bucket lock(s) once; from the value seen before the
           // probe, the probe stands, else probe again under the lock
@@ -290,16 +320,7 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
           if (!retry) {
             locked = true;
             from_lo &= 0x7FFFFFFFu;
-            if (!(same_lo && same_hi)) {
-              hb = b1;
-              slot = probe_cas(t, b1, key, d, ctr[kCompares]);
-              ctr[kLoads]++;
-              if (slot == -1 && t.dual) {
-                hb = b2;
-                slot = probe_cas(t, b2, key, d, ctr[kCompares]);
-                ctr[kLoads]++;
-              }
-            }
+            if (!(same_lo && same_hi)) slot = probe_op(t, b1, b2, key, d, ctr, hb, w1, w2);
           }
         }
         if (retry || slot == kBusy) {
@@ -310,15 +331,14 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
           if (cas_key(t, row, key)) {
             const uint64_t old = hit_needs_old(t.policy) ? __ldcg(sptr(t, row)) : 0;
             *sptr(t, row) = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
-            summ_invalidate(t, hb, slot);
             task = a.op == kOpFindOrInsert ? kTaskRead : kTaskHit;
           } else {
             retry = true;
           }
         } else {
+          // the occupancy the probe under the lock(s) saw stands: only
+          // structural changes move it, and they hold the bucket lock
           s_in = insert_score(t.policy, a.epoch, tick, cs);
-          const uint4 w1 = __ldcg(reinterpret_cast<const uint4*>(t.bits + b1 * 4));
-          const uint4 w2 = t.dual ? __ldcg(reinterpret_cast<const uint4*>(t.bits + b2 * 4)) : w1;
           const int o1 = __popc(w1.x) + __popc(w1.y) + __popc(w1.z) + __popc(w1.w);
           const int o2 = t.dual ? __popc(w2.x) + __popc(w2.y) + __popc(w2.z) + __popc(w2.w) : kSlots;
           if (o1 < kSlots || o2 < kSlots) {
@@ -337,77 +357,73 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
             t.bits[tb * 4 + q] = ws[q] | (1u << (slot & 31));
             t.digests[row] = (uint8_t)d;
             *sptr(t, row) = s_in;
-            t.svalid[tb] = 0u;
+            // the summary is consulted only while the bucket is full: the
+            // insert that fills it marks every group unknown
+            if ((first ? o1 : o2) + 1 == kSlots) t.svalid[tb] = 0u;
             task = kTaskInsert;
           } else {
             need_scan = true;
           }
         }
       }
-      // ---- warp-cooperative score scans for full-bucket decisions ----
-      unsigned sm = __ballot_sync(kFullMask, need_scan);
-      while (sm) {
-        // kScanBatch ops' buckets per pass, all loads in flight before the reductions
-        int ls[kScanBatch];
-        uint64_t p1[kScanBatch], p2[kScanBatch];
-#pragma unroll
-        for (int k = 0; k < kScanBatch; k++) {
-          ls[k] = sm ? __ffs(sm) - 1 : -1;
-          if (sm) sm &= sm - 1;
-          p1[k] = __shfl_sync(kFullMask, b1, ls[k] < 0 ? 0 : ls[k]);
-          p2[k] = __shfl_sync(kFullMask, b2, ls[k] < 0 ? 0 : ls[k]);
-        }
-        ulonglong2 x1[kScanBatch], y1[kScanBatch], x2[kScanBatch], y2[kScanBatch];
-#pragma unroll
-        for (int k = 0; k < kScanBatch; k++) {
-          if (ls[k] < 0) continue;
-          const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(kptr(t, p1[k] * kSlots + 4 * lane));
-          x1[k] = make_ulonglong2(__ldcg(sp).y, __ldcg(sp + 1).y);
-          y1[k] = make_ulonglong2(__ldcg(sp + 2).y, __ldcg(sp + 3).y);
-          if (t.dual) {
-            const ulonglong2* sq = reinterpret_cast<const ulonglong2*>(kptr(t, p2[k] * kSlots + 4 * lane));
-            x2[k] = make_ulonglong2(__ldcg(sq).y, __ldcg(sq + 1).y);
-            y2[k] = make_ulonglong2(__ldcg(sq + 2).y, __ldcg(sq + 3).y);
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < kScanBatch; k++) {
-          if (ls[k] < 0) continue;
-          uint64_t n1, n2 = kMaxScore;
-          int m1, m2 = 0;
-          lane_min4(x1[k], y1[k], lane, n1, m1);
-          if (t.dual) lane_min4(x2[k], y2[k], lane, n2, m2);
-          if (lane == ls[k]) {
-            if (!t.dual) {
-              ctr[kScans]++;
-              minv = n1, slot = m1, tb = b1;
-            } else {
-              ctr[kScans] += 2;
-              const bool use2 = n2 < n1;  // D2: the bucket with the lower minimum
-              minv = use2 ? n2 : n1, slot = use2 ? m2 : m1, tb = use2 ? b2 : b1;
-            }
-          }
-        }
-      }
+      // ---- full-bucket decisions through the eviction summary ----
       if (need_scan) {
+        // first-index minimum of each bucket (table.py:1079-1083, 1099-1104)
+        int gi;
+        summ_min_thread(t, b1, minv, gi);
+        tb = b1;
+        ctr[kScans]++;
+        if (t.dual) {
+          uint64_t n2;
+          int g2;
+          summ_min_thread(t, b2, n2, g2);
+          ctr[kScans]++;
+          if (n2 < minv) {  // D2: the bucket with the lower minimum
+            minv = n2;
+            gi = g2;
+            tb = b2;
+          }
+        }
         const bool admit = t.dual ? (t.admit_unified ? s_in >= minv : s_in > minv) : s_in >= minv;
         if (!admit) {
           outcome = kRejected;
           done = true;
         } else {
-          row = tb * kSlots + slot;
-          victim = ld_key(t, row);
-          if (victim == kLockedKey || !cas_key(t, row, victim)) {
-            retry = true;  // an op holds the minimum slot: rescan next round
+          // the victim's group: its 16 pairs give the first slot holding the
+          // minimum and, after the replacement, the group's new minimum
+          const ulonglong2* gp = reinterpret_cast<const ulonglong2*>(kptr(t, tb * kSlots + 16 * gi));
+          uint64_t v[16];
+#pragma unroll
+          for (int k = 0; k < 16; k++) v[k] = __ldcg(gp + k).y;
+          uint64_t mn = v[0];
+          int ms = 0;
+#pragma unroll
+          for (int k = 1; k < 16; k++)
+            if (v[k] < mn) { mn = v[k]; ms = k; }
+          if (mn != minv) {
+            // a hit moved the group's minimum after the summary was read:
+            // record the exact value and decide again next round
+            t.smin[tb * 8 + gi] = mn;
+            retry = true;
           } else {
-            if (a.collect) {
-              a.ek[kRecU64 * i] = victim;
-              a.es[kRecU64 * i] = minv;
+            row = tb * kSlots + 16 * gi + ms;
+            victim = ld_key(t, row);
+            if (victim == kLockedKey || !cas_key(t, row, victim)) {
+              retry = true;  // an op holds the minimum slot: decide again next round
+            } else {
+              if (a.collect) {
+                a.ek[kRecU64 * i] = victim;
+                a.es[kRecU64 * i] = minv;
+              }
+              t.digests[row] = (uint8_t)d;
+              *sptr(t, row) = s_in;
+              uint64_t nm = s_in;
+#pragma unroll
+              for (int k = 0; k < 16; k++)
+                if (k != ms && v[k] < nm) nm = v[k];
+              t.smin[tb * 8 + gi] = nm;  // the group stays exact
+              task = kTaskEvict;
             }
-            t.digests[row] = (uint8_t)d;
-            *sptr(t, row) = s_in;
-            t.svalid[tb] = 0u;
-            task = kTaskEvict;
           }
         }
       }
@@ -436,6 +452,12 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
       __syncwarp();
       fence_rel();  // rows (every lane's stores) before the keys
       __syncwarp();
+      if (task == kTaskHit || task == kTaskRead) {
+        // the score write is fenced above: bump the generation, then drop
+        // the group's bit (in this order, see summ_min_thread)
+        atomicAdd(t.svalid + row / kSlots, 0x100u);
+        atomicAnd(t.svalid + row / kSlots, ~(1u << ((row % kSlots) >> 4)));
+      }
       if (task != kTaskNone) st_release_u64(kptr(t, row), key);
       if (!__any_sync(kFullMask, task != kTaskNone) && !__all_sync(kFullMask, done)) {
         if (++idle_rounds > 2) __nanosleep(64);

@@ -183,8 +183,18 @@ __global__ void __launch_bounds__(kTpsThreads, HKV_TPS_MINB) k_meta_tps(TableDev
   // ahead of the segment that compares them
   auto prefetch_keys = [&](const SegRec& r, const uint4* L, uint64_t& k0, uint64_t& k1, int& nk) {
     nk = 0;
-    if (!t.digest_filter) return;
     const uint32_t* O = reinterpret_cast<const uint32_t*>(L + 8);
+#if HKV_SUMM_PREFETCH
+    // a full bucket's op reads the eviction summary: start it towards L2 a
+    // segment ahead (no registers held)
+    if (OP != kOpErase && (O[0] & O[1] & O[2] & O[3]) == 0xFFFFFFFFu) {
+      const char* sp = reinterpret_cast<const char*>(t.smin + (uint64_t)r.b * 8);
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(sp));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(sp + 32));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(t.svalid + r.b));
+    }
+#endif
+    if (!t.digest_filter) return;
     const uint32_t d = r.flags >> 8;
     int s0 = -1, s1 = -1;
 #pragma unroll

@@ -91,6 +91,9 @@ __device__ __forceinline__ uint64_t run_hit_score(int policy, uint64_t old, uint
 #ifndef HKV_TPS_STAGES
 #define HKV_TPS_STAGES 2  // line buffers per thread in k_meta_tps (2 or 3)
 #endif
+#ifndef HKV_SUMM_PREFETCH
+#define HKV_SUMM_PREFETCH 1  // L2 prefetch of a full bucket's summary one segment ahead
+#endif
 #ifndef HKV_TPS_MINB
 #define HKV_TPS_MINB 2  // resident blocks per SM the metadata pass is compiled for
 #endif
