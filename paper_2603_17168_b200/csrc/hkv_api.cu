@@ -438,11 +438,6 @@ int hkv_set_workers(hkv_table* t, int32_t workers) {
         (e = cudaMemset(t->locks, 0, (size_t)t->buckets * 4)) || (e = cudaDeviceSynchronize()))
       return fail(HKV_ENOMEM, "bucket lock allocation failed");
   }
-  // the serial engines rely on exact summary groups; the concurrent engine's
-  // may be conservatively low after racing hits, so leaving it drops them
-  if (workers == 1 && t->cfg.workers > 1 &&
-      ((e = cudaMemset(t->svalid, 0, (size_t)t->buckets * 4)) || (e = cudaDeviceSynchronize())))
-    return cuda_fail(e, "summary reset");
   t->cfg.workers = workers;
   t->dev.cas = workers > 1;
   t->dev.locks = t->locks;

@@ -6,28 +6,26 @@
 // contention, so tests check the policy invariants.
 //
 // One THREAD per op (HKV's TLPv1 shape): an op's chain is a
-// handful of dependent round trips (probe, lock, claim, publish), so what
-// pays is the number of ops in flight -- 32 per warp instead of 4 with an
-// 8-lane tile (measured: 1M hits 0.51 -> see DESIGN.md).
-//   probe      lock-free: the 128-B digest line and the 16-B occupancy word,
-//              candidate keys in slot order.  A candidate whose key is LOCKED
-//              may be this very key mid-update: the probe retries until it
-//              resolves.
-//   hit        CAS key -> LOCKED on the matched slot (a lost race retries the
-//              whole op), refresh the score, write (or, find_or_insert, read)
-//              the value row, release-store the key back (_scalar_hit,
+// handful of dependent round trips, so what pays is the number of ops in
+// flight and the length of each chain.  Every op first takes its bucket
+// lock(s) with non-blocking acquire CASes (dual: both at once), then works
+// the bucket(s) exclusively -- the lock is what makes a short chain possible:
+//   probe      the 128-B digest line(s) and 16-B occupancy word(s), both
+//              buckets' in flight at once, candidate keys in slot order.
+//   hit        claim key -> LOCKED, refresh the score, write (or,
+//              find_or_insert, read) the value row (_scalar_hit,
 //              table.py:749-772).
-//   miss       take the bucket lock(s) (dual: both, lower index first), probe
-//              again under it (a same-key insert may have won meanwhile),
-//              then the structural change the reference does under its stripe
-//              lock: claim the lowest free slot EMPTY -> LOCKED, or pick the
-//              first-index minimum score, admit, CAS the victim old -> LOCKED
-//              (a slot a hit holds is waited out and rescanned), capture the
-//              evicted tuple, publish digest, score, value and the key last
-//              (_publish_entry, table.py:737-747); release the lock(s).
-// Bucket locks serialise only structural changes of one bucket; hits never
-// wait on them.  Compiled with -dlcm=cg: metadata another SM just published
-// must not be served from a stale L1 line.
+//   miss       claim the lowest free slot EMPTY -> LOCKED, or take the
+//              first-index minimum through the eviction summary (the victim's
+//              16-score group read once), admit, claim the victim old ->
+//              LOCKED and capture the evicted tuple (table.py:678-693,
+//              775-857).
+// The round's fence then orders metadata and rows before the key is
+// published (key last, _publish_entry table.py:737-747) and the locks drop.
+// Readers never run beside this kernel (the triple-group gate), so the
+// LOCKED state only guards the publish order.  Compiled with -dlcm=cg:
+// metadata another SM just published must not be served from a stale L1
+// line.
 #include "hkv_kernels.h"
 #include "hkv_probe.cuh"
 
@@ -42,21 +40,13 @@ __device__ __forceinline__ void fence_rel() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 #endif
 }
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ unsigned cas_acquire_u32(unsigned* p, unsigned cmp, unsigned val) {
   unsigned old;
   asm volatile("atom.acquire.gpu.global.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "l"(p), "r"(cmp), "r"(val) : "memory");
   return old;
 }
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint64_t ld_key(const TableDev& t, uint64_t row) {
 #ifdef HKV_CAS_KEYLDCG
@@ -65,27 +55,18 @@ __device__ __forceinline__ uint64_t ld_key(const TableDev& t, uint64_t row) {
   return *(volatile const uint64_t*)kptr(t, row);
 #endif
 }
-__device__ __forceinline__ bool cas_key(const TableDev& t, uint64_t row, uint64_t expect) {
-  return atomicCAS((unsigned long long*)kptr(t, row), (unsigned long long)expect,
-                   (unsigned long long)kLockedKey) == (unsigned long long)expect;
-}
 
-// Bucket locks are sequence locks: even = free, odd = held; every holder
-// advances the word by 2 (lock +1, unlock +1).  An op reads the word before
-// its lock-free probe; if it can take the lock from that same even value, no
-// structural change touched the bucket in between and the probe stands (no
-// second probe under the lock).
-__device__ __forceinline__ unsigned lock_bucket(unsigned* locks, uint64_t b, unsigned seen, bool& unchanged) {
-  unchanged = (seen & 1u) == 0 && cas_acquire_u32(locks + b, seen, seen + 1) == seen;
-  if (unchanged) return seen;
-  for (;;) {
-    const unsigned v = ld_acquire_u32(locks + b);
-    if ((v & 1u) == 0 && cas_acquire_u32(locks + b, v, v + 1) == v) return v;
-    __nanosleep(64);
-  }
+// Bucket locks: 0 free, 1 held; taken by a non-blocking acquire CAS, dropped
+// by a relaxed store after the round's fence.
+__device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void unlock_bucket(unsigned* locks, uint64_t b, unsigned from) {
-  st_release_u32(locks + b, from + 2);
+// The slot claim of the reference's protocol (table.py:678-693, 775-857):
+// key `expect` -> LOCKED.  Every structural change and every hit holds the
+// slot's bucket lock, so the claim cannot lose and its result is not waited
+// on; the entry is published (key last) after the round's fence.
+__device__ __forceinline__ void claim_slot(const TableDev& t, uint64_t row, uint64_t expect) {
+  atomicCAS((unsigned long long*)kptr(t, row), (unsigned long long)expect, (unsigned long long)kLockedKey);
 }
 
 // A bucket's probe state: digest-candidate mask (digest equal, slot occupied)
@@ -155,19 +136,13 @@ __device__ __forceinline__ int probe_op(const TableDev& t, uint64_t b1, uint64_t
 }
 
 // A full bucket's minimum through the eviction summary, by one thread that
-// holds the bucket's lock: exact groups come from the 64-B summary line, the
-// others are rescanned (16 pairs each) and made exact.  gmin = the bucket's
-// minimum, gi = the lowest group holding it (groups are in slot order, so the
-// group's first slot holding gmin is np.argmin's first index, table.py:1080).
-//
-// svalid under this engine: bits 0-7 group valid, bits 8-31 a generation that
-// every hit's score write bumps (then clears its group's bit).  The rescans
-// are validated by a CAS from the word read before them, so a hit whose score
-// write the rescan may have missed either fails that CAS (its bump landed
-// first) or clears the bit after it -- a valid group never holds a minimum
-// above its true one.
+// holds the bucket's lock (every score write of this engine does): exact
+// groups come from the 64-B summary line, the others are rescanned (16
+// scores each) and made exact.  gmin = the bucket's minimum, gi = the lowest
+// group holding it (groups are in slot order, so the group's first slot
+// holding gmin is np.argmin's first index, table.py:1080).
 __device__ __forceinline__ void summ_min_thread(const TableDev& t, uint64_t b, uint64_t& gmin, int& gi) {
-  const uint32_t sv0 = ld_acquire_u32(t.svalid + b);
+  const uint32_t sv0 = __ldcg(t.svalid + b);
   const uint32_t inv = ~sv0 & 0xFFu;
   const ulonglong2* p = reinterpret_cast<const ulonglong2*>(t.smin + b * 8);
   uint64_t sm[8];
@@ -192,7 +167,7 @@ __device__ __forceinline__ void summ_min_thread(const TableDev& t, uint64_t b, u
         t.smin[b * 8 + g] = mn;
       }
     }
-    atomicCAS(t.svalid + b, sv0, sv0 | inv);
+    t.svalid[b] = sv0 | inv;
   }
   gmin = sm[0];
   gi = 0;
@@ -203,14 +178,14 @@ __device__ __forceinline__ void summ_min_thread(const TableDev& t, uint64_t b, u
 
 // ---------------------------------------------------------------------------
 // Warp-synchronous rounds.  A warp owns 32 ops (one per lane).  Each round,
-// every unfinished op makes one NON-BLOCKING attempt: probe; hit -> CAS the
-// slot; miss -> try the bucket lock(s), claim a free slot or (after the
-// full-bucket decision through the eviction summary) CAS the victim, write the slot's metadata and
-// drop the bucket lock(s) -- the slot itself stays LOCKED.  Then the warp
-// moves every claimed op's value row with coalesced copies, fences, and
-// publishes the keys.  An op that met a LOCKED candidate, a held lock or a
-// lost CAS simply tries again next round; nothing is ever waited on while a
-// lock or a LOCKED slot is held, so the rounds cannot deadlock.
+// every unfinished op makes one NON-BLOCKING attempt: try its bucket lock(s);
+// holding them, probe, and claim the hit slot, the lowest free slot or (after
+// the full-bucket decision through the eviction summary) the victim, writing
+// the slot's metadata.  Then the warp moves every claimed op's value row with
+// coalesced copies, fences, publishes the keys and drops the locks.  An op
+// that met a held lock or an unpublished (LOCKED) candidate tries again next
+// round; locks are only ever kept across rounds in bucket order (the lower
+// one while the higher one is busy), so the rounds cannot deadlock.
 // ---------------------------------------------------------------------------
 enum : int { kTaskNone = 0, kTaskHit = 1, kTaskRead = 2, kTaskInsert = 3, kTaskEvict = 4 };
 constexpr unsigned kFullMask = 0xFFFFFFFFu;
@@ -247,11 +222,24 @@ __device__ __forceinline__ void warp_copy_rows(unsigned mask, float* dst, const 
   }
 }
 
+#ifndef HKV_CAS_STAGE
+#define HKV_CAS_STAGE 1
+#endif
 #ifndef HKV_CAS_MINB
 #define HKV_CAS_MINB 2
 #endif
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+// stage_dim > 0: each warp stages its 32 ops' input rows (contiguous in the
+// batch) into shared memory with cp.async when it takes the chunk, so the
+// row writes of the rounds are stores only (no dependent global load)
 template <int VEC>
-__global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, OpArgs a, unsigned* locks, int64_t n) {
+__global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, OpArgs a, unsigned* locks, int64_t n,
+                                                                  int stage_dim) {
+  extern __shared__ uint4 cas_rows[];
   if (a.sc->err) return;
   const int lane = threadIdx.x & 31;
   const uint64_t clock0 = *t.clock;
@@ -277,160 +265,144 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
     }
     const uint64_t lo = b1 < b2 ? b1 : b2, hi = b1 < b2 ? b2 : b1;
     float* vin = done ? nullptr : a.values + (uint64_t)i * dim;
+    const float* vsrc = vin;  // the row this op writes from
+    if (stage_dim) {
+      uint4* wrows = cas_rows + (size_t)(threadIdx.x / 32) * 32 * (stage_dim / 4);
+      const int64_t cnt = n - base < 32 ? n - base : 32;
+      const uint4* g = reinterpret_cast<const uint4*>(a.values + (uint64_t)base * dim);
+      __syncwarp();  // the previous chunk's rows are consumed
+      for (int k = lane; k < (int)cnt * (dim / 4); k += 32) cp_async16(wrows + k, g + k);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      vsrc = reinterpret_cast<const float*>(wrows + lane * (dim / 4));
+    }
+    bool staged = stage_dim == 0;
+    bool have_lo = false;    // the lower bucket's lock, kept while the higher one is busy
+    bool contended = false;  // lost the lower bucket once: lock in order from now on
     uint8_t outcome = kRejected;
     unsigned idle_rounds = 0;
     while (__any_sync(kFullMask, !done)) {
       int task = kTaskNone;
-      bool need_scan = false, locked = false, retry = false;
-      unsigned from_lo = 0, from_hi = 0;
-      uint64_t row = 0, tb = b1, s_in = 0, victim = 0, minv = 0;
-      int slot = -1;
+      bool locked = false, retry = false;
+      uint64_t row = 0;
       if (!done) {
-        const unsigned seen_lo = ld_acquire_u32(locks + lo);
-        const unsigned seen_hi = hi != lo ? ld_acquire_u32(locks + hi) : 0u;
-        uint64_t hb = b1;
-        uint4 w1, w2;
-        slot = probe_op(t, b1, b2, key, d, ctr, hb, w1, w2);
-        if (slot == -1) {
-          // try the bucket lock(s) once; from the value seen before the
-          // probe, the probe stands, else probe again under the lock
-          const bool same_lo = (seen_lo & 1u) == 0 && cas_acquire_u32(locks + lo, seen_lo, seen_lo + 1) == seen_lo;
-          if (same_lo) {
-            from_lo = seen_lo;
-          } else {
-            const unsigned v = ld_acquire_u32(locks + lo);
-            if ((v & 1u) == 0 && cas_acquire_u32(locks + lo, v, v + 1) == v) from_lo = v | 0x80000000u;
-            else retry = true;
-          }
-          bool same_hi = true;
-          if (!retry && hi != lo) {
-            same_hi = (seen_hi & 1u) == 0 && cas_acquire_u32(locks + hi, seen_hi, seen_hi + 1) == seen_hi;
-            if (same_hi) {
-              from_hi = seen_hi;
-            } else {
-              const unsigned v = ld_acquire_u32(locks + hi);
-              if ((v & 1u) == 0 && cas_acquire_u32(locks + hi, v, v + 1) == v) {
-                from_hi = v;
-              } else {
-                unlock_bucket(locks, lo, from_lo & 0x7FFFFFFFu);
-                retry = true;
-              }
-            }
-          }
-          if (!retry) {
-            locked = true;
-            from_lo &= 0x7FFFFFFFu;
-            if (!(same_lo && same_hi)) slot = probe_op(t, b1, b2, key, d, ctr, hb, w1, w2);
-          }
+        // try the bucket lock(s).  Locks are taken in bucket order: an op
+        // may keep its lower bucket across rounds while it waits for the
+        // higher one, never the reverse, so holders form no cycle.  The first
+        // attempt issues both CASes at once; after a lost lower bucket the op
+        // touches its higher bucket only once the lower one is its own, so a
+        // hot pair's higher lock is left to the lower lock's holder.  Nothing
+        // waits inside a round.
+        unsigned glo = 0u, ghi = 0u;
+        if (!have_lo) {
+          glo = cas_acquire_u32(locks + lo, 0u, 1u);
+          if (hi != lo && (!contended || !glo)) ghi = cas_acquire_u32(locks + hi, 0u, 1u);
+        } else {
+          ghi = cas_acquire_u32(locks + hi, 0u, 1u);
         }
-        if (retry || slot == kBusy) {
+        if (glo) {
+          if (hi != lo && !contended && !ghi) st_relaxed_u32(locks + hi, 0u);
+          contended = true;
           retry = true;
-        } else if (slot >= 0) {
-          // hit (table.py:749-772): hold the slot
-          row = hb * kSlots + slot;
-          if (cas_key(t, row, key)) {
+        } else if (ghi) {
+          have_lo = true;
+          retry = true;
+        } else {
+          locked = true;
+          uint64_t hb = b1;
+          uint4 w1, w2;
+          int slot = probe_op(t, b1, b2, key, d, ctr, hb, w1, w2);
+          if (slot == kBusy) {
+            retry = true;  // a previous holder's entry is not published yet
+          } else if (slot >= 0) {
+            // hit (table.py:749-772): hold the slot, refresh the score
+            row = hb * kSlots + slot;
+            claim_slot(t, row, key);
             const uint64_t old = hit_needs_old(t.policy) ? __ldcg(sptr(t, row)) : 0;
             *sptr(t, row) = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
+            atomicAnd(t.svalid + hb, ~(1u << (slot >> 4)));  // the group's minimum may have moved
             task = a.op == kOpFindOrInsert ? kTaskRead : kTaskHit;
           } else {
-            retry = true;
-          }
-        } else {
-          // the occupancy the probe under the lock(s) saw stands: only
-          // structural changes move it, and they hold the bucket lock
-          s_in = insert_score(t.policy, a.epoch, tick, cs);
-          const int o1 = __popc(w1.x) + __popc(w1.y) + __popc(w1.z) + __popc(w1.w);
-          const int o2 = t.dual ? __popc(w2.x) + __popc(w2.y) + __popc(w2.z) + __popc(w2.w) : kSlots;
-          if (o1 < kSlots || o2 < kSlots) {
-            // free insert (table.py:678-693, 1165-1181): single -> b1, dual D1
-            const bool first = !t.dual || o1 <= o2;
-            tb = first ? b1 : b2;
-            const uint4 w = first ? w1 : w2;
-            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-            int q = 0;
-            while (ws[q] == 0xFFFFFFFFu) q++;
-            slot = 32 * q + __ffs(~ws[q]) - 1;  // the lowest EMPTY slot
-            row = tb * kSlots + slot;
-            // EMPTY -> LOCKED; under the bucket lock nothing else claims it
-            atomicCAS((unsigned long long*)kptr(t, row), (unsigned long long)kEmptyKey,
-                      (unsigned long long)kLockedKey);
-            t.bits[tb * 4 + q] = ws[q] | (1u << (slot & 31));
-            t.digests[row] = (uint8_t)d;
-            *sptr(t, row) = s_in;
-            // the summary is consulted only while the bucket is full: the
-            // insert that fills it marks every group unknown
-            if ((first ? o1 : o2) + 1 == kSlots) t.svalid[tb] = 0u;
-            task = kTaskInsert;
-          } else {
-            need_scan = true;
-          }
-        }
-      }
-      // ---- full-bucket decisions through the eviction summary ----
-      if (need_scan) {
-        // first-index minimum of each bucket (table.py:1079-1083, 1099-1104)
-        int gi;
-        summ_min_thread(t, b1, minv, gi);
-        tb = b1;
-        ctr[kScans]++;
-        if (t.dual) {
-          uint64_t n2;
-          int g2;
-          summ_min_thread(t, b2, n2, g2);
-          ctr[kScans]++;
-          if (n2 < minv) {  // D2: the bucket with the lower minimum
-            minv = n2;
-            gi = g2;
-            tb = b2;
-          }
-        }
-        const bool admit = t.dual ? (t.admit_unified ? s_in >= minv : s_in > minv) : s_in >= minv;
-        if (!admit) {
-          outcome = kRejected;
-          done = true;
-        } else {
-          // the victim's group: its 16 pairs give the first slot holding the
-          // minimum and, after the replacement, the group's new minimum
-          const ulonglong2* gp = reinterpret_cast<const ulonglong2*>(kptr(t, tb * kSlots + 16 * gi));
-          uint64_t v[16];
-#pragma unroll
-          for (int k = 0; k < 16; k++) v[k] = __ldcg(gp + k).y;
-          uint64_t mn = v[0];
-          int ms = 0;
-#pragma unroll
-          for (int k = 1; k < 16; k++)
-            if (v[k] < mn) { mn = v[k]; ms = k; }
-          if (mn != minv) {
-            // a hit moved the group's minimum after the summary was read:
-            // record the exact value and decide again next round
-            t.smin[tb * 8 + gi] = mn;
-            retry = true;
-          } else {
-            row = tb * kSlots + 16 * gi + ms;
-            victim = ld_key(t, row);
-            if (victim == kLockedKey || !cas_key(t, row, victim)) {
-              retry = true;  // an op holds the minimum slot: decide again next round
-            } else {
-              if (a.collect) {
-                a.ek[kRecU64 * i] = victim;
-                a.es[kRecU64 * i] = minv;
-              }
+            const uint64_t s_in = insert_score(t.policy, a.epoch, tick, cs);
+            const int o1 = __popc(w1.x) + __popc(w1.y) + __popc(w1.z) + __popc(w1.w);
+            const int o2 = t.dual ? __popc(w2.x) + __popc(w2.y) + __popc(w2.z) + __popc(w2.w) : kSlots;
+            if (o1 < kSlots || o2 < kSlots) {
+              // free insert (table.py:678-693, 1165-1181): single -> b1, dual D1
+              const bool first = !t.dual || o1 <= o2;
+              const uint64_t tb = first ? b1 : b2;
+              const uint4 w = first ? w1 : w2;
+              const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+              int q = 0;
+              while (ws[q] == 0xFFFFFFFFu) q++;
+              slot = 32 * q + __ffs(~ws[q]) - 1;  // the lowest EMPTY slot
+              row = tb * kSlots + slot;
+              claim_slot(t, row, kEmptyKey);
+              t.bits[tb * 4 + q] = ws[q] | (1u << (slot & 31));
               t.digests[row] = (uint8_t)d;
               *sptr(t, row) = s_in;
-              uint64_t nm = s_in;
+              // the summary is consulted only while the bucket is full: the
+              // insert that fills it marks every group unknown
+              if ((first ? o1 : o2) + 1 == kSlots) t.svalid[tb] = 0u;
+              task = kTaskInsert;
+            } else {
+              // full bucket(s): first-index minimum through the eviction
+              // summary (table.py:1079-1083; dual D2, table.py:1099-1104)
+              uint64_t minv, tb = b1;
+              int gi;
+              summ_min_thread(t, b1, minv, gi);
+              ctr[kScans]++;
+              if (t.dual) {
+                uint64_t n2;
+                int g2;
+                summ_min_thread(t, b2, n2, g2);
+                ctr[kScans]++;
+                if (n2 < minv) {  // the bucket with the lower minimum
+                  minv = n2;
+                  gi = g2;
+                  tb = b2;
+                }
+              }
+              const bool admit = t.dual ? (t.admit_unified ? s_in >= minv : s_in > minv) : s_in >= minv;
+              if (!admit) {
+                outcome = kRejected;
+                done = true;
+              } else {
+                // the victim's group: its 16 scores give the first slot holding
+                // the minimum and, after the replacement, the group's new minimum
+                const ulonglong2* gp = reinterpret_cast<const ulonglong2*>(kptr(t, tb * kSlots + 16 * gi));
+                uint64_t v[16];
 #pragma unroll
-              for (int k = 0; k < 16; k++)
-                if (k != ms && v[k] < nm) nm = v[k];
-              t.smin[tb * 8 + gi] = nm;  // the group stays exact
-              task = kTaskEvict;
+                for (int k = 0; k < 16; k++) v[k] = __ldcg(gp + k).y;
+                uint64_t mn = v[0];
+                int ms = 0;
+#pragma unroll
+                for (int k = 1; k < 16; k++)
+                  if (v[k] < mn) { mn = v[k]; ms = k; }
+                row = tb * kSlots + 16 * gi + ms;
+                const uint64_t victim = mn == minv ? ld_key(t, row) : kLockedKey;
+                if (victim == kLockedKey) {
+                  // (defensive: under the lock the summary is exact) or the
+                  // minimum slot's previous holder has not published it yet
+                  t.smin[tb * 8 + gi] = mn;
+                  retry = true;
+                } else {
+                  claim_slot(t, row, victim);
+                  if (a.collect) {
+                    a.ek[kRecU64 * i] = victim;
+                    a.es[kRecU64 * i] = minv;
+                  }
+                  t.digests[row] = (uint8_t)d;
+                  *sptr(t, row) = s_in;
+                  uint64_t nm = s_in;
+#pragma unroll
+                  for (int k = 0; k < 16; k++)
+                    if (k != ms && v[k] < nm) nm = v[k];
+                  t.smin[tb * 8 + gi] = nm;  // the group stays exact
+                  task = kTaskEvict;
+                }
+              }
             }
           }
         }
-      }
-      // structure is settled: drop the bucket locks (claimed slots stay LOCKED)
-      if (locked) {  // st.release: this thread's metadata writes before the unlock
-        if (hi != lo) unlock_bucket(locks, hi, from_hi);
-        unlock_bucket(locks, lo, from_lo);
       }
       if (retry) ctr[kRetries]++;
       // ---- warp-cooperative value movement ----
@@ -441,7 +413,14 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
       const unsigned rd_mask = __ballot_sync(kFullMask, task == kTaskRead);
       if (rd_mask) warp_copy_rows<VEC>(rd_mask, vin, vr, dim, lane);
       const unsigned wr_mask = __ballot_sync(kFullMask, task == kTaskHit || task == kTaskInsert || task == kTaskEvict);
-      if (wr_mask) warp_copy_rows<VEC>(wr_mask, vr, vin, dim, lane);
+      if (wr_mask) {
+        if (!staged) {
+          asm volatile("cp.async.wait_all;" ::: "memory");
+          __syncwarp();
+          staged = true;
+        }
+        warp_copy_rows<VEC>(wr_mask, vr, vsrc, dim, lane);
+      }
       if (task != kTaskNone) {
         ctr[row < t.fast_rows ? kVFast : kVOver] += (task == kTaskEvict && a.collect) ? 2 : 1;
         if (task == kTaskInsert) sd++;
@@ -449,16 +428,16 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
         outcome = task == kTaskHit ? kUpdated : task == kTaskRead ? kFound : task == kTaskInsert ? kInserted : kEvicted;
         done = true;
       }
+      // metadata and rows (every lane's stores) before the keys and the unlocks
       __syncwarp();
-      fence_rel();  // rows (every lane's stores) before the keys
+      fence_rel();
       __syncwarp();
-      if (task == kTaskHit || task == kTaskRead) {
-        // the score write is fenced above: bump the generation, then drop
-        // the group's bit (in this order, see summ_min_thread)
-        atomicAdd(t.svalid + row / kSlots, 0x100u);
-        atomicAnd(t.svalid + row / kSlots, ~(1u << ((row % kSlots) >> 4)));
+      if (task != kTaskNone) st_relaxed_u64(kptr(t, row), key);  // publish: the key last (table.py:742-747)
+      if (locked) {
+        st_relaxed_u32(locks + lo, 0u);
+        if (hi != lo) st_relaxed_u32(locks + hi, 0u);
+        have_lo = false;
       }
-      if (task != kTaskNone) st_release_u64(kptr(t, row), key);
       if (!__any_sync(kFullMask, task != kTaskNone) && !__all_sync(kFullMask, done)) {
         if (++idle_rounds > 2) __nanosleep(64);
       } else {
@@ -478,16 +457,25 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
 cudaError_t run_cas(const TableDev& t, OpArgs a, int64_t n, unsigned* locks, int vec, cudaStream_t s,
                     int num_sms) {
   void* fn = vec == 4 ? (void*)k_cas_upsert<4> : vec == 2 ? (void*)k_cas_upsert<2> : (void*)k_cas_upsert<1>;
+  // input-row staging: 8 warps x 32 rows per block, up to 64 KB (dim <= 64)
+  const int stage_dim = (vec == 4 && t.dim <= 64 && HKV_CAS_STAGE) ? t.dim : 0;
+  const size_t smem = (size_t)8 * 32 * stage_dim * 4;
+  static bool attr_set = false;
+  if (smem && !attr_set) {
+    for (void* f : {(void*)k_cas_upsert<4>, (void*)k_cas_upsert<2>, (void*)k_cas_upsert<1>})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 32 * 64 * 4);
+    attr_set = true;
+  }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
   if (e) return e;
   if (per_sm < 1) per_sm = 1;
   int64_t blocks = (int64_t)per_sm * num_sms;
   const int64_t want = (n + 255) / 256;
   if (blocks > want) blocks = want < 1 ? 1 : want;
-  if (vec == 4) k_cas_upsert<4><<<(unsigned)blocks, 256, 0, s>>>(t, a, locks, n);
-  else if (vec == 2) k_cas_upsert<2><<<(unsigned)blocks, 256, 0, s>>>(t, a, locks, n);
-  else k_cas_upsert<1><<<(unsigned)blocks, 256, 0, s>>>(t, a, locks, n);
+  if (vec == 4) k_cas_upsert<4><<<(unsigned)blocks, 256, smem, s>>>(t, a, locks, n, stage_dim);
+  else if (vec == 2) k_cas_upsert<2><<<(unsigned)blocks, 256, smem, s>>>(t, a, locks, n, stage_dim);
+  else k_cas_upsert<1><<<(unsigned)blocks, 256, smem, s>>>(t, a, locks, n, stage_dim);
   g_launches++;
   return cudaGetLastError();
 }

@@ -152,14 +152,12 @@ __global__ void k_consistency(TableDev t, int64_t buckets, int* ok_dev, unsigned
       }
     }
     if (occ != load_occ(t, b, r)) bad = 1;
-    // eviction summary of a full bucket: a group marked exact holds its
-    // minimum (the concurrent engine may leave it conservatively low after a
-    // racing hit raised a score: it rescans the victim's group before use)
+    // eviction summary of a full bucket: a group marked exact holds its minimum
     if (tile.sum((unsigned)__popc(occ)) == kSlots && ((t.svalid[b] >> r) & 1u)) {
       uint64_t gm = kMaxScore;
       for (int j = 0; j < kSPL; j++) gm = kp[2 * j + 1] < gm ? kp[2 * j + 1] : gm;
       const uint64_t sm = t.smin[b * 8 + r];
-      if (sm > gm || (!t.cas && sm != gm)) bad = 1;
+      if (sm != gm) bad = 1;
     }
     cnt += __popc(occ);
   }
