@@ -141,16 +141,25 @@ __device__ __forceinline__ int probe_op(const TableDev& t, uint64_t b1, uint64_t
 // scores each) and made exact.  gmin = the bucket's minimum, gi = the lowest
 // group holding it (groups are in slot order, so the group's first slot
 // holding gmin is np.argmin's first index, table.py:1080).
-__device__ __forceinline__ void summ_min_thread(const TableDev& t, uint64_t b, uint64_t& gmin, int& gi) {
-  const uint32_t sv0 = __ldcg(t.svalid + b);
-  const uint32_t inv = ~sv0 & 0xFFu;
+struct Summ {
+  ulonglong2 m[4];  // the 8 group minima
+  uint32_t sv;      // group valid bits
+};
+__device__ __forceinline__ Summ load_summ(const TableDev& t, uint64_t b) {
+  Summ s;
   const ulonglong2* p = reinterpret_cast<const ulonglong2*>(t.smin + b * 8);
+#pragma unroll
+  for (int k = 0; k < 4; k++) s.m[k] = __ldcg(p + k);
+  s.sv = __ldcg(t.svalid + b);
+  return s;
+}
+__device__ __forceinline__ void summ_min(const TableDev& t, uint64_t b, const Summ& s, uint64_t& gmin, int& gi) {
+  const uint32_t inv = ~s.sv & 0xFFu;
   uint64_t sm[8];
 #pragma unroll
   for (int k = 0; k < 4; k++) {
-    const ulonglong2 x = __ldcg(p + k);
-    sm[2 * k] = x.x;
-    sm[2 * k + 1] = x.y;
+    sm[2 * k] = s.m[k].x;
+    sm[2 * k + 1] = s.m[k].y;
   }
   if (inv) {
 #pragma unroll
@@ -167,7 +176,7 @@ __device__ __forceinline__ void summ_min_thread(const TableDev& t, uint64_t b, u
         t.smin[b * 8 + g] = mn;
       }
     }
-    t.svalid[b] = sv0 | inv;
+    t.svalid[b] = s.sv | inv;
   }
   gmin = sm[0];
   gi = 0;
@@ -222,6 +231,9 @@ __device__ __forceinline__ void warp_copy_rows(unsigned mask, float* dst, const 
   }
 }
 
+#ifndef HKV_CAS_SPEC
+#define HKV_CAS_SPEC 0
+#endif
 #ifndef HKV_CAS_STAGE
 #define HKV_CAS_STAGE 1
 #endif
@@ -245,6 +257,8 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
   const uint64_t clock0 = *t.clock;
   const bool fel_open = !*t.fel_set;
   const int dim = t.dim;
+  // at lambda > 0.97 a full bucket is the rule (as the metadata pass's spec)
+  const bool spec = HKV_CAS_SPEC && (unsigned long long)*t.size * 100ull > t.capacity * 97ull;
   ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
   int sd = 0;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x / 32);
@@ -310,6 +324,12 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
           locked = true;
           uint64_t hb = b1;
           uint4 w1, w2;
+          // when full buckets are the rule, the summaries travel with the probe
+          Summ s1, s2;
+          if (spec) {
+            s1 = load_summ(t, b1);
+            if (t.dual) s2 = load_summ(t, b2);
+          }
           int slot = probe_op(t, b1, b2, key, d, ctr, hb, w1, w2);
           if (slot == kBusy) {
             retry = true;  // a previous holder's entry is not published yet
@@ -346,14 +366,18 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
             } else {
               // full bucket(s): first-index minimum through the eviction
               // summary (table.py:1079-1083; dual D2, table.py:1099-1104)
+              if (!spec) {
+                s1 = load_summ(t, b1);
+                if (t.dual) s2 = load_summ(t, b2);
+              }
               uint64_t minv, tb = b1;
               int gi;
-              summ_min_thread(t, b1, minv, gi);
+              summ_min(t, b1, s1, minv, gi);
               ctr[kScans]++;
               if (t.dual) {
                 uint64_t n2;
                 int g2;
-                summ_min_thread(t, b2, n2, g2);
+                summ_min(t, b2, s2, n2, g2);
                 ctr[kScans]++;
                 if (n2 < minv) {  // the bucket with the lower minimum
                   minv = n2;

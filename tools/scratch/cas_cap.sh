@@ -10,3 +10,5 @@ ncu -i /tmp/cap/dual_$L.ncu-rep --page raw --csv > "$O/ncu_dual_cas_${L}_raw.csv
 ncu -i /tmp/cap/dual_$L.ncu-rep --page source --csv --kernel-name "regex:k_cas" > /tmp/cap/src_cas.csv 2>/dev/null &&
   python tools/ncu_src_top.py /tmp/cap/src_cas.csv 25 > "$O/src_top_k_cas_$L.txt" 2>&1
 echo done
+ncu -i /tmp/cap/dual_$L.ncu-rep --page source --print-source cuda,sass --csv --kernel-name "regex:k_cas" > /tmp/cap/srcl_cas.csv 2>/dev/null &&
+  python tools/ncu_cuda_lines.py /tmp/cap/srcl_cas.csv 40 > "$O/cuda_lines_k_cas_$L.txt" 2>&1
