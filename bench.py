@@ -463,6 +463,20 @@ def run_extras(a, tables, torch, hkv, W):
     ex["c4_dim64_find"] = _rec(ms, B, {"gbs_pcie": round(B * 256 / ms / 1e6, 1), "paper_h100_nvl_bkvs": 0.172})
     del t
     torch.cuda.empty_cache()
+    # the paper's Config D itself: dim 64, 128M slots,
+    # half the value rows in HBM and half in mapped host memory
+    t = hkv.CacheTable(hkv.TableConfig(capacity=cap, value_dim=64, fast_tier_budget=cap // 256))
+    t.validate_keys = False
+    _fill(t, 0.5, cap, 64, B, torch, W)
+    res = torch.from_numpy(t.occupied_keys().view(np.int64)).cuda()
+    hits = res[torch.randint(0, res.numel(), (B,), device="cuda", generator=gen)]
+    del res
+    ms, o = _timed(torch, lambda r: t.find(hits), reps)
+    ex["c4_configD_find"] = _rec(ms, B, {"capacity": cap, "fast_tier_rows": cap // 2, "paper_h100_nvl_bkvs": 0.172})
+    ms, o = _timed(torch, lambda r: t.find_ptr(hits), reps)
+    ex["c4_configD_find_ptr"] = _rec(ms, B, {"paper_h100_nvl_bkvs": 6.949})
+    del t
+    torch.cuda.empty_cache()
     return ex
 
 def run_single(a):

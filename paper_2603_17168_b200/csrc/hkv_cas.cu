@@ -231,6 +231,9 @@ __device__ __forceinline__ void warp_copy_rows(unsigned mask, float* dst, const 
   }
 }
 
+#ifndef HKV_CAS_EARLY_UNLOCK
+#define HKV_CAS_EARLY_UNLOCK 0  // measured: fewer retries, but the extra fence costs more
+#endif
 #ifndef HKV_CAS_SPEC
 #define HKV_CAS_SPEC 0
 #endif
@@ -428,6 +431,17 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
           }
         }
       }
+#if HKV_CAS_EARLY_UNLOCK
+      // structure settled: the locks drop before the row copies (the claimed
+      // slot stays LOCKED until its key is published after the round fence)
+      if (locked) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        st_relaxed_u32(locks + lo, 0u);
+        if (hi != lo) st_relaxed_u32(locks + hi, 0u);
+        have_lo = false;
+        locked = false;
+      }
+#endif
       if (retry) ctr[kRetries]++;
       // ---- warp-cooperative value movement ----
       float* vr = task != kTaskNone ? value_row(t, row) : nullptr;
