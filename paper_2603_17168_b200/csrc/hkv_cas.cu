@@ -490,6 +490,222 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_cas_upsert(TableDev t, Op
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(t.size, (unsigned long long)v);
 }
 
+
+// ---------------------------------------------------------------------------
+// Deterministic dual mode in warp-synchronous rounds (workers == 1): serial
+// batch-order semantics.  Every op has its rank in the
+// batch-ordered op list of each of its buckets (run_dual's prep); a bucket's
+// turn counter says how many of its ops are done.  Each round an op whose
+// buckets' turns have reached its ranks runs -- exclusively: no other op of
+// those buckets can be ready -- with the same thread-per-op chain as the
+// concurrent engine (both probe lines in flight, D1 / D2 through the
+// eviction summary), the warp writes the rows, fences and advances the
+// turns.  Ops are taken in batch order in 32-op chunks, so the lowest
+// pending op is always in some warp's current chunk and ready: progress.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64v(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(256, HKV_CAS_MINB) k_dual_rounds(TableDev t, OpArgs a,
+                                                                   const uint32_t* __restrict__ rank,
+                                                                   unsigned long long* turn, unsigned long long tag,
+                                                                   int64_t n, int stage_dim) {
+  extern __shared__ uint4 cas_rows[];
+  if (a.sc->err) return;
+  const int lane = threadIdx.x & 31;
+  const uint64_t clock0 = *t.clock;
+  const bool fel_open = !*t.fel_set;
+  const int dim = t.dim;
+  const bool erase = a.op == kOpErase;
+  ctr_t ctr[6] = {0, 0, 0, 0, 0, 0};
+  int sd = 0;
+  unsigned* next = &a.sc->npend[0];
+  for (;;) {
+    int64_t base = 0;
+    if (lane == 0) base = (int64_t)atomicAdd(next, 32u);
+    base = __shfl_sync(kFullMask, base, 0);
+    if (base >= n) break;
+    const int64_t i = base + lane;
+    bool done = i >= n, ready = false;
+    uint64_t key = 0, b1 = 0, b2 = 0, tick = 0, cs = 0;
+    uint32_t d = 0, r1 = 0, r2 = 0;
+    if (!done) {
+      key = a.keys[i];
+      const uint64_t h = fmix64(key);
+      d = digest_of(h);
+      b1 = h & t.mask;
+      b2 = second_hash(h) & t.mask;
+      r1 = rank[2 * i];
+      r2 = b2 == b1 ? 0u : rank[2 * i + 1];
+      tick = a.ticks ? a.ticks[i] : clock0 + (uint64_t)i + 1;
+      cs = a.scores ? a.scores[i] : 0;
+    }
+    float* vin = done || erase ? nullptr : a.values + (uint64_t)i * dim;
+    const float* vsrc = vin;
+    if (stage_dim && !erase) {
+      uint4* wrows = cas_rows + (size_t)(threadIdx.x / 32) * 32 * (stage_dim / 4);
+      const int64_t cnt = n - base < 32 ? n - base : 32;
+      const uint4* g = reinterpret_cast<const uint4*>(a.values + (uint64_t)base * dim);
+      __syncwarp();  // the previous chunk's rows are consumed
+      for (int k = lane; k < (int)cnt * (dim / 4); k += 32) cp_async16(wrows + k, g + k);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      vsrc = reinterpret_cast<const float*>(wrows + lane * (dim / 4));
+    }
+    unsigned idle_rounds = 0;
+    while (__any_sync(kFullMask, !done)) {
+      int task = kTaskNone;
+      bool ran = false;
+      uint64_t row = 0;
+      uint8_t outcome = kRejected;
+      if (!done && !ready) {
+        // the turn loads acquire: the bucket state they follow was fenced
+        // before the previous op of the bucket advanced them
+        const bool ok1 = r1 == 0 || ld_acquire_u64(turn + b1) >= (tag | r1);
+        const bool ok2 = b2 == b1 || r2 == 0 || ld_acquire_u64(turn + b2) >= (tag | r2);
+        ready = ok1 && ok2;
+      }
+      if (!done && ready) {
+        ran = true;
+        uint64_t hb = b1;
+        uint4 w1, w2;
+        int slot = probe_op(t, b1, b2, key, d, ctr, hb, w1, w2);
+        if (erase) {
+          // _round_erase, table.py:1017-1023: key -> EMPTY; digest/score/value stay stale
+          if (slot >= 0) {
+            row = hb * kSlots + slot;
+            *kptr(t, row) = kEmptyKey;
+            const uint4 w = hb == b1 ? w1 : w2;
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+            t.bits[hb * 4 + (slot >> 5)] = ws[slot >> 5] & ~(1u << (slot & 31));
+            sd--;
+            outcome = kErased;
+          } else {
+            outcome = kNotFound;
+          }
+        } else if (slot >= 0) {
+          // hit: table.py:1045-1062
+          row = hb * kSlots + slot;
+          const uint64_t old = hit_needs_old(t.policy) ? __ldcg(sptr(t, row)) : 0;
+          *sptr(t, row) = hit_score(t.policy, old, a.epoch, tick, a.scores != nullptr, cs);
+          atomicAnd(t.svalid + hb, ~(1u << (slot >> 4)));
+          task = a.op == kOpFindOrInsert ? kTaskRead : kTaskHit;
+        } else {
+          const uint64_t s_in = insert_score(t.policy, a.epoch, tick, cs);
+          const int o1 = __popc(w1.x) + __popc(w1.y) + __popc(w1.z) + __popc(w1.w);
+          const int o2 = __popc(w2.x) + __popc(w2.y) + __popc(w2.z) + __popc(w2.w);
+          if (o1 < kSlots || o2 < kSlots) {
+            // D1 (table.py:1089-1095): the less occupied bucket, b1 on ties;
+            // its lowest EMPTY slot (table.py:1171)
+            const bool first = o1 <= o2;
+            const uint64_t tb = first ? b1 : b2;
+            const uint4 w = first ? w1 : w2;
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+            int q = 0;
+            while (ws[q] == 0xFFFFFFFFu) q++;
+            slot = 32 * q + __ffs(~ws[q]) - 1;
+            row = tb * kSlots + slot;
+            *kptr(t, row) = key;
+            t.bits[tb * 4 + q] = ws[q] | (1u << (slot & 31));
+            t.digests[row] = (uint8_t)d;
+            *sptr(t, row) = s_in;
+            if ((first ? o1 : o2) + 1 == kSlots) t.svalid[tb] = 0u;
+            sd++;
+            task = kTaskInsert;
+          } else {
+            // D2 (table.py:1096-1119): the bucket with the lower minimum
+            const Summ s1 = load_summ(t, b1), s2 = load_summ(t, b2);
+            uint64_t minv, n2, tb = b1;
+            int gi, g2;
+            summ_min(t, b1, s1, minv, gi);
+            summ_min(t, b2, s2, n2, g2);
+            ctr[kScans] += 2;
+            if (n2 < minv) {
+              minv = n2;
+              gi = g2;
+              tb = b2;
+            }
+            const bool admit = t.admit_unified ? s_in >= minv : s_in > minv;
+            if (admit) {
+              const ulonglong2* gp = reinterpret_cast<const ulonglong2*>(kptr(t, tb * kSlots + 16 * gi));
+              uint64_t v[16];
+#pragma unroll
+              for (int k = 0; k < 16; k++) v[k] = __ldcg(gp + k).y;
+              uint64_t mn = v[0];
+              int ms = 0;
+#pragma unroll
+              for (int k = 1; k < 16; k++)
+                if (v[k] < mn) { mn = v[k]; ms = k; }
+              row = tb * kSlots + 16 * gi + ms;
+              if (a.collect) {
+                a.ek[kRecU64 * i] = __ldcg(kptr(t, row));
+                a.es[kRecU64 * i] = minv;
+              }
+              *kptr(t, row) = key;
+              t.digests[row] = (uint8_t)d;
+              *sptr(t, row) = s_in;
+              uint64_t nm = s_in;
+#pragma unroll
+              for (int k = 0; k < 16; k++)
+                if (k != ms && v[k] < nm) nm = v[k];
+              t.smin[tb * 8 + gi] = nm;  // the group stays exact
+              task = kTaskEvict;
+            }
+          }
+        }
+      }
+      // ---- warp-cooperative value movement (rows of this round's ops) ----
+      float* vr = task != kTaskNone ? value_row(t, row) : nullptr;
+      const unsigned cap_mask = __ballot_sync(kFullMask, task == kTaskEvict && a.collect);
+      if (cap_mask) warp_copy_rows<VEC>(cap_mask, a.collect && task == kTaskEvict ? a.ev + (uint64_t)i * dim : nullptr,
+                                        vr, dim, lane);
+      const unsigned rd_mask = __ballot_sync(kFullMask, task == kTaskRead);
+      if (rd_mask) warp_copy_rows<VEC>(rd_mask, vin, vr, dim, lane);
+      const unsigned wr_mask = __ballot_sync(kFullMask, task == kTaskHit || task == kTaskInsert || task == kTaskEvict);
+      if (wr_mask) {
+        if (stage_dim) {
+          asm volatile("cp.async.wait_all;" ::: "memory");
+          __syncwarp();
+        }
+        warp_copy_rows<VEC>(wr_mask, vr, vsrc, dim, lane);
+      }
+      if (task != kTaskNone) {
+        ctr[row < t.fast_rows ? kVFast : kVOver] += (task == kTaskEvict && a.collect) ? 2 : 1;
+        if (task == kTaskEvict && fel_open) atomicMin(&a.sc->first_ev, (unsigned)i);
+        outcome = task == kTaskHit ? kUpdated : task == kTaskRead ? kFound : task == kTaskInsert ? kInserted : kEvicted;
+      }
+      // metadata and rows (every lane's stores) before the turns advance
+      const bool any_ran = __any_sync(kFullMask, ran);
+      if (any_ran) {
+        __syncwarp();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        __syncwarp();
+      }
+      if (ran) {
+        a.outcomes[i] = outcome;
+        st_relaxed_u64v(turn + b1, tag | (r1 + 1));
+        if (b2 != b1) st_relaxed_u64v(turn + b2, tag | (r2 + 1));
+        done = true;
+      }
+      if (!any_ran && !__all_sync(kFullMask, done)) {
+        if (++idle_rounds > 2) __nanosleep(64);
+      } else {
+        idle_rounds = 0;
+      }
+    }
+  }
+  flush_counters<256>(t.counters, ctr, 6);
+  long long v = sd;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(t.size, (unsigned long long)v);
+}
+
 }  // namespace
 
 cudaError_t run_cas(const TableDev& t, OpArgs a, int64_t n, unsigned* locks, int vec, cudaStream_t s,
@@ -518,4 +734,31 @@ cudaError_t run_cas(const TableDev& t, OpArgs a, int64_t n, unsigned* locks, int
   return cudaGetLastError();
 }
 
+}  // namespace hkv
+
+namespace hkv {
+cudaError_t run_dual_rounds(const TableDev& t, OpArgs a, int64_t n, const uint32_t* rank, unsigned long long* turn,
+                            unsigned long long tag, int vec, cudaStream_t s, int num_sms) {
+  void* fn = vec == 4 ? (void*)k_dual_rounds<4> : vec == 2 ? (void*)k_dual_rounds<2> : (void*)k_dual_rounds<1>;
+  const int stage_dim = (vec == 4 && t.dim <= 64 && HKV_CAS_STAGE && a.op != kOpErase) ? t.dim : 0;
+  const size_t smem = (size_t)8 * 32 * stage_dim * 4;
+  static bool attr_set = false;
+  if (!attr_set) {
+    for (void* f : {(void*)k_dual_rounds<4>, (void*)k_dual_rounds<2>, (void*)k_dual_rounds<1>})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 32 * 64 * 4);
+    attr_set = true;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
+  if (e) return e;
+  if (per_sm < 1) per_sm = 1;
+  int64_t blocks = (int64_t)per_sm * num_sms;
+  const int64_t want = (n + 255) / 256;
+  if (blocks > want) blocks = want < 1 ? 1 : want;
+  if (vec == 4) k_dual_rounds<4><<<(unsigned)blocks, 256, smem, s>>>(t, a, rank, turn, tag, n, stage_dim);
+  else if (vec == 2) k_dual_rounds<2><<<(unsigned)blocks, 256, smem, s>>>(t, a, rank, turn, tag, n, stage_dim);
+  else k_dual_rounds<1><<<(unsigned)blocks, 256, smem, s>>>(t, a, rank, turn, tag, n, stage_dim);
+  g_launches++;
+  return cudaGetLastError();
+}
 }  // namespace hkv

@@ -16,6 +16,13 @@
 // applied by one 8-lane tile with process_op (exclusive ownership of both
 // buckets while it runs).
 //
+// The default consumer of these ranks and turns is k_dual_rounds
+// (hkv_cas.cu, HKV_DUAL_ROUNDS): the same handoff, but thread-per-op in
+// warp-synchronous rounds -- an op whose turns have not come simply tries
+// again next round -- so 32 ops per warp are in flight instead of 4, and the
+// warp moves its rows with coalesced copies.  k_dual_flow stays as the
+// reference point (HKV_DUAL_ROUNDS=0).
+//
 // This file is compiled with -dlcm=cg: a bucket written by one SM is read by
 // another right after the turn handoff, so global loads must not be served
 // from a stale L1 line.
@@ -272,6 +279,10 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+#ifndef HKV_DUAL_ROUNDS
+#define HKV_DUAL_ROUNDS 1  // 0: the 8-lane-tile turn-counter dataflow (k_dual_flow)
+#endif
+
 // 2n (bucket, code) pairs, code = 2i + which; a second bucket equal to the
 // first is parked at bucket `none` (sorts last, ignored).
 __global__ void k_dual_pairs(const uint32_t* __restrict__ b1s, const uint32_t* __restrict__ b2s, int64_t n,
@@ -357,6 +368,9 @@ cudaError_t run_dual(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, W
   k_dual_ranks<<<blk2, 256, 0, s>>>(ws.dsk, ws.dsv, ws.dpv, m, none, ws.drank);
   ktimer_end("dual_ranks", s, 2);
   g_launches += 10;
+#if HKV_DUAL_ROUNDS
+  return run_dual_rounds(t, a, n, ws.drank, turn, tag, vec, s, num_sms);
+#endif
   int per_sm = 0;
   void* fn = vec == 4 ? (void*)k_dual_flow<4> : vec == 2 ? (void*)k_dual_flow<2> : (void*)k_dual_flow<1>;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0))) return e;

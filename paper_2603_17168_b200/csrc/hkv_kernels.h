@@ -163,6 +163,9 @@ cudaError_t run_dual(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, W
                      unsigned long long* turn, unsigned long long tag, int vec, cudaStream_t s, int num_sms);
 void ws_free(Workspace& ws);
 // concurrent upserts (workers > 1): LOCKED-sentinel slot CAS + bucket locks
+// deterministic dual mode in warp-synchronous rounds over run_dual's ranks / turns (hkv_cas.cu)
+cudaError_t run_dual_rounds(const TableDev& t, OpArgs a, int64_t n, const uint32_t* rank, unsigned long long* turn,
+                            unsigned long long tag, int vec, cudaStream_t s, int num_sms);
 cudaError_t run_cas(const TableDev& t, OpArgs a, int64_t n, unsigned* locks, int vec, cudaStream_t s,
                     int num_sms);
 

@@ -177,11 +177,14 @@ def test_cas_contended_invariants(hkv, mode, policy):
     assert (oi == 4).all() and np.array_equal(vi, v)
 
 
-def test_cas_c2_shape_invariants(hkv):
+@pytest.mark.parametrize("mode", MODES)
+def test_cas_c2_shape_invariants(hkv, mode):
     """1M-key batches at 2^24 slots, dim 64, filled past lambda = 1 with the
-    CAS engine: invariants at scale, every resident key found with its row."""
+    concurrent engine (single and dual: full-bucket decisions through the
+    eviction summary, which check_consistency verifies group by group):
+    invariants at scale, every resident key found with its row."""
     cap, dim, B = 2**24, 64, 2**20
-    t = hkv.CacheTable(hkv.TableConfig(capacity=cap, value_dim=dim, workers=8))
+    t = hkv.CacheTable(hkv.TableConfig(capacity=cap, value_dim=dim, mode=mode, workers=8))
     total_ins = 0
     for j in range(20):
         keys = torch.arange(j * B + 1, (j + 1) * B + 1, device="cuda", dtype=torch.int64)
