@@ -31,6 +31,13 @@ for mode in modes:
         t.set_workers(8)
         ms, o = bench._timed(torch, lambda r: t.insert_or_assign(fresh[r], vals), reps, after=t.restore)
         out[f"{k}_cas"] = bench._rec(ms, B, {"outcomes": bench._mix(torch, o)})
+        t.set_workers(1)
+        res = torch.from_numpy(t.occupied_keys().view(np.int64)).cuda()
+        hits = res[torch.randint(0, res.numel(), (B,), device="cuda", generator=gen)]
+        del res
+        ms, _ = bench._timed(torch, lambda r: t.find(hits), reps)
+        out[f"{k}_find"] = bench._rec(ms, B)
+        t.set_workers(8)
         t.counters.reset()
         t.insert_or_assign(fresh[0], vals)
         out[f"{k}_cas"]["counters"] = t.counters.as_dict()
