@@ -279,6 +279,9 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+#ifndef HKV_DUAL_CSORT
+#define HKV_DUAL_CSORT 1  // counting-sort rank prep (0: radix sort of the 2n pairs)
+#endif
 #ifndef HKV_DUAL_ROUNDS
 #define HKV_DUAL_ROUNDS 1  // 0: the 8-lane-tile turn-counter dataflow (k_dual_flow)
 #endif
@@ -310,6 +313,45 @@ __global__ void k_dual_ranks(const uint32_t* __restrict__ sk, const uint32_t* __
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= m || sk[p] == none) return;
   rank[sv[p]] = (uint32_t)(p - first[p]);
+}
+
+// Counting-sort rank prep (HKV_DUAL_CSORT): the ranks need only each
+// bucket's references in batch order, and a bucket holds ~2 of them, so a
+// count / scan / scatter into per-bucket lists (all L2-resident: 4 B per
+// bucket, 4 B per reference) plus a count of smaller op indices inside the
+// reference's own short list replaces the radix sort of the 2n pairs.
+__global__ void k_dcount(const uint32_t* __restrict__ b1s, const uint32_t* __restrict__ b2s, int64_t n,
+                         uint32_t* __restrict__ cnt, const Scalars* sc) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || sc->err) return;
+  const uint32_t b1 = b1s[i], b2 = b2s[i];
+  atomicAdd(cnt + b1, 1u);
+  if (b2 != b1) atomicAdd(cnt + b2, 1u);
+}
+// list[off[b] .. off[b+1]) = codes 2i + which of bucket b's references (any order)
+__global__ void k_dscatter(const uint32_t* __restrict__ b1s, const uint32_t* __restrict__ b2s, int64_t n,
+                           const uint32_t* __restrict__ off, uint32_t* __restrict__ cnt, uint32_t* __restrict__ list,
+                           const Scalars* sc) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || sc->err) return;
+  const uint32_t b1 = b1s[i], b2 = b2s[i];
+  list[off[b1] + atomicSub(cnt + b1, 1u) - 1u] = (uint32_t)(2 * i);
+  if (b2 != b1) list[off[b2] + atomicSub(cnt + b2, 1u) - 1u] = (uint32_t)(2 * i + 1);
+}
+// rank of reference 2i + which = references of its bucket from smaller op indices
+__global__ void k_drank(const uint32_t* __restrict__ b1s, const uint32_t* __restrict__ b2s, int64_t n,
+                        const uint32_t* __restrict__ off, const uint32_t* __restrict__ list,
+                        uint32_t* __restrict__ rank, const Scalars* sc) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= 2 * n || sc->err) return;
+  const uint32_t i = (uint32_t)(p >> 1);
+  const uint32_t b1 = b1s[i], b2 = b2s[i];
+  if ((p & 1) && b2 == b1) return;
+  const uint32_t b = (p & 1) ? b2 : b1;
+  const uint32_t lo = off[b], hi = off[b + 1];
+  uint32_t r = 0;
+  for (uint32_t q = lo; q < hi; q++) r += (list[q] >> 1) < i;
+  rank[p] = r;
 }
 
 template <int VEC>
@@ -357,6 +399,20 @@ cudaError_t run_dual(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, W
   const uint32_t none = (uint32_t)(1ull << log2_buckets);
   const unsigned blk = (unsigned)((n + 255) / 256), blk2 = (unsigned)((m + 255) / 256);
   ktimer_begin("dual_ranks", s, 2);
+#if HKV_DUAL_CSORT
+  {
+    const int64_t nb = (int64_t)none;  // buckets
+    if ((e = cudaMemsetAsync(ws.dcnt, 0, (size_t)(nb + 1) * 4, s))) return e;
+    k_dcount<<<blk, 256, 0, s>>>(ws.bkt, ws.b2, n, ws.dcnt, ws.sc);
+    size_t sb = ws.dcub_bytes;
+    if ((e = cub::DeviceScan::ExclusiveSum(ws.dcub, sb, ws.dcnt, ws.doff, (int)(nb + 1), s))) return e;
+    k_dscatter<<<blk, 256, 0, s>>>(ws.bkt, ws.b2, n, ws.doff, ws.dcnt, ws.dpk, ws.sc);
+    k_drank<<<blk2, 256, 0, s>>>(ws.bkt, ws.b2, n, ws.doff, ws.dpk, ws.drank, ws.sc);
+    ktimer_end("dual_ranks", s, 2);
+    g_launches += 6;
+    if ((e = cudaGetLastError())) return e;
+  }
+#else
   k_dual_pairs<<<blk, 256, 0, s>>>(ws.bkt, ws.b2, n, none, ws.dpk, ws.dpv, ws.sc);
   size_t bytes = ws.dcub_bytes;
   if ((e = cub::DeviceRadixSort::SortPairs(ws.dcub, bytes, ws.dpk, ws.dsk, ws.dpv, ws.dsv, (int)m, 0,
@@ -368,6 +424,7 @@ cudaError_t run_dual(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, W
   k_dual_ranks<<<blk2, 256, 0, s>>>(ws.dsk, ws.dsv, ws.dpv, m, none, ws.drank);
   ktimer_end("dual_ranks", s, 2);
   g_launches += 10;
+#endif
 #if HKV_DUAL_ROUNDS
   return run_dual_rounds(t, a, n, ws.drank, turn, tag, vec, s, num_sms);
 #endif
@@ -388,6 +445,16 @@ cudaError_t run_dual(const TableDev& t, OpArgs a, int64_t n, int log2_buckets, W
 cudaError_t ws_reserve_dual(Workspace& ws, int64_t n, int log2_buckets) {
   cudaError_t e = cudaSuccess;
   const int64_t m = 2 * n;
+  const int64_t nb1 = (1ll << log2_buckets) + 1;
+  if (nb1 > ws.dbk) {
+    if (ws.dcnt) cudaFree(ws.dcnt);
+    if (ws.doff) cudaFree(ws.doff);
+    ws.dcnt = ws.doff = nullptr;
+    ws.dbk = 0;
+    if ((e = cudaMalloc((void**)&ws.dcnt, (size_t)nb1 * 4)) || (e = cudaMalloc((void**)&ws.doff, (size_t)nb1 * 4)))
+      return e;
+    ws.dbk = nb1;
+  }
   if (m > ws.dcap) {
     const int64_t c = m + m / 4 + 2048;
     uint32_t** arrs[] = {&ws.dpk, &ws.dpv, &ws.dsk, &ws.dsv, &ws.drank};
@@ -407,11 +474,21 @@ cudaError_t ws_reserve_dual(Workspace& ws, int64_t n, int log2_buckets) {
     ws.dcub_bytes = need;
     ws.dcap = c;
   }
+  // the counting-sort prep scans the per-bucket counters with the same temp storage
+  size_t b_bscan = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b_bscan, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)ws.dbk);
+  if (b_bscan > ws.dcub_bytes) {
+    if (ws.dcub) cudaFree(ws.dcub);
+    ws.dcub = nullptr;
+    ws.dcub_bytes = 0;
+    if ((e = cudaMalloc(&ws.dcub, b_bscan))) return e;
+    ws.dcub_bytes = b_bscan;
+  }
   return cudaSuccess;
 }
 
 void ws_free_dual(Workspace& ws) {
-  void* ptrs[] = {ws.dpk, ws.dpv, ws.dsk, ws.dsv, ws.drank, ws.dcub};
+  void* ptrs[] = {ws.dpk, ws.dpv, ws.dsk, ws.dsv, ws.drank, ws.dcub, ws.dcnt, ws.doff};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }

@@ -79,6 +79,9 @@ struct Workspace {
   uint32_t* dsk = nullptr;
   uint32_t* dsv = nullptr;
   uint32_t* drank = nullptr;
+  int64_t dbk = 0;             // dual: per-bucket counters / offsets of the rank prep (buckets + 1)
+  uint32_t* dcnt = nullptr;
+  uint32_t* doff = nullptr;
   void* dcub = nullptr;
   size_t dcub_bytes = 0;
   void* cub_tmp = nullptr;
