@@ -26,6 +26,8 @@
 // LOCKED state only guards the publish order.  Compiled with -dlcm=cg:
 // metadata another SM just published must not be served from a stale L1
 // line.
+#include <atomic>
+
 #include "hkv_kernels.h"
 #include "hkv_probe.cuh"
 
@@ -762,6 +764,12 @@ __global__ void __launch_bounds__(256, HKV_CAS_MINB) k_dual_rounds(TableDev t, O
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(t.size, (unsigned long long)v);
 }
 
+unsigned long long dev_bit() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return 1ull << (dev & 63);
+}
+
 }  // namespace
 
 cudaError_t run_cas(const TableDev& t, OpArgs a, int64_t n, unsigned* locks, int vec, cudaStream_t s,
@@ -770,11 +778,11 @@ cudaError_t run_cas(const TableDev& t, OpArgs a, int64_t n, unsigned* locks, int
   // input-row staging: 8 warps x 32 rows per block, up to 64 KB (dim <= 64)
   const int stage_dim = (vec == 4 && t.dim <= 64 && HKV_CAS_STAGE) ? t.dim : 0;
   const size_t smem = (size_t)8 * 32 * stage_dim * 4;
-  static bool attr_set = false;
-  if (smem && !attr_set) {
+  static std::atomic<unsigned long long> attr_set{0};  // the opt-in is per device
+  if (smem && !(attr_set.load() & dev_bit())) {
     for (void* f : {(void*)k_cas_upsert<4>, (void*)k_cas_upsert<2>, (void*)k_cas_upsert<1>})
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 32 * 64 * 4);
-    attr_set = true;
+    attr_set.fetch_or(dev_bit());
   }
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
@@ -798,11 +806,11 @@ cudaError_t run_dual_rounds(const TableDev& t, OpArgs a, int64_t n, const uint32
   void* fn = vec == 4 ? (void*)k_dual_rounds<4> : vec == 2 ? (void*)k_dual_rounds<2> : (void*)k_dual_rounds<1>;
   const int stage_dim = (vec == 4 && t.dim <= 64 && HKV_CAS_STAGE && a.op != kOpErase) ? t.dim : 0;
   const size_t smem = (size_t)8 * 32 * stage_dim * 4;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<unsigned long long> attr_set{0};  // the opt-in is per device
+  if (!(attr_set.load() & dev_bit())) {
     for (void* f : {(void*)k_dual_rounds<4>, (void*)k_dual_rounds<2>, (void*)k_dual_rounds<1>})
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 32 * 64 * 4);
-    attr_set = true;
+    attr_set.fetch_or(dev_bit());
   }
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
