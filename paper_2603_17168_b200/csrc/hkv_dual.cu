@@ -350,7 +350,19 @@ __global__ void k_drank(const uint32_t* __restrict__ b1s, const uint32_t* __rest
   const uint32_t b = (p & 1) ? b2 : b1;
   const uint32_t lo = off[b], hi = off[b + 1];
   uint32_t r = 0;
-  for (uint32_t q = lo; q < hi; q++) r += (list[q] >> 1) < i;
+  uint32_t q = lo;
+  if (hi - lo > 16) {
+    // a hot bucket (skewed batch): the warp's lanes mostly share the list,
+    // so read it through L1 four entries at a time.  The work stays
+    // quadratic in the bucket's reference count -- fine for zipf-skewed
+    // batches, slow (not wrong) for a batch of one repeated key.
+    for (; q < hi && (q & 3u); q++) r += (__ldg(list + q) >> 1) < i;
+    for (; q + 4 <= hi; q += 4) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(list + q));
+      r += ((v.x >> 1) < i) + ((v.y >> 1) < i) + ((v.z >> 1) < i) + ((v.w >> 1) < i);
+    }
+  }
+  for (; q < hi; q++) r += (list[q] >> 1) < i;
   rank[p] = r;
 }
 
